@@ -1,0 +1,418 @@
+/*
+ * bcgs_oracle.c -- CPU ORACLE for the preconditioned Bi-CGSTAB Poisson hot path of
+ * arXiv 2503.08935 ("A Parallel and Highly-Portable HPC Poisson Solver: Preconditioned
+ * Bi-CGSTAB with alpaka").
+ *
+ * THIS IS TEST INFRASTRUCTURE, NOT PRODUCT CODE.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load it.  It shares no code, header,
+ * constant table or helper with the CUDA library under paper_2503_08935_b200/; the two are
+ * written independently from the paper and from the arithmetic contract in DESIGN.md §3.
+ *
+ * Style: plain loops, one stencil sweep per pass, one vector operation per pass, fp64,
+ * compiled with -ffp-contract=off (no FMA contraction; fma() appears only in TwoProd, where
+ * it is exact by construction).  OpenMP is used only over z-planes of element-wise passes
+ * (order-independent) and for per-plane dot partials that are combined in ascending z.
+ *
+ * Citations: "P:n" = line n of the paper's LaTeX source.  Section / equation /
+ * algorithm numbers are given next to every citation.
+ *
+ * Layout (DESIGN.md §3 R14): unknown (i,j,k), 0-based, i fastest:  idx = i + nx*(j + ny*k).
+ * The grid has nx*ny*nz unknowns strictly inside the domain; all physical boundary ghosts
+ * are homogeneous Dirichlet zeros (Eq. 4); non-zero boundary data are folded into
+ * the right-hand side once (orc_fold_boundary).
+ *
+ * Parity status: every function below is pinned by tests/test_oracle_pins.py against values
+ * that do not come from this file (dense Kronecker assembly, closed-form spectra, closed-form
+ * Chebyshev polynomials, dense direct solves, manufactured solutions, exact summation,
+ * splitmix64's published test vector).  No function is "parity unpinned".
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#ifndef M_PI
+#define M_PI 3.14159265358979323846
+#endif
+
+#define IDX(i, j, k) ((i) + nx * ((j) + ny * (k)))
+
+/* ------------------------------------------------------------------------------------------
+ * Right-hand side: splitmix64 counter generator (DESIGN.md §3 R16).  Input generation, not
+ * part of the method; each side implements it independently.
+ * state = seed + (g+1)*0x9E3779B97F4A7C15, then the splitmix64 finaliser; u = (v>>11)*2^-53;
+ * b = 2u - 1 (exact).  g = global linear index.
+ * ---------------------------------------------------------------------------------------- */
+uint64_t orc_splitmix64(uint64_t seed, uint64_t g)
+{
+    uint64_t z = seed + (g + 1u) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+void orc_rhs_random(int64_t nx, int64_t ny, int64_t nz, uint64_t seed, double* b)
+{
+    int64_t n = nx * ny * nz;
+#pragma omp parallel for schedule(static)
+    for (int64_t g = 0; g < n; ++g) {
+        uint64_t v = orc_splitmix64(seed, (uint64_t)g);
+        double u = (double)(v >> 11) * 0x1.0p-53;
+        b[g] = 2.0 * u - 1.0;
+    }
+}
+
+/* Fold constant Dirichlet boundary values into the RHS (DESIGN.md §3 R15).  For the unknown
+ * next to face f the stencil row (Eq. 3) references one ghost whose value is g_f;
+ * moving it to the right-hand side adds g_f/h^2.  Faces: 0=x-,1=x+,2=y-,3=y+,4=z-,5=z+.
+ * Faces are folded in face order 0..5, each as b += g*h2inv. */
+void orc_fold_boundary(int64_t nx, int64_t ny, int64_t nz, double h, const double* g6, double* b)
+{
+    double h2inv = 1.0 / (h * h);
+    for (int f = 0; f < 6; ++f) {
+        double add = g6[f] * h2inv;
+        if (g6[f] == 0.0) continue;
+        for (int64_t k = 0; k < nz; ++k)
+            for (int64_t j = 0; j < ny; ++j)
+                for (int64_t i = 0; i < nx; ++i) {
+                    int on = (f == 0 && i == 0) || (f == 1 && i == nx - 1) ||
+                             (f == 2 && j == 0) || (f == 3 && j == ny - 1) ||
+                             (f == 4 && k == 0) || (f == 5 && k == nz - 1);
+                    if (on) b[IDX(i, j, k)] = b[IDX(i, j, k)] + add;
+                }
+    }
+}
+
+/* ------------------------------------------------------------------------------------------
+ * The operator.  P:95-100 (Eq. 6): P = I⊗I⊗D_x/Δx² + I⊗D_y/Δy²⊗I + D_z/Δz²⊗I⊗I with D from
+ * Eq. 4.  With uniform spacing h the row for unknown c reads
+ *     (A v)_c = (6 v_c - (((((v_xm + v_xp) + v_ym) + v_yp) + v_zm) + v_zp)) * h2inv,
+ * h2inv = 1/(h*h), out-of-domain neighbours = +0.0 (homogeneous Dirichlet).
+ * nslab > 1 gives the block-diagonal operator Σ_s R_s^T (R_s A R_s^T) R_s of Eq. 12-14
+ * (P:185-205): z is cut into nslab equal slabs and neighbours across a cut are also +0.0.
+ * nslab == 1 is the global operator (used by KernelBiCGS1/3).
+ * ---------------------------------------------------------------------------------------- */
+void orc_apply_A(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab,
+                 const double* v, double* out)
+{
+    double h2inv = 1.0 / (h * h);
+    int64_t L = nz / nslab;
+    int64_t pl = nx * ny;
+#pragma omp parallel for schedule(static)
+    for (int64_t k = 0; k < nz; ++k) {
+        int cut_lo = (k % L) == 0;          /* plane below is outside this block */
+        int cut_hi = (k % L) == L - 1;      /* plane above is outside this block */
+        for (int64_t j = 0; j < ny; ++j)
+            for (int64_t i = 0; i < nx; ++i) {
+                int64_t c = IDX(i, j, k);
+                double xm = (i > 0) ? v[c - 1] : 0.0;
+                double xp = (i < nx - 1) ? v[c + 1] : 0.0;
+                double ym = (j > 0) ? v[c - nx] : 0.0;
+                double yp = (j < ny - 1) ? v[c + nx] : 0.0;
+                double zm = cut_lo ? 0.0 : v[c - pl];
+                double zp = cut_hi ? 0.0 : v[c + pl];
+                double nb = ((((xm + xp) + ym) + yp) + zm) + zp;
+                out[c] = (6.0 * v[c] - nb) * h2inv;
+            }
+    }
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Dot products: Dot2 of Ogita, Rump & Oishi (compensated dot, DESIGN.md §3 R19).  The paper
+ * computes r~ᵀw, tᵀr, tᵀt, r0ᵀr, rᵀr (Alg. 3) and notes that
+ * reduction order changes results; Dot2 makes the result (almost always) the
+ * correctly rounded value, independent of order.
+ * Per z-plane: sequential Dot2 in index order -> pair (p_k, s_k).  Planes are combined in
+ * ascending z: (P, q) = TwoSum(P, p_k); S = S + (q + s_k).  Result fl(P + S).
+ * ---------------------------------------------------------------------------------------- */
+static inline void two_sum(double a, double b, double* s, double* e)
+{
+    double x = a + b;
+    double z = x - a;
+    *e = (a - (x - z)) + (b - z);
+    *s = x;
+}
+
+static inline void two_prod(double a, double b, double* p, double* e)
+{
+    double x = a * b;
+    *e = fma(a, b, -x);
+    *p = x;
+}
+
+/* Dot2 of n contiguous elements -> (hi, lo) pair, result = hi + lo */
+static void dot2_run(int64_t n, const double* a, const double* b, double* hi, double* lo)
+{
+    double p = 0.0, s = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        double h, r, q;
+        two_prod(a[i], b[i], &h, &r);
+        two_sum(p, h, &p, &q);
+        s = s + (q + r);
+    }
+    *hi = p;
+    *lo = s;
+}
+
+/* Dot over a field of nplanes planes of plen elements each. */
+double orc_dot(int64_t plen, int64_t nplanes, const double* a, const double* b)
+{
+    double* ph = (double*)malloc(sizeof(double) * (size_t)(nplanes > 0 ? nplanes : 1));
+    double* pl = (double*)malloc(sizeof(double) * (size_t)(nplanes > 0 ? nplanes : 1));
+#pragma omp parallel for schedule(static)
+    for (int64_t k = 0; k < nplanes; ++k)
+        dot2_run(plen, a + k * plen, b + k * plen, &ph[k], &pl[k]);
+    double P = 0.0, S = 0.0;
+    for (int64_t k = 0; k < nplanes; ++k) {
+        double q;
+        two_sum(P, ph[k], &P, &q);
+        S = S + (q + pl[k]);
+    }
+    free(ph);
+    free(pl);
+    return P + S;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Eigenvalue bounds.  Eq. 9: eigenvalues of D_n are 4 sin²(iπ/(2(n+1))).
+ * Eqs. 10-11: λmin/λmax of P = Σ_axes min/max μ / Δ².
+ *   mu(n, i)  = 4.0 * (s*s),  s = sin(((double)i * M_PI) / (2.0 * (double)(n + 1)))
+ *   lam       = ((mu_x * h2inv) + (mu_y * h2inv)) + (mu_z * h2inv)
+ * The local block R_s A R_s^T of a z-slab of L planes is the Dirichlet box nx*ny*L
+ * (Eq. 14, P:202 with zero ghosts at the cuts), so its bounds use L in place of nz.
+ * ---------------------------------------------------------------------------------------- */
+double orc_mu(int64_t n, int64_t i)
+{
+    double s = sin(((double)i * M_PI) / (2.0 * (double)(n + 1)));
+    return 4.0 * (s * s);
+}
+
+void orc_bounds(int64_t nx, int64_t ny, int64_t nzb, double h, double* lmin, double* lmax)
+{
+    double h2inv = 1.0 / (h * h);
+    *lmin = ((orc_mu(nx, 1) * h2inv) + (orc_mu(ny, 1) * h2inv)) + (orc_mu(nzb, 1) * h2inv);
+    *lmax = ((orc_mu(nx, nx) * h2inv) + (orc_mu(ny, ny) * h2inv)) + (orc_mu(nzb, nzb) * h2inv);
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Chebyshev iteration, Alg. 2 as implemented in Alg. 4.
+ * Interval [a, b] (Eq. 15): θ = (b+a)/2, δ = (b-a)/2, σ = θ/δ.
+ * ρ_0 = 1/σ; ρ_j = 1/(2σ - ρ_{j-1}) (the garbled "1/2σ - ρ_old" of
+ * Alg. 4 line 2, is read as Alg. 2's 1/(2σ - ρ_old): DESIGN.md §3 R2).
+ * Host constants: cz = 1/θ, g1 = 2*(ρ_1/δ), A2 = 2*σ, B2 = 2/δ (DESIGN.md §3 R18).
+ * iterMax = k (DESIGN.md §3 R1): k = 0 returns z = b/θ; k = 1 returns y;
+ * k >= 2 runs the loop of P:224-230 and returns w.
+ * The stencil inside is the block operator (nslab cuts): GNoComm / BJ.
+ * ---------------------------------------------------------------------------------------- */
+#define ORC_KMAX 256
+
+typedef struct {
+    double theta, delta, sigma, cz, g1, A2, B2;
+    double rho[ORC_KMAX + 2];
+} orc_cheb;
+
+int orc_cheb_setup(double a, double b, int k, double* out7, double* rho_out)
+{
+    orc_cheb c;
+    if (k < 0 || k > ORC_KMAX) return 1;
+    c.theta = (b + a) / 2.0;
+    c.delta = (b - a) / 2.0;
+    if (!(c.delta > 0.0) || !(a > 0.0)) return 2;
+    c.sigma = c.theta / c.delta;
+    c.rho[0] = 1.0 / c.sigma;
+    for (int j = 1; j <= (k > 1 ? k : 1); ++j) c.rho[j] = 1.0 / (2.0 * c.sigma - c.rho[j - 1]);
+    c.cz = 1.0 / c.theta;
+    c.g1 = 2.0 * (c.rho[1] / c.delta);
+    c.A2 = 2.0 * c.sigma;
+    c.B2 = 2.0 / c.delta;
+    if (out7) {
+        out7[0] = c.theta; out7[1] = c.delta; out7[2] = c.sigma; out7[3] = c.cz;
+        out7[4] = c.g1; out7[5] = c.A2; out7[6] = c.B2;
+    }
+    if (rho_out)
+        for (int j = 0; j <= (k > 1 ? k : 1); ++j) rho_out[j] = c.rho[j];
+    return 0;
+}
+
+int orc_apply_cheb(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, int k,
+                   double a, double b, const double* q, double* out)
+{
+    double cst[7], rho[ORC_KMAX + 2];
+    int rc = orc_cheb_setup(a, b, k, cst, rho);
+    if (rc) return rc;
+    double cz = cst[3], g1 = cst[4], A2 = cst[5], B2 = cst[6];
+    int64_t n = nx * ny * nz;
+
+    if (k == 0) {                                   /* z = b/θ; iterMax = 0 exits here */
+        for (int64_t c = 0; c < n; ++c) out[c] = q[c] * cz;
+        return 0;
+    }
+    double* S = (double*)malloc(sizeof(double) * (size_t)n);
+    double* y = (double*)malloc(sizeof(double) * (size_t)n);
+    double* z = (double*)malloc(sizeof(double) * (size_t)n);
+    double* w = (double*)malloc(sizeof(double) * (size_t)n);
+
+    /* KernelCI1: z = b/θ ; y = 2(ρ_cur/δ)(2b - A b/θ) */
+    orc_apply_A(nx, ny, nz, h, nslab, q, S);
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < n; ++c) {
+        z[c] = q[c] * cz;
+        y[c] = g1 * ((2.0 * q[c]) - (S[c] * cz));
+    }
+    /* KernelCI2 for i = 2..iterMax, with the pointer swaps of P:361-362 */
+    for (int j = 2; j <= k; ++j) {
+        orc_apply_A(nx, ny, nz, h, nslab, y, S);
+        double rc_ = rho[j], ro_ = rho[j - 1];
+#pragma omp parallel for schedule(static)
+        for (int64_t c = 0; c < n; ++c)
+            w[c] = rc_ * (((A2 * y[c]) + (B2 * (q[c] - S[c]))) - (ro_ * z[c]));
+        double* tmp = z; z = y; y = w; w = tmp;   /* z <- y, y <- w */
+    }
+    /* KernelCI3: x = w (after the swap, the last w is in y) */
+    memcpy(out, y, sizeof(double) * (size_t)n);
+    free(S); free(y); free(z); free(w);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Preconditioned Bi-CGSTAB, Alg. 3, Alg. 1 for the scalar forms.
+ *
+ * pc: 0 = none (M = I), 1 = GNoComm(CI), 2 = BJ(CI).
+ * nslab = number of z-slabs of the decomposition (ranks x blocks per rank): the
+ * preconditioner acts on each slab separately (Eq. 13); the global stencils of
+ * KernelBiCGS1/3 ignore the cuts (halo exchange MPI1/MPI3).
+ * Bounds: GNoComm uses the global Eq. 9-11 bounds rescaled by (c_min, c_max);
+ * BJ uses the exact bounds of the local Dirichlet block, unscaled (DESIGN.md §3 R10).
+ * lmin_ov/lmax_ov > 0 override the interval [a', b'] directly.
+ *
+ * Stopping rule (DESIGN.md §3 R4): rel_i = sqrt(rᵀr)/||b|| < tol.  fixed_it > 0 runs exactly
+ * fixed_it iterations (tol ignored).  Breakdown (R7): r~ᵀw == 0 or non-finite -> stop before
+ * any update in that iteration; after the residual update, ω == 0, ρ_new == 0 or any
+ * non-finite scalar -> stop.  tᵀt == 0 -> ω = 0 (R6).
+ *
+ * Outputs: x (solution), hist[0..iters] (hist[0] = 1), scal[8*(i-1) + ...] per iteration =
+ * {rw, alpha, ts, tt, omega, rho_new, rr, beta}.  Returns status:
+ *   0 converged / fixed iterations done, 6 not converged (max_it), 7 breakdown, 1 bad config.
+ * *iters_out = number of completed iterations (each appended one entry to hist); a
+ * breakdown at r~ᵀw ends the run before iteration i appends anything (iters = i-1).
+ * ---------------------------------------------------------------------------------------- */
+int orc_bicgstab(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, int pc, int k,
+                 double c_min, double c_max, double lmin_ov, double lmax_ov,
+                 const double* b, const double* x0, double tol, int max_it, int fixed_it,
+                 double* x, double* hist, double* scal, int* iters_out, double* true_rel)
+{
+    int64_t n = nx * ny * nz, pl = nx * ny;
+    if (nslab < 1 || nz % nslab != 0) return 1;
+    double a_iv = 0.0, b_iv = 0.0;
+    if (pc == 1 || pc == 2) {
+        if (lmin_ov > 0.0 && lmax_ov > 0.0) {
+            a_iv = lmin_ov; b_iv = lmax_ov;
+        } else if (pc == 1) {
+            double lmn, lmx;
+            orc_bounds(nx, ny, nz, h, &lmn, &lmx);
+            a_iv = c_min * lmn;
+            b_iv = c_max * lmx;
+        } else {
+            orc_bounds(nx, ny, nz / nslab, h, &a_iv, &b_iv);
+        }
+        if (!(a_iv < b_iv) || !(a_iv > 0.0)) return 1;
+    } else if (pc != 0) {
+        return 1;
+    }
+    int max_run = fixed_it > 0 ? fixed_it : max_it;
+
+    double* r = (double*)calloc((size_t)n, sizeof(double));
+    double* rt = (double*)calloc((size_t)n, sizeof(double));
+    double* p = (double*)calloc((size_t)n, sizeof(double));
+    double* ph = (double*)calloc((size_t)n, sizeof(double));
+    double* rh = (double*)calloc((size_t)n, sizeof(double));
+    double* w = (double*)calloc((size_t)n, sizeof(double));
+    double* t = (double*)calloc((size_t)n, sizeof(double));
+    double* tmp = (double*)calloc((size_t)n, sizeof(double));
+
+    /* Alg. 3 line 1: r0 = b - A x0 */
+    if (x0) {
+        memcpy(x, x0, sizeof(double) * (size_t)n);
+        orc_apply_A(nx, ny, nz, h, 1, x, tmp);
+        for (int64_t c = 0; c < n; ++c) r[c] = b[c] - tmp[c];
+    } else {
+        memset(x, 0, sizeof(double) * (size_t)n);
+        memcpy(r, b, sizeof(double) * (size_t)n);
+    }
+    /* line 2-4: r~ = r0, p0 = r0, ρ0 = r~ᵀ r0 */
+    memcpy(rt, r, sizeof(double) * (size_t)n);
+    memcpy(p, r, sizeof(double) * (size_t)n);
+    double rho = orc_dot(pl, nz, rt, r);
+    double nb = sqrt(orc_dot(pl, nz, b, b));     /* ||b||: relative tolerance */
+    hist[0] = 1.0;
+    int status = 6, it = 0;
+    if (nb == 0.0) {          /* b = 0: x = x0 is exact only if x0 = 0; report converged */
+        status = 0;
+        goto done;
+    }
+    for (int i = 1; i <= max_run; ++i) {
+        it = i;
+        double* sc = scal ? scal + 8 * (i - 1) : NULL;
+        /* line 6: solve M p̂ = p */
+        if (pc == 0) memcpy(ph, p, sizeof(double) * (size_t)n);
+        else orc_apply_cheb(nx, ny, nz, h, nslab, k, a_iv, b_iv, p, ph);
+        /* MPI1 + KernelBiCGS1: w = A p̂ (global), local r~ᵀw; MPI2 */
+        orc_apply_A(nx, ny, nz, h, 1, ph, w);
+        double rw = orc_dot(pl, nz, rt, w);
+        if (sc) sc[0] = rw;
+        if (rw == 0.0 || !isfinite(rw)) { status = 7; it = i - 1; break; }
+        double alpha = rho / rw;
+        if (sc) sc[1] = alpha;
+        /* KernelBiCGS2: r = r - α w   (the half-step residual, "s") */
+#pragma omp parallel for schedule(static)
+        for (int64_t c = 0; c < n; ++c) r[c] = r[c] - alpha * w[c];
+        /* solve M r̂ = r */
+        if (pc == 0) memcpy(rh, r, sizeof(double) * (size_t)n);
+        else orc_apply_cheb(nx, ny, nz, h, nslab, k, a_iv, b_iv, r, rh);
+        /* MPI3 + KernelBiCGS3: t = A r̂, tᵀr, tᵀt; MPI4 */
+        orc_apply_A(nx, ny, nz, h, 1, rh, t);
+        double ts = orc_dot(pl, nz, t, r);
+        double tt = orc_dot(pl, nz, t, t);
+        double omega = (tt == 0.0) ? 0.0 : ts / tt;  /* P:293, guard R6 */
+        if (sc) { sc[2] = ts; sc[3] = tt; sc[4] = omega; }
+        /* KernelBiCGS4: x = x + α p̂ + ω r̂ */
+#pragma omp parallel for schedule(static)
+        for (int64_t c = 0; c < n; ++c) x[c] = (x[c] + alpha * ph[c]) + omega * rh[c];
+        /* KernelBiCGS5: r = r - ω t, r0ᵀr, rᵀr; MPI5 */
+#pragma omp parallel for schedule(static)
+        for (int64_t c = 0; c < n; ++c) r[c] = r[c] - omega * t[c];
+        double rho_new = orc_dot(pl, nz, rt, r);
+        double rr = orc_dot(pl, nz, r, r);
+        double rel = sqrt(rr) / nb;
+        hist[i] = rel;
+        if (sc) { sc[5] = rho_new; sc[6] = rr; sc[7] = 0.0; }
+        /* P:300-302 stopping test */
+        if (fixed_it > 0) {
+            if (i == fixed_it) { status = 0; break; }
+        } else if (rel < tol) {
+            status = 0;
+            break;
+        }
+        if (omega == 0.0 || rho_new == 0.0 || !isfinite(rho_new) || !isfinite(rr) ||
+            !isfinite(omega)) {
+            status = 7;
+            break;
+        }
+        /* ρ_i, β_i  (Alg. 1 form: β = (ρ_i/ρ_{i-1})(α/ω); R20) */
+        double beta = (rho_new / rho) * (alpha / omega);
+        rho = rho_new;
+        if (sc) sc[7] = beta;
+        /* KernelBiCGS6: p = r + β (p - ω w) */
+#pragma omp parallel for schedule(static)
+        for (int64_t c = 0; c < n; ++c) p[c] = r[c] + beta * (p[c] - omega * w[c]);
+    }
+done:
+    *iters_out = it;
+    if (true_rel) {
+        orc_apply_A(nx, ny, nz, h, 1, x, tmp);
+        for (int64_t c = 0; c < n; ++c) tmp[c] = b[c] - tmp[c];
+        *true_rel = nb == 0.0 ? 0.0 : sqrt(orc_dot(pl, nz, tmp, tmp)) / nb;
+    }
+    free(r); free(rt); free(p); free(ph); free(rh); free(w); free(t); free(tmp);
+    return status;
+}
