@@ -1,0 +1,315 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200-native preconditioned Bi-CGSTAB hot path (arXiv 2503.08935).
+
+Metric (BASELINE.json): fp64 Bi-CGSTAB iters/s & GDoF/s at 512³, % of HBM roofline.
+A "step" = one outer iteration of Alg. 3 (all §8(a) rows a2-a14) on the 512³ grid
+(config C3: GNoComm(CI) k = 4, slab decomposition over N GPUs, strong scaling).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 Bi-CGSTAB iters/s & GDoF/s at 512^3; % of HBM roofline"
+ALG_BYTES_PER_PT = 200.0   # compulsory bytes per point per outer iteration
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--pc", default="gnocomm", choices=["gnocomm", "bj", "none"])
+    ap.add_argument("--degree", type=int, default=4)
+    ap.add_argument("--kernels", type=int, default=1, help="0 = reference kernels, 1 = fused")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms while running."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 8:
+                for nm, v in zip(names, r[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(n, pc, k, seed):
+    """The oracle as it stands, on this host's cores, on a bounded sample of the workload:
+    one outer iteration of the same 512³ problem (fixed_it = 1; includes the setup dots,
+    copies and the final true-residual stencil)."""
+    import oracle
+    import synth_inputs as si
+    h = si.unit_cube_h(n)
+    b = oracle.rhs_random((n, n, n), seed)
+    t0 = time.perf_counter()
+    oracle.bicgstab(b, h, pc=pc, k=k, fixed_it=1)
+    dt = time.perf_counter() - t0
+    return {"value": 1.0 / dt, "unit": "iters/s", "cores": oracle.threads(), "kind": "oracle",
+            "sample": f"1 outer iteration of {n}^3 {pc} k={k} (incl. setup + true residual), "
+                      f"{dt:.2f} s"}
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the oracle as it stands on host cores.  Each step is a bounded
+    sample: one oracle outer iteration on a 512x512xLs z-slab sub-problem; iters/s is scaled
+    to the full 512³ grid by the point ratio (work per point is the same)."""
+    if rank != 0:
+        return
+    import oracle
+    import synth_inputs as si
+    n = args.n
+    ls = 8
+    h = si.unit_cube_h(n)
+    b = si.rhs_random(n, n, n, si.SEED, z0=0, nzl=ls)
+    for _ in range(args.warmup):
+        oracle.bicgstab(b, h, pc=args.pc, k=args.degree, fixed_it=1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.bicgstab(b, h, pc=args.pc, k=args.degree, fixed_it=1)
+    dt = (time.perf_counter() - t0) / max(args.steps, 1)
+    scale = n / ls
+    v = 1.0 / (dt * scale)
+    sample = (f"1 oracle outer iteration per step on a {n}x{n}x{ls} slab of the {n}^3 "
+              f"problem, scaled x{scale:g} to {n}^3")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "iters/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt * scale * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C3 {n}^3 {args.pc} k={args.degree}", "grid": n,
+                       "preconditioner": args.pc, "degree": args.degree},
+            "gdof_s": n ** 3 * v / 1e9,
+            "cpu_baseline": {"value": v, "unit": "iters/s", "cores": oracle.threads(),
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import synth_inputs as si
+    from paper_2503_08935_b200 import bcgs
+
+    assert world == args.gpus, f"WORLD_SIZE {world} != --gpus {args.gpus}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    nccl_id = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(bcgs.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().numpy().tobytes())
+
+    n, k = args.n, args.degree
+    h = si.unit_cube_h(n)
+    s = bcgs.Solver(n, h, rank=rank, nranks=world, nccl_id=nccl_id, device=local)
+    s.set_option(bcgs.OPT_KERNELS, args.kernels)
+    s.set_preconditioner(args.pc, k)
+    s.set_rhs_random(si.SEED)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    total = args.warmup + args.steps
+    clocks = ClockSampler(local)
+    clocks.start()
+    s.begin(fixed_iters=total)
+    s.iterate(args.warmup)
+    barrier()
+    s.set_option(bcgs.OPT_PROFILE, 1)
+    s.kernel_times_reset()
+    stream = torch.cuda.current_stream(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    s.iterate(args.steps)           # enqueued on the library stream, joined below
+    rep = s.finish()                # waits; joins the library stream into `stream`
+    e1.record(stream)
+    barrier()
+    ms_total = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    ktimes = s.kernel_times()
+    s.set_option(bcgs.OPT_PROFILE, 0)
+    # finish() also ran one true-residual check (1 stencil + 1 dot) inside the region:
+    # time it separately and subtract, so ms_per_step is the iterations only.
+    tr0 = torch.cuda.Event(enable_timing=True)
+    tr1 = torch.cuda.Event(enable_timing=True)
+    tr0.record(stream)
+    s.finish()
+    tr1.record(stream)
+    torch.cuda.synchronize()
+    ms_iter = max(ms_total - tr0.elapsed_time(tr1), 1e-6) / args.steps
+    if world > 1:
+        t = torch.tensor([ms_iter], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_iter = float(t.item())
+
+    its = 1000.0 / ms_iter
+    gdof = n ** 3 * its / 1e9
+    peak, peak_src = peaks()
+    pts_local = n * n * (n // world)
+    iter_gbs = ALG_BYTES_PER_PT * pts_local / (ms_iter * 1e-3) / 1e9
+
+    # dominant kernel of the timed region (largest total device time)
+    ours = {kname: v for kname, v in ktimes.items() if kname not in ("halo", "allgather")}
+    dom_name = max(ours, key=lambda kk: ours[kk]["ms"]) if ours else None
+    roof = None
+    if dom_name:
+        d = ours[dom_name]
+        per_launch_ms = d["ms"] / d["calls"]
+        achieved = d["bytes_per_call"] / (per_launch_ms * 1e-3) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                tr = json.load(f)
+            traffic = tr.get(f"{dom_name}@{n}")
+        except Exception:
+            pass
+        roof = {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_source": peak_src,
+                "share_of_step": d["ms"] / (ms_iter * args.steps)}
+    launches = sum(v["calls"] for kname, v in ktimes.items() if kname not in ("halo", "allgather"))
+
+    # e2e through the public API with host buffers: set_rhs(host) + solve(K) + x -> host
+    e2e = None
+    if not args.no_e2e:
+        f_host = torch.from_numpy(si.rhs_random(n, n, n, si.SEED, z0=rank * (n // world),
+                                                nzl=n // world)).pin_memory()
+        x_host = torch.empty_like(f_host).pin_memory()
+        barrier()
+        t0 = time.perf_counter()
+        s.set_rhs(f_host)
+        s.solve(fixed_iters=args.steps)
+        s.lib.bcgs_get_solution(s.ctx, x_host.data_ptr(), bcgs.MEM_HOST)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": args.steps / dt, "unit": "iters/s",
+               "h2d_bytes_per_step": f_host.numel() * 8 / args.steps,
+               "d2h_bytes_per_step": x_host.numel() * 8 / args.steps,
+               "note": "set_rhs(host pinned) + solve(fixed K) + get_solution(host); per-step "
+                       "bytes = one RHS in and one solution out amortised over K"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(n, args.pc, k, si.SEED)
+        except Exception as ex:  # report, do not fail the bench
+            cpu = {"error": repr(ex)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": its, "unit": "iters/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_iter,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C3 {n}^3 GNoComm(CI) k={k}" if args.pc == "gnocomm"
+                       else f"{n}^3 {args.pc} k={k}",
+                       "grid": n, "preconditioner": args.pc, "degree": k,
+                       "c_min": 10.0, "c_max": 1 - 1e-4, "decomposition": f"z-slab x{world}",
+                       "kernels": "fused" if args.kernels else "reference",
+                       "l2": "inputs larger than L2 (each field 8*N^3/P bytes >> 126 MB)",
+                       "rhs": "splitmix64 uniform[-1,1), seed 20250311"},
+            "gdof_s": gdof,
+            "iteration_roofline": {"alg_bytes_per_pt": ALG_BYTES_PER_PT,
+                                   "achieved_gbs": iter_gbs, "peak_gbs": peak,
+                                   "frac": iter_gbs / peak},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "kernel_ms_per_step": {kk: v["ms"] / args.steps for kk, v in ktimes.items()},
+            "clocks": clk, "report": {kk: rep[kk] for kk in ("iterations", "rel_residual",
+                                                             "true_rel_residual")},
+        }
+        print(json.dumps(line), flush=True)
+    s.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,185 @@
+/*
+ * bcgs.h -- C ABI of the B200-native preconditioned Bi-CGSTAB Poisson hot path
+ * (arXiv 2503.08935, "A Parallel and Highly-Portable HPC Poisson Solver: Preconditioned
+ * Bi-CGSTAB with alpaka").  Implemented by paper_2503_08935_b200/lib/libbcgs.so.
+ *
+ * Citations: P:n = line n of the paper's LaTeX source, with the equation /
+ * algorithm it falls in.  R-numbers refer to the arithmetic contract in DESIGN.md §3.
+ *
+ * Problem (Eq. 1-6): -Δφ = f on a box of nx*ny*nz unknowns with uniform spacing
+ * h and homogeneous Dirichlet ghosts; constant Dirichlet face values are folded into the
+ * right-hand side (R15).  Matrix-free 7-point operator A (Eq. 6).
+ *
+ * Decomposition: the z axis is split into `nranks` equal slabs, one per process
+ * (one GPU each); rank r owns global planes [r*L, (r+1)*L), L = nz/nranks.  Each slab may
+ * further be split into `blocks_per_rank` preconditioner blocks (single-GPU emulation of a
+ * larger slab count; the preconditioner acts on nranks*blocks_per_rank z-slabs).
+ *
+ * Data layout of every field argument: this rank's slab, fp64, x fastest then y then z,
+ * nx*ny*L contiguous values (no ghost planes, no padding).  `mem` says whether a pointer
+ * is host (BCGS_MEM_HOST, pageable or pinned) or device (BCGS_MEM_DEVICE) memory.
+ *
+ * Ownership: the caller owns the device workspace (bcgs_workspace_bytes) and the CUDA
+ * stream passed to bcgs_create; both must outlive the context.  The library never frees
+ * caller memory; inputs are copied in, results copied out.  The context owns its private
+ * CUDA stream, events, graphs and (nranks > 1) NCCL communicator.
+ *
+ * Streams: set_* / get_* / apply_* calls are ordered after prior work on the caller's
+ * stream and the caller's stream is ordered after them (event joins); host-memory
+ * variants synchronise the host.  bcgs_solve returns after the solve ends.
+ *
+ * Errors: every call returns a bcgs_status; bcgs_last_error gives a one-line diagnostic.
+ * Configuration errors are detected before any device work.  Breakdown and non-convergence
+ * are reported as statuses with the report filled, never as crashes.
+ *
+ * Collective semantics (nranks > 1): every rank calls create, set_*, solve, dot, apply_*
+ * in the same order (bulk synchronous); scalars and the residual history are identical
+ * on every rank.  A context is not thread-safe.
+ */
+#ifndef BCGS_H
+#define BCGS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BCGS_ABI_VERSION 1
+#define BCGS_MAX_DEGREE 64       /* Chebyshev degree k (sweeps per application) cap      */
+#define BCGS_HIST_CAP 16384      /* max outer iterations recorded per solve              */
+
+typedef struct bcgs_ctx_s* bcgs_ctx;
+
+typedef enum {
+    BCGS_OK = 0,
+    BCGS_E_INVALID = 1,       /* bad argument (null pointer, out-of-range value)          */
+    BCGS_E_CONFIG = 2,        /* inconsistent configuration (e.g. nz % nranks != 0)        */
+    BCGS_E_SPECTRUM = 3,      /* empty / non-positive Chebyshev interval                  */
+    BCGS_E_CUDA = 4,          /* CUDA runtime error (message in bcgs_last_error)          */
+    BCGS_E_NCCL = 5,          /* NCCL error                                               */
+    BCGS_NOT_CONVERGED = 6,   /* max_iter reached without rel residual < tol (R23)        */
+    BCGS_BREAKDOWN = 7,       /* exact zero / non-finite r~ᵀw, ω or ρ (R7)                */
+    BCGS_E_STATE = 8          /* call out of order (e.g. iterate before begin)            */
+} bcgs_status;
+
+/* Preconditioner M of Alg. 3 l.6/12; Table I. */
+typedef enum {
+    BCGS_PC_NONE = 0,          /* M = I: plain Bi-CGSTAB (Alg. 1)               */
+    BCGS_PC_CHEB_GNOCOMM = 1,  /* GNoComm(CI): Chebyshev on each slab block with   */
+                               /* the global Eq. 9-11 bounds rescaled by (c_min, c_max)    */
+    BCGS_PC_CHEB_BJ = 2        /* BJ(CI): Chebyshev on each slab block with the    */
+                               /* exact local-block bounds (R10)                           */
+} bcgs_pc;
+
+typedef enum { BCGS_MEM_DEVICE = 0, BCGS_MEM_HOST = 1 } bcgs_mem;
+
+/* Implementation switches (bcgs_set_option). */
+typedef enum {
+    BCGS_OPT_KERNELS = 0,      /* 0 = reference kernels (one sweep per launch, one op per */
+                               /*     launch); 1 = fused / temporally blocked (default)   */
+    BCGS_OPT_GRAPH = 1,        /* 1 = replay iterations from a captured CUDA graph        */
+    BCGS_OPT_PROFILE = 2,      /* 1 = CUDA events around every kernel (bcgs_kernel_times) */
+    BCGS_OPT_POLL = 3          /* iterations launched between done-flag polls (tol mode)  */
+} bcgs_option;
+
+typedef struct {
+    int64_t n[3];   /* global unknowns along x, y, z (each >= 1)                          */
+    double h;       /* uniform grid spacing (> 0); unit cube: h = 1/(n+1)                  */
+} bcgs_grid_desc;
+
+typedef struct {
+    int32_t status;            /* bcgs_status of the solve                                 */
+    int32_t converged;         /* 1 if rel_residual < tol (or fixed iterations completed)  */
+    int32_t iterations;        /* completed outer iterations                               */
+    int32_t degree_warning;    /* 1 if k > L_block/2 (R24)                           */
+    double rel_residual;       /* recurrence residual sqrt(rᵀr)/||b|| of the last iteration */
+    double true_rel_residual;  /* ||b - A x|| / ||b|| computed once at the end (R22)       */
+    double seconds;            /* wall time of the solve                                   */
+} bcgs_report;
+
+int32_t bcgs_abi_version(void);
+const char* bcgs_status_string(bcgs_status s);
+
+/* Device workspace the caller must provide to bcgs_create for this grid and rank count. */
+size_t bcgs_workspace_bytes(const bcgs_grid_desc* grid, int32_t nranks);
+
+/* Chebyshev interval and constants for a configuration, computed on the host exactly as
+ * the solver computes them (Eq. 9-11, Eq. 15, Alg. 2, R9,
+ * R10, R18).  out7 = {θ, δ, σ, 1/θ, 2ρ₁/δ, 2σ, 2/δ}; rho = ρ_0..ρ_k (k+1 values, at least
+ * 2).  Host-only; no GPU needed.  nslab = nranks*blocks_per_rank. */
+bcgs_status bcgs_chebyshev_constants(const bcgs_grid_desc* grid, int32_t nslab, bcgs_pc pc,
+                                     int32_t degree, double c_min, double c_max,
+                                     double* interval2, double* out7, double* rho);
+
+/* 128-byte NCCL unique id for a new communicator (call on rank 0 only; broadcast it). */
+bcgs_status bcgs_nccl_unique_id(void* out128);
+
+/* Create a context.  nccl_unique_id: 128-byte ncclUniqueId from rank 0 (broadcast by the
+ * caller), NULL iff nranks == 1.  cuda_stream: caller's cudaStream_t (may be 0).
+ * d_workspace: >= bcgs_workspace_bytes device bytes, 256-byte aligned. */
+bcgs_status bcgs_create(const bcgs_grid_desc* grid, int32_t rank, int32_t nranks,
+                        const void* nccl_unique_id, int32_t cuda_device, void* d_workspace,
+                        size_t ws_bytes, void* cuda_stream, bcgs_ctx* out);
+void bcgs_destroy(bcgs_ctx ctx);
+const char* bcgs_last_error(bcgs_ctx ctx);
+bcgs_status bcgs_set_option(bcgs_ctx ctx, int32_t option, int64_t value);
+
+/* Right-hand side b (Eq. 1; Alg. 3 l.1).  Random: R16, generated on the device from
+ * the global index (identical bits for any rank count).  bcgs_set_rhs copies this rank's
+ * slab.  Face values (R15): face 0..5 = x-,x+,y-,y+,z-,z+; the values set are folded
+ * into b by every subsequent set_rhs* call (R15). */
+bcgs_status bcgs_set_rhs_random(bcgs_ctx ctx, uint64_t seed);
+bcgs_status bcgs_set_rhs(bcgs_ctx ctx, const double* f, int32_t mem);
+bcgs_status bcgs_set_boundary_value(bcgs_ctx ctx, int32_t face, double value);
+/* Initial guess x0 (Alg. 3 l.1); NULL -> 0 (R21). */
+bcgs_status bcgs_set_initial_guess(bcgs_ctx ctx, const double* x0, int32_t mem);
+
+/* Preconditioner: kind, degree k (R1, 0..BCGS_MAX_DEGREE), rescaling (c_min, c_max) for
+ * GNoComm (R9), blocks_per_rank >= 1 with L % blocks_per_rank == 0. */
+bcgs_status bcgs_set_preconditioner(bcgs_ctx ctx, bcgs_pc pc, int32_t degree, double c_min,
+                                    double c_max, int32_t blocks_per_rank);
+/* Override the Chebyshev interval [a', b'] (0 < a' < b'); (0, 0) restores the default. */
+bcgs_status bcgs_set_eigen_bounds(bcgs_ctx ctx, double a, double b);
+
+/* Solve A x = b with Alg. 3.  fixed_iters > 0: run exactly that many iterations
+ * (tol ignored); else stop when rel < rel_tol (R4) or after max_iter (<= BCGS_HIST_CAP). */
+bcgs_status bcgs_solve(bcgs_ctx ctx, double rel_tol, int32_t max_iter, int32_t fixed_iters,
+                       bcgs_report* out);
+
+/* Split form of bcgs_solve for timing: begin = Alg. 3 l.1-4 (setup, row a1); iterate
+ * enqueues n more outer iterations (rows a2-a14) on the stream and returns without host
+ * synchronisation (fixed-iteration semantics); finish waits and fills the report. */
+bcgs_status bcgs_begin(bcgs_ctx ctx, double rel_tol, int32_t max_iter, int32_t fixed_iters);
+bcgs_status bcgs_iterate(bcgs_ctx ctx, int32_t n);
+bcgs_status bcgs_finish(bcgs_ctx ctx, bcgs_report* out);
+
+/* Residual history rel_0..rel_iters (rel_0 = 1); returns the count copied. */
+int32_t bcgs_residual_history(bcgs_ctx ctx, double* host_out, int32_t cap);
+/* Per-iteration scalars, 8 per iteration: r~ᵀw, α, tᵀs, tᵀt, ω, ρ_new, rᵀr, β. */
+int32_t bcgs_scalar_history(bcgs_ctx ctx, double* host_out, int32_t cap_iters);
+/* Solution x (this rank's slab). */
+bcgs_status bcgs_get_solution(bcgs_ctx ctx, double* x, int32_t mem);
+
+/* Single steps of the path on device slabs, for parity tests and micro-benchmarks.
+ * apply_operator: out = A in (global operator with halo exchange; block_local != 0 gives
+ * the block-diagonal slab operator of Eq. 12-14).  apply_preconditioner: out = M^-1 in
+ * with the configured preconditioner.  dot: global Dot2 (R19) -> *host_out. */
+bcgs_status bcgs_apply_operator(bcgs_ctx ctx, const double* d_in, double* d_out,
+                                int32_t block_local);
+bcgs_status bcgs_apply_preconditioner(bcgs_ctx ctx, const double* d_in, double* d_out);
+bcgs_status bcgs_dot(bcgs_ctx ctx, const double* d_a, const double* d_b, double* host_out);
+
+/* Kernel timings accumulated while BCGS_OPT_PROFILE = 1 (CUDA events on the launching
+ * stream).  Returns the number of kernel classes; names are '\n'-separated in names_out.
+ * ms_out[i] = total milliseconds, calls_out[i] = launches; bytes_out[i] = algorithmic
+ * bytes per launch of class i. */
+int32_t bcgs_kernel_times(bcgs_ctx ctx, char* names_out, int32_t names_cap, double* ms_out,
+                          int64_t* calls_out, double* bytes_out, int32_t cap);
+void bcgs_kernel_times_reset(bcgs_ctx ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BCGS_H */

@@ -45,6 +45,7 @@ def lib() -> ctypes.CDLL:
     if _lib is None:
         _lib = ctypes.CDLL(build())
         i64, f64, P = ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
+        _lib.orc_threads.restype = ctypes.c_int
         _lib.orc_splitmix64.restype = ctypes.c_uint64
         _lib.orc_splitmix64.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
         _lib.orc_rhs_random.argtypes = [i64, i64, i64, ctypes.c_uint64, P]
@@ -77,6 +78,10 @@ def _shape(shape):
 
 
 # Problem arrays are numpy arrays of shape (nz, ny, nx) (x fastest), fp64.
+
+def threads() -> int:
+    return int(lib().orc_threads())
+
 
 def splitmix64(seed: int, g: int) -> int:
     return int(lib().orc_splitmix64(seed, g))

@@ -30,6 +30,9 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 #ifndef M_PI
 #define M_PI 3.14159265358979323846
@@ -344,9 +347,16 @@ int orc_bicgstab(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, in
     memcpy(p, r, sizeof(double) * (size_t)n);
     double rho = orc_dot(pl, nz, rt, r);
     double nb = sqrt(orc_dot(pl, nz, b, b));     /* ||b||: relative tolerance */
-    hist[0] = 1.0;
     int status = 6, it = 0;
-    if (nb == 0.0) {          /* b = 0: x = x0 is exact only if x0 = 0; report converged */
+    if (nb == 0.0) {          /* b = 0: report converged with x = x0 (R26) */
+        hist[0] = 0.0;
+        status = 0;
+        goto done;
+    }
+    /* R26: rel_0 = sqrt(r~ᵀr0)/||b|| (= 1 for x0 = 0); a converged initial guess stops
+     * before the first iteration (tol mode). */
+    hist[0] = sqrt(rho) / nb;
+    if (fixed_it <= 0 && hist[0] < tol) {
         status = 0;
         goto done;
     }
@@ -415,4 +425,14 @@ done:
     }
     free(r); free(rt); free(p); free(ph); free(rh); free(w); free(t); free(tmp);
     return status;
+}
+
+/* Number of OpenMP threads the oracle's parallel loops use (reported as cpu_baseline.cores). */
+int orc_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
 }

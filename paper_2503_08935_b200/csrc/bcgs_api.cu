@@ -1,0 +1,976 @@
+// bcgs_api.cu -- C ABI (include/bcgs.h) and solver driver of the B200-native Bi-CGSTAB
+// Poisson hot path (arXiv 2503.08935).  One context per rank / GPU.  The driver enqueues
+// the kernels of one outer iteration of Alg. 3 on a private stream; all
+// scalars live on the device (state.cuh), the host only polls a done flag.
+//
+// Built with --fmad=false (R17): no FMA contraction in any kernel; fma() appears only in
+// Dot2's TwoProd (dd.cuh).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bcgs.h"
+#include "dd.cuh"
+#include "state.cuh"
+#include "k_ref.cuh"
+#include "k_fused.cuh"
+
+namespace {
+
+constexpr int kNumSMs = 148;
+constexpr int kEwBlocks = kNumSMs * 8;   // element-wise grid: fixed -> deterministic partials
+constexpr size_t kAlign = 256;
+
+enum KClass {
+    KC_PRECOND = 0, KC_STENCIL1, KC_AXPY, KC_STENCIL2, KC_UPDATE_XR, KC_UPDATE_P,
+    KC_FINALIZE, KC_HALO, KC_ALLGATHER, KC_SCALARS, KC_FUSED_P1, KC_FUSED_P2, KC_FUSED_XR,
+    KC_COUNT
+};
+const char* kClassName[KC_COUNT] = {
+    "precond_sweep", "stencil_dot1", "axpy_s", "stencil_dot2", "update_xr", "update_p",
+    "finalize", "halo", "allgather", "scalars", "fused_p_cheb", "fused_s_cheb", "fused_xr"};
+
+size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+struct Layout {
+    int64_t nx, ny, nz, L, plane, vec_elems;   // vec_elems = (L + 2) * plane
+    int64_t n_part;
+    size_t off_vec[13];
+    size_t off_state, off_hist, off_scal, off_part, off_rank, off_gath, total;
+};
+
+constexpr int V_X = 0, V_R = 1, V_RT = 2, V_P = 3, V_PH = 4, V_RH = 5, V_W = 6, V_T = 7,
+              V_B = 8, V_C1 = 9, V_C2 = 10, V_IO = 11, V_W2 = 12, V_COUNT = 13;
+
+int64_t stencil_blocks(int64_t nx, int64_t ny, int64_t L)
+{
+    return ((nx + ref::BX - 1) / ref::BX) * ((ny + ref::BY - 1) / ref::BY) *
+           ((L + ref::ZC - 1) / ref::ZC);
+}
+
+bool make_layout(const bcgs_grid_desc* g, int32_t nranks, Layout* lay)
+{
+    if (!g || nranks < 1) return false;
+    lay->nx = g->n[0];
+    lay->ny = g->n[1];
+    lay->nz = g->n[2];
+    if (lay->nx < 1 || lay->ny < 1 || lay->nz < 1 || lay->nz % nranks) return false;
+    lay->L = lay->nz / nranks;
+    lay->plane = lay->nx * lay->ny;
+    lay->vec_elems = (lay->L + 2) * lay->plane;
+    lay->n_part = std::max<int64_t>(
+        {stencil_blocks(lay->nx, lay->ny, lay->L), (int64_t)kEwBlocks, fused::max_blocks(lay->nx, lay->ny, lay->L)});
+    size_t off = 0;
+    for (int v = 0; v < V_COUNT; ++v) {
+        lay->off_vec[v] = off;
+        off = align_up(off + sizeof(double) * (size_t)lay->vec_elems);
+    }
+    lay->off_state = off; off = align_up(off + sizeof(DevState));
+    lay->off_hist = off;  off = align_up(off + sizeof(double) * (BCGS_HIST_CAP + 1));
+    lay->off_scal = off;  off = align_up(off + sizeof(double) * 8 * BCGS_HIST_CAP);
+    lay->off_part = off;  off = align_up(off + sizeof(dd) * 2 * (size_t)lay->n_part);
+    lay->off_rank = off;  off = align_up(off + sizeof(dd) * 2);
+    lay->off_gath = off;  off = align_up(off + sizeof(dd) * 2 * (size_t)nranks);
+    lay->total = off;
+    return true;
+}
+
+struct EvRec {
+    int cls;
+    cudaEvent_t a, b;
+    double bytes;
+};
+
+}  // namespace
+
+struct bcgs_ctx_s {
+    Layout lay;
+    double h = 0.0, h2inv = 0.0;
+    int rank = 0, nranks = 1, device = 0;
+    cudaStream_t user = nullptr, s = nullptr;
+    cudaEvent_t join = nullptr;
+    ncclComm_t comm = nullptr;
+    char* ws = nullptr;
+    double* vec[V_COUNT] = {};     // interior plane 0 of each field
+    DevState* st = nullptr;
+    double *hist = nullptr, *scal = nullptr;
+    dd *part = nullptr, *rank_out = nullptr, *gath = nullptr;
+    double* h_pinned = nullptr;    // small pinned buffer for flag polls
+    // options
+    int kernels = 1, use_graph = 0, profile = 0, poll = 8;
+    // preconditioner
+    bcgs_pc pc = BCGS_PC_NONE;
+    int degree = 0, bpr = 1;
+    double c_min = 10.0, c_max = 1.0 - 1e-4, ov_a = 0.0, ov_b = 0.0;
+    double ivl[2] = {0, 0}, cst[7] = {}, rho[BCGS_MAX_DEGREE + 2] = {};
+    int have_x0 = 0;
+    double face[6] = {0, 0, 0, 0, 0, 0};
+    // solve bookkeeping
+    int begun = 0, launched = 0, fixed = 0, max_iter = 0;
+    double tol = 0.0;
+    std::chrono::steady_clock::time_point t0;
+    // graph
+    cudaGraphExec_t gexec = nullptr;
+    int graph_key = -1;
+    // profiling
+    std::vector<EvRec> pending;
+    std::vector<cudaEvent_t> free_ev;
+    double ktime[KC_COUNT] = {}, kbytes[KC_COUNT] = {};
+    int64_t kcalls[KC_COUNT] = {};
+    std::string err;
+};
+
+namespace {
+
+bcgs_status fail(bcgs_ctx c, bcgs_status s, const char* fmt, ...)
+{
+    if (c) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        c->err = buf;
+    }
+    return s;
+}
+
+#define CUDA_OK(c, call)                                                                    \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return fail((c), BCGS_E_CUDA, "%s failed: %s (%s:%d)", #call,                   \
+                        cudaGetErrorString(e_), __FILE__, __LINE__);                       \
+    } while (0)
+
+#define NCCL_OK(c, call)                                                                    \
+    do {                                                                                    \
+        ncclResult_t r_ = (call);                                                           \
+        if (r_ != ncclSuccess)                                                              \
+            return fail((c), BCGS_E_NCCL, "%s failed: %s", #call, ncclGetErrorString(r_)); \
+    } while (0)
+
+inline double* F(bcgs_ctx c, int v) { return c->vec[v]; }
+inline int64_t npts(bcgs_ctx c) { return c->lay.L * c->lay.plane; }
+
+ref::Grid ref_grid(bcgs_ctx c, int Lb)
+{
+    ref::Grid g;
+    g.nx = (int)c->lay.nx;
+    g.ny = (int)c->lay.ny;
+    g.L = (int)c->lay.L;
+    g.Lb = Lb;
+    g.h2inv = c->h2inv;
+    return g;
+}
+
+dim3 stencil_grid(bcgs_ctx c)
+{
+    return dim3((unsigned)((c->lay.nx + ref::BX - 1) / ref::BX),
+                (unsigned)((c->lay.ny + ref::BY - 1) / ref::BY),
+                (unsigned)((c->lay.L + ref::ZC - 1) / ref::ZC));
+}
+
+// ------------------------------------------------------------------ profiling events
+cudaEvent_t get_ev(bcgs_ctx c)
+{
+    if (!c->free_ev.empty()) {
+        cudaEvent_t e = c->free_ev.back();
+        c->free_ev.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct Prof {
+    bcgs_ctx c;
+    int cls;
+    double bytes;
+    cudaEvent_t a = nullptr;
+    Prof(bcgs_ctx c_, int cls_, double bytes_) : c(c_), cls(cls_), bytes(bytes_)
+    {
+        if (c->profile) {
+            a = get_ev(c);
+            cudaEventRecord(a, c->s);
+        }
+    }
+    ~Prof()
+    {
+        if (c->profile) {
+            cudaEvent_t b = get_ev(c);
+            cudaEventRecord(b, c->s);
+            c->pending.push_back({cls, a, b, bytes});
+        }
+    }
+};
+
+void harvest(bcgs_ctx c)
+{
+    if (c->pending.empty()) return;
+    cudaStreamSynchronize(c->s);
+    for (auto& r : c->pending) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        c->ktime[r.cls] += ms;
+        c->kcalls[r.cls] += 1;
+        c->kbytes[r.cls] = r.bytes;
+        c->free_ev.push_back(r.a);
+        c->free_ev.push_back(r.b);
+    }
+    c->pending.clear();
+}
+
+// ------------------------------------------------------------------ host constants
+// Eq. 9: μ_i = 4 sin²(iπ/(2(n+1))); Eqs. 10-11; R9, R10, R18.
+double mu(int64_t n, int64_t i)
+{
+    double s = sin(((double)i * M_PI) / (2.0 * (double)(n + 1)));
+    return 4.0 * (s * s);
+}
+
+void bounds_box(int64_t nx, int64_t ny, int64_t nzb, double h, double* lo, double* hi)
+{
+    double h2inv = 1.0 / (h * h);
+    *lo = ((mu(nx, 1) * h2inv) + (mu(ny, 1) * h2inv)) + (mu(nzb, 1) * h2inv);
+    *hi = ((mu(nx, nx) * h2inv) + (mu(ny, ny) * h2inv)) + (mu(nzb, nzb) * h2inv);
+}
+
+bcgs_status cheb_constants(const bcgs_grid_desc* g, int32_t nslab, bcgs_pc pc, int32_t k,
+                           double c_min, double c_max, double ov_a, double ov_b, double* ivl,
+                           double* cst, double* rho)
+{
+    if (k < 0 || k > BCGS_MAX_DEGREE) return BCGS_E_INVALID;
+    double a, b;
+    if (ov_a > 0.0 || ov_b > 0.0) {
+        a = ov_a;
+        b = ov_b;
+    } else if (pc == BCGS_PC_CHEB_GNOCOMM) {
+        double lo, hi;
+        bounds_box(g->n[0], g->n[1], g->n[2], g->h, &lo, &hi);
+        a = c_min * lo;
+        b = c_max * hi;
+    } else {
+        bounds_box(g->n[0], g->n[1], g->n[2] / nslab, g->h, &a, &b);   // R10
+    }
+    if (!(a > 0.0) || !(a < b) || !std::isfinite(b)) return BCGS_E_SPECTRUM;
+    double theta = (b + a) / 2.0, delta = (b - a) / 2.0;   // Eq. 15
+    double sigma = theta / delta;
+    rho[0] = 1.0 / sigma;
+    int kk = std::max(k, 1);
+    for (int j = 1; j <= kk; ++j) rho[j] = 1.0 / (2.0 * sigma - rho[j - 1]);
+    ivl[0] = a;
+    ivl[1] = b;
+    cst[0] = theta;
+    cst[1] = delta;
+    cst[2] = sigma;
+    cst[3] = 1.0 / theta;
+    cst[4] = 2.0 * (rho[1] / delta);
+    cst[5] = 2.0 * sigma;
+    cst[6] = 2.0 / delta;
+    return BCGS_OK;
+}
+
+// ------------------------------------------------------------------ init / state
+__global__ void k_init_state(DevState* st, double tol, int max_iter, int fixed)
+{
+    st->tol = tol;
+    st->max_iter = max_iter;
+    st->fixed_iters = fixed;
+    st->done = DONE_RUNNING;
+    st->iter = 0;
+}
+
+// ------------------------------------------------------------------ communication
+bcgs_status halo(bcgs_ctx c, double* v)
+{
+    if (c->nranks == 1) return BCGS_OK;
+    Prof pf(c, KC_HALO, 0.0);
+    const size_t pl = (size_t)c->lay.plane;
+    NCCL_OK(c, ncclGroupStart());
+    if (c->rank > 0) {
+        NCCL_OK(c, ncclSend(v, pl, ncclDouble, c->rank - 1, c->comm, c->s));
+        NCCL_OK(c, ncclRecv(v - pl, pl, ncclDouble, c->rank - 1, c->comm, c->s));
+    }
+    if (c->rank < c->nranks - 1) {
+        NCCL_OK(c, ncclSend(v + (c->lay.L - 1) * pl, pl, ncclDouble, c->rank + 1, c->comm, c->s));
+        NCCL_OK(c, ncclRecv(v + c->lay.L * pl, pl, ncclDouble, c->rank + 1, c->comm, c->s));
+    }
+    NCCL_OK(c, ncclGroupEnd());
+    return BCGS_OK;
+}
+
+// Reduce `nparts` partial pairs of ND dots, then run the scalar stage.
+template <int ND>
+bcgs_status reduce(bcgs_ctx c, int nparts, int stage)
+{
+    {
+        Prof pf(c, KC_FINALIZE, 0.0);
+        k_finalize<ND><<<1, 1024, 0, c->s>>>(c->part, nparts, stage, c->st, c->hist, c->scal,
+                                              c->rank_out, c->nranks);
+    }
+    if (c->nranks > 1) {
+        {
+            Prof pf(c, KC_ALLGATHER, 0.0);
+            NCCL_OK(c, ncclAllGather(c->rank_out, c->gath, 2 * ND, ncclDouble, c->comm, c->s));
+        }
+        Prof pf(c, KC_SCALARS, 0.0);
+        k_scalars<ND><<<1, 1, 0, c->s>>>(c->gath, c->nranks, stage, c->st, c->hist, c->scal);
+    }
+    CUDA_OK(c, cudaGetLastError());
+    return BCGS_OK;
+}
+
+#define TRY(x)                        \
+    do {                              \
+        bcgs_status s_ = (x);         \
+        if (s_ != BCGS_OK) return s_; \
+    } while (0)
+
+// ------------------------------------------------------------------ preconditioner (ref)
+// Alg. 4 with one sweep per launch; out = M^-1 q on every block.
+bcgs_status precond_ref(bcgs_ctx c, const double* q, double* out, const DevState* st)
+{
+    const int64_t n = npts(c);
+    const int k = c->degree;
+    if (c->pc == BCGS_PC_NONE) {
+        Prof pf(c, KC_PRECOND, 16.0 * n);
+        ref::k_copy<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(q, out, n, st);
+        CUDA_OK(c, cudaGetLastError());
+        return BCGS_OK;
+    }
+    ref::ChebConst cc{c->cst[3], c->cst[4], c->cst[5], c->cst[6]};
+    if (k == 0) {
+        Prof pf(c, KC_PRECOND, 16.0 * n);
+        ref::k_scale<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(q, out, n, cc.cz, st);
+        CUDA_OK(c, cudaGetLastError());
+        return BCGS_OK;
+    }
+    ref::Grid g = ref_grid(c, (int)(c->lay.L / c->bpr));
+    dim3 grid = stencil_grid(c), blk(ref::BX, ref::BY);
+    double* A = F(c, V_C1);
+    double* B = F(c, V_C2);
+    // x_1
+    {
+        Prof pf(c, KC_PRECOND, 16.0 * n);
+        ref::k_cheb_sweep<<<grid, blk, 0, c->s>>>(q, nullptr, nullptr, k == 1 ? out : A, g, cc,
+                                                 0.0, 0.0, 1, st);
+    }
+    // Sweeps j >= 3 write in place over x_{j-2} (each point reads x_{j-2} only at its own
+    // index); x_0 = q*cz is recomputed by sweep 2 instead of stored.
+    double* xm1 = A;
+    double* xm2 = nullptr;
+    for (int j = 2; j <= k; ++j) {
+        double* dst = (j == k) ? out : (xm2 ? xm2 : B);
+        {
+            Prof pf(c, KC_PRECOND, (xm2 ? 32.0 : 24.0) * n);
+            ref::k_cheb_sweep<<<grid, blk, 0, c->s>>>(q, xm1, xm2, dst, g, cc, c->rho[j],
+                                                     c->rho[j - 1], 0, st);
+        }
+        xm2 = xm1;
+        xm1 = dst;
+    }
+    CUDA_OK(c, cudaGetLastError());
+    return BCGS_OK;
+}
+
+// ------------------------------------------------------------------ one outer iteration
+bcgs_status iteration_ref(bcgs_ctx c)
+{
+    const int64_t n = npts(c);
+    DevState* st = c->st;
+    ref::Grid g = ref_grid(c, (int)c->lay.L);
+    dim3 sg = stencil_grid(c), sb(ref::BX, ref::BY);
+    const int nsb = (int)(sg.x * sg.y * sg.z);
+    // a2: p̂ = M^-1 p
+    TRY(precond_ref(c, F(c, V_P), F(c, V_PH), st));
+    // a3: halo p̂
+    TRY(halo(c, F(c, V_PH)));
+    // a4: w = A p̂, r~ᵀw
+    {
+        Prof pf(c, KC_STENCIL1, 24.0 * n);
+        ref::k_stencil_dot<1><<<sg, sb, 0, c->s>>>(F(c, V_PH), F(c, V_RT), F(c, V_W), g, 0,
+                                                  c->part, st);
+    }
+    // a5: α
+    TRY(reduce<1>(c, nsb, STAGE_ALPHA));
+    // a6: s = r - α w
+    {
+        Prof pf(c, KC_AXPY, 24.0 * n);
+        ref::k_axpy_s<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(F(c, V_R), F(c, V_W), n, st);
+    }
+    // a7: r̂ = M^-1 s
+    TRY(precond_ref(c, F(c, V_R), F(c, V_RH), st));
+    // a8: halo r̂
+    TRY(halo(c, F(c, V_RH)));
+    // a9: t = A r̂, tᵀs, tᵀt
+    {
+        Prof pf(c, KC_STENCIL2, 24.0 * n);
+        ref::k_stencil_dot<2><<<sg, sb, 0, c->s>>>(F(c, V_RH), F(c, V_R), F(c, V_T), g, 0,
+                                                  c->part, st);
+    }
+    // a10: ω
+    TRY(reduce<2>(c, nsb, STAGE_OMEGA));
+    // a11 + a12: x, r, r~ᵀr, rᵀr
+    {
+        Prof pf(c, KC_UPDATE_XR, 64.0 * n);
+        ref::k_update_xr<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(
+            F(c, V_X), F(c, V_PH), F(c, V_RH), F(c, V_R), F(c, V_T), F(c, V_RT), n, c->part, st);
+    }
+    // a13: test, ρ, β
+    TRY(reduce<2>(c, kEwBlocks, STAGE_RHO));
+    // a14: p = r + β (p - ω w)
+    {
+        Prof pf(c, KC_UPDATE_P, 32.0 * n);
+        ref::k_update_p<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(F(c, V_P), F(c, V_R), F(c, V_W),
+                                                                n, st);
+    }
+    CUDA_OK(c, cudaGetLastError());
+    return BCGS_OK;
+}
+
+bcgs_status iteration(bcgs_ctx c)
+{
+    if (c->kernels == 1 && fused::supported(c->lay.nx, c->lay.ny, c->lay.L, c->bpr, c->degree,
+                                            c->pc != BCGS_PC_NONE))
+        return fused::iteration(c);
+    return iteration_ref(c);
+}
+
+bcgs_status enqueue_iterations(bcgs_ctx c, int n)
+{
+    if (c->use_graph && !c->profile) {
+        if (!c->gexec) {
+            cudaGraph_t graph;
+            CUDA_OK(c, cudaStreamBeginCapture(c->s, cudaStreamCaptureModeThreadLocal));
+            bcgs_status st = iteration(c);
+            cudaError_t e = cudaStreamEndCapture(c->s, &graph);
+            if (st != BCGS_OK) return st;
+            CUDA_OK(c, e);
+            CUDA_OK(c, cudaGraphInstantiate(&c->gexec, graph, 0));
+            cudaGraphDestroy(graph);
+        }
+        for (int i = 0; i < n; ++i) CUDA_OK(c, cudaGraphLaunch(c->gexec, c->s));
+        return BCGS_OK;
+    }
+    for (int i = 0; i < n; ++i) TRY(iteration(c));
+    return BCGS_OK;
+}
+
+void drop_graph(bcgs_ctx c)
+{
+    if (c->gexec) {
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+    }
+}
+
+// caller stream -> private stream
+bcgs_status enter(bcgs_ctx c)
+{
+    CUDA_OK(c, cudaSetDevice(c->device));
+    CUDA_OK(c, cudaEventRecord(c->join, c->user));
+    CUDA_OK(c, cudaStreamWaitEvent(c->s, c->join, 0));
+    return BCGS_OK;
+}
+
+// private stream -> caller stream
+bcgs_status leave(bcgs_ctx c)
+{
+    CUDA_OK(c, cudaEventRecord(c->join, c->s));
+    CUDA_OK(c, cudaStreamWaitEvent(c->user, c->join, 0));
+    return BCGS_OK;
+}
+
+bcgs_status copy_in(bcgs_ctx c, double* dst, const double* src, int32_t mem)
+{
+    const size_t bytes = sizeof(double) * (size_t)npts(c);
+    CUDA_OK(c, cudaMemcpyAsync(dst, src, bytes,
+                               mem == BCGS_MEM_HOST ? cudaMemcpyHostToDevice
+                                                    : cudaMemcpyDeviceToDevice,
+                               c->s));
+    if (mem == BCGS_MEM_HOST) CUDA_OK(c, cudaStreamSynchronize(c->s));
+    return BCGS_OK;
+}
+
+bcgs_status fold_faces(bcgs_ctx c)
+{
+    int mask = 0;
+    double add[6];
+    for (int f = 0; f < 6; ++f) {
+        add[f] = c->face[f] * c->h2inv;
+        if (c->face[f] != 0.0) mask |= 1 << f;
+    }
+    if (!mask) return BCGS_OK;
+    ref::k_fold_boundary<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(
+        F(c, V_B), ref_grid(c, (int)c->lay.L), c->rank * c->lay.L, c->lay.nz, add[0], add[1],
+        add[2], add[3], add[4], add[5], mask);
+    CUDA_OK(c, cudaGetLastError());
+    return BCGS_OK;
+}
+
+bcgs_status validate_pc(bcgs_ctx c)
+{
+    bcgs_grid_desc g{{c->lay.nx, c->lay.ny, c->lay.nz}, c->h};
+    if (c->pc == BCGS_PC_NONE) return BCGS_OK;
+    bcgs_status s = cheb_constants(&g, c->nranks * c->bpr, c->pc, c->degree, c->c_min, c->c_max,
+                                   c->ov_a, c->ov_b, c->ivl, c->cst, c->rho);
+    if (s != BCGS_OK)
+        return fail(c, s, "Chebyshev interval invalid (a'=%g, b'=%g, k=%d)", c->ivl[0],
+                    c->ivl[1], c->degree);
+    return BCGS_OK;
+}
+
+}  // namespace
+
+#include "fused_driver.cuh"
+
+// =================================================================== C ABI
+extern "C" {
+
+int32_t bcgs_abi_version(void) { return BCGS_ABI_VERSION; }
+
+const char* bcgs_status_string(bcgs_status s)
+{
+    switch (s) {
+    case BCGS_OK: return "ok";
+    case BCGS_E_INVALID: return "invalid argument";
+    case BCGS_E_CONFIG: return "configuration error";
+    case BCGS_E_SPECTRUM: return "invalid Chebyshev interval";
+    case BCGS_E_CUDA: return "CUDA error";
+    case BCGS_E_NCCL: return "NCCL error";
+    case BCGS_NOT_CONVERGED: return "not converged";
+    case BCGS_BREAKDOWN: return "breakdown";
+    case BCGS_E_STATE: return "call out of order";
+    }
+    return "unknown";
+}
+
+size_t bcgs_workspace_bytes(const bcgs_grid_desc* grid, int32_t nranks)
+{
+    Layout lay;
+    if (!make_layout(grid, nranks, &lay)) return 0;
+    return lay.total;
+}
+
+bcgs_status bcgs_chebyshev_constants(const bcgs_grid_desc* grid, int32_t nslab, bcgs_pc pc,
+                                     int32_t degree, double c_min, double c_max,
+                                     double* interval2, double* out7, double* rho)
+{
+    if (!grid || nslab < 1 || grid->n[2] % nslab || !interval2 || !out7 || !rho)
+        return BCGS_E_INVALID;
+    if (pc != BCGS_PC_CHEB_GNOCOMM && pc != BCGS_PC_CHEB_BJ) return BCGS_E_INVALID;
+    return cheb_constants(grid, nslab, pc, degree, c_min, c_max, 0.0, 0.0, interval2, out7, rho);
+}
+
+bcgs_status bcgs_nccl_unique_id(void* out128)
+{
+    if (!out128) return BCGS_E_INVALID;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return BCGS_E_NCCL;
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    memcpy(out128, &id, sizeof id);
+    return BCGS_OK;
+}
+
+bcgs_status bcgs_create(const bcgs_grid_desc* grid, int32_t rank, int32_t nranks,
+                        const void* nccl_unique_id, int32_t cuda_device, void* d_workspace,
+                        size_t ws_bytes, void* cuda_stream, bcgs_ctx* out)
+{
+    if (!grid || !out || nranks < 1 || rank < 0 || rank >= nranks) return BCGS_E_INVALID;
+    if (!(grid->h > 0.0)) return BCGS_E_INVALID;
+    if (nranks > 1 && !nccl_unique_id) return BCGS_E_INVALID;
+    Layout lay;
+    if (!make_layout(grid, nranks, &lay)) return BCGS_E_CONFIG;
+    if (lay.nx > (1 << 30) || lay.ny > (1 << 30)) return BCGS_E_CONFIG;
+    if (!d_workspace || ws_bytes < lay.total || ((uintptr_t)d_workspace % kAlign))
+        return BCGS_E_INVALID;
+    bcgs_ctx c = new bcgs_ctx_s();
+    c->lay = lay;
+    c->h = grid->h;
+    c->h2inv = 1.0 / (grid->h * grid->h);
+    c->rank = rank;
+    c->nranks = nranks;
+    c->device = cuda_device;
+    c->user = (cudaStream_t)cuda_stream;
+    c->ws = (char*)d_workspace;
+    *out = c;
+    CUDA_OK(c, cudaSetDevice(cuda_device));
+    CUDA_OK(c, cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+    CUDA_OK(c, cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
+    CUDA_OK(c, cudaMallocHost(&c->h_pinned, 64));
+    for (int v = 0; v < V_COUNT; ++v)
+        c->vec[v] = (double*)(c->ws + lay.off_vec[v]) + lay.plane;
+    c->st = (DevState*)(c->ws + lay.off_state);
+    c->hist = (double*)(c->ws + lay.off_hist);
+    c->scal = (double*)(c->ws + lay.off_scal);
+    c->part = (dd*)(c->ws + lay.off_part);
+    c->rank_out = (dd*)(c->ws + lay.off_rank);
+    c->gath = (dd*)(c->ws + lay.off_gath);
+    TRY(enter(c));
+    CUDA_OK(c, cudaMemsetAsync(c->ws, 0, lay.total, c->s));   // zero ghost planes + state
+    if (nranks > 1) {
+        ncclUniqueId id;
+        memcpy(&id, nccl_unique_id, sizeof id);
+        NCCL_OK(c, ncclCommInitRank(&c->comm, nranks, id, rank));
+    }
+    TRY(leave(c));
+    return BCGS_OK;
+}
+
+void bcgs_destroy(bcgs_ctx c)
+{
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->s) cudaStreamSynchronize(c->s);
+    harvest(c);
+    drop_graph(c);
+    for (auto e : c->free_ev) cudaEventDestroy(e);
+    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->join) cudaEventDestroy(c->join);
+    if (c->s) cudaStreamDestroy(c->s);
+    if (c->h_pinned) cudaFreeHost(c->h_pinned);
+    delete c;
+}
+
+const char* bcgs_last_error(bcgs_ctx c) { return c ? c->err.c_str() : "null context"; }
+
+bcgs_status bcgs_set_option(bcgs_ctx c, int32_t option, int64_t value)
+{
+    if (!c) return BCGS_E_INVALID;
+    switch (option) {
+    case BCGS_OPT_KERNELS: c->kernels = (int)value; break;
+    case BCGS_OPT_GRAPH: c->use_graph = (int)value; break;
+    case BCGS_OPT_PROFILE: c->profile = (int)value; break;
+    case BCGS_OPT_POLL: c->poll = std::max<int>(1, (int)value); break;
+    default: return fail(c, BCGS_E_INVALID, "unknown option %d", option);
+    }
+    drop_graph(c);
+    return BCGS_OK;
+}
+
+bcgs_status bcgs_set_rhs_random(bcgs_ctx c, uint64_t seed)
+{
+    if (!c) return BCGS_E_INVALID;
+    TRY(enter(c));
+    ref::k_rhs_random<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(
+        F(c, V_B), npts(c), (int64_t)c->rank * npts(c), seed);
+    CUDA_OK(c, cudaGetLastError());
+    TRY(fold_faces(c));
+    c->begun = 0;
+    return leave(c);
+}
+
+bcgs_status bcgs_set_rhs(bcgs_ctx c, const double* f, int32_t mem)
+{
+    if (!c || !f) return BCGS_E_INVALID;
+    TRY(enter(c));
+    TRY(copy_in(c, F(c, V_B), f, mem));
+    TRY(fold_faces(c));
+    c->begun = 0;
+    return leave(c);
+}
+
+bcgs_status bcgs_set_boundary_value(bcgs_ctx c, int32_t face, double value)
+{
+    if (!c || face < 0 || face > 5 || !std::isfinite(value)) return BCGS_E_INVALID;
+    c->face[face] = value;
+    return BCGS_OK;
+}
+
+bcgs_status bcgs_set_initial_guess(bcgs_ctx c, const double* x0, int32_t mem)
+{
+    if (!c) return BCGS_E_INVALID;
+    if (!x0) {
+        c->have_x0 = 0;
+        return BCGS_OK;
+    }
+    TRY(enter(c));
+    TRY(copy_in(c, F(c, V_X), x0, mem));
+    c->have_x0 = 1;
+    c->begun = 0;
+    return leave(c);
+}
+
+bcgs_status bcgs_set_preconditioner(bcgs_ctx c, bcgs_pc pc, int32_t degree, double c_min,
+                                    double c_max, int32_t blocks_per_rank)
+{
+    if (!c) return BCGS_E_INVALID;
+    if (pc != BCGS_PC_NONE && pc != BCGS_PC_CHEB_GNOCOMM && pc != BCGS_PC_CHEB_BJ)
+        return fail(c, BCGS_E_INVALID, "unknown preconditioner %d", (int)pc);
+    if (degree < 0 || degree > BCGS_MAX_DEGREE)
+        return fail(c, BCGS_E_INVALID, "degree %d outside [0, %d]", degree, BCGS_MAX_DEGREE);
+    if (blocks_per_rank < 1 || c->lay.L % blocks_per_rank)
+        return fail(c, BCGS_E_CONFIG, "slab of %lld planes not divisible into %d blocks (axis z)",
+                    (long long)c->lay.L, blocks_per_rank);
+    c->pc = pc;
+    c->degree = degree;
+    c->c_min = c_min;
+    c->c_max = c_max;
+    c->bpr = blocks_per_rank;
+    drop_graph(c);
+    c->begun = 0;
+    return validate_pc(c);
+}
+
+bcgs_status bcgs_set_eigen_bounds(bcgs_ctx c, double a, double b)
+{
+    if (!c) return BCGS_E_INVALID;
+    if (!(a == 0.0 && b == 0.0) && !(a > 0.0 && a < b))
+        return fail(c, BCGS_E_SPECTRUM, "need 0 < a < b (got %g, %g)", a, b);
+    c->ov_a = a;
+    c->ov_b = b;
+    drop_graph(c);
+    return validate_pc(c);
+}
+
+bcgs_status bcgs_begin(bcgs_ctx c, double rel_tol, int32_t max_iter, int32_t fixed_iters)
+{
+    if (!c) return BCGS_E_INVALID;
+    if (fixed_iters < 0 || fixed_iters > BCGS_HIST_CAP || max_iter < 0 ||
+        (fixed_iters == 0 && (max_iter < 1 || max_iter > BCGS_HIST_CAP)))
+        return fail(c, BCGS_E_INVALID, "iteration counts out of range (cap %d)", BCGS_HIST_CAP);
+    TRY(validate_pc(c));
+    TRY(enter(c));
+    c->t0 = std::chrono::steady_clock::now();
+    const int64_t n = npts(c);
+    const size_t bytes = sizeof(double) * (size_t)n;
+    k_init_state<<<1, 1, 0, c->s>>>(c->st, rel_tol, max_iter, fixed_iters);
+    // Alg. 3 l.1-4: r0 = b - A x0; r~ = r0; p0 = r0; ρ0 = r~ᵀr0
+    if (c->have_x0) {
+        TRY(halo(c, F(c, V_X)));
+        ref::k_stencil_dot<0><<<stencil_grid(c), dim3(ref::BX, ref::BY), 0, c->s>>>(
+            F(c, V_X), nullptr, F(c, V_R), ref_grid(c, (int)c->lay.L), 0, nullptr, nullptr);
+        ref::k_residual0<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(F(c, V_B), F(c, V_R), n);
+    } else {
+        CUDA_OK(c, cudaMemsetAsync(F(c, V_X), 0, bytes, c->s));
+        CUDA_OK(c, cudaMemcpyAsync(F(c, V_R), F(c, V_B), bytes, cudaMemcpyDeviceToDevice, c->s));
+    }
+    CUDA_OK(c, cudaMemcpyAsync(F(c, V_RT), F(c, V_R), bytes, cudaMemcpyDeviceToDevice, c->s));
+    CUDA_OK(c, cudaMemcpyAsync(F(c, V_P), F(c, V_R), bytes, cudaMemcpyDeviceToDevice, c->s));
+    fused::on_begin(c);
+    ref::k_dot2<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(F(c, V_B), F(c, V_B), F(c, V_RT),
+                                                        F(c, V_R), n, 2, c->part);
+    CUDA_OK(c, cudaGetLastError());
+    TRY(reduce<2>(c, kEwBlocks, STAGE_SETUP));
+    c->begun = 1;
+    c->launched = 0;
+    c->fixed = fixed_iters;
+    c->max_iter = max_iter;
+    c->tol = rel_tol;
+    return BCGS_OK;
+}
+
+bcgs_status bcgs_iterate(bcgs_ctx c, int32_t n)
+{
+    if (!c || n < 0) return BCGS_E_INVALID;
+    if (!c->begun) return fail(c, BCGS_E_STATE, "bcgs_iterate before bcgs_begin");
+    TRY(enqueue_iterations(c, n));
+    c->launched += n;
+    return BCGS_OK;
+}
+
+static bcgs_status poll_state(bcgs_ctx c, int32_t* done, int32_t* iter)
+{
+    CUDA_OK(c, cudaMemcpyAsync(c->h_pinned, &c->st->iter, 2 * sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, c->s));
+    CUDA_OK(c, cudaStreamSynchronize(c->s));
+    *iter = ((int32_t*)c->h_pinned)[0];
+    *done = ((int32_t*)c->h_pinned)[1];
+    return BCGS_OK;
+}
+
+bcgs_status bcgs_finish(bcgs_ctx c, bcgs_report* out)
+{
+    if (!c) return BCGS_E_INVALID;
+    if (!c->begun) return fail(c, BCGS_E_STATE, "bcgs_finish before bcgs_begin");
+    int32_t done = 0, iter = 0;
+    TRY(poll_state(c, &done, &iter));
+    // true residual (R22): ||b - A x|| / ||b||, once
+    double true_rel = NAN, rel = NAN;
+    {
+        TRY(halo(c, F(c, V_X)));
+        ref::k_stencil_dot<0><<<stencil_grid(c), dim3(ref::BX, ref::BY), 0, c->s>>>(
+            F(c, V_X), nullptr, F(c, V_IO), ref_grid(c, (int)c->lay.L), 0, nullptr, nullptr);
+        ref::k_residual0<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(F(c, V_B), F(c, V_IO), npts(c));
+        ref::k_dot2<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(F(c, V_IO), F(c, V_IO), nullptr,
+                                                            nullptr, npts(c), 1, c->part);
+        TRY(reduce<1>(c, kEwBlocks, STAGE_DOT));
+        double h[2];
+        CUDA_OK(c, cudaMemcpyAsync(h, c->st->scratch, sizeof h, cudaMemcpyDeviceToHost, c->s));
+        double nbv;
+        CUDA_OK(c, cudaMemcpyAsync(&nbv, &c->st->nb, sizeof nbv, cudaMemcpyDeviceToHost, c->s));
+        CUDA_OK(c, cudaMemcpyAsync(&rel, &c->st->rel, sizeof rel, cudaMemcpyDeviceToHost, c->s));
+        CUDA_OK(c, cudaStreamSynchronize(c->s));
+        true_rel = nbv == 0.0 ? 0.0 : sqrt(h[0]) / nbv;
+    }
+    harvest(c);
+    TRY(leave(c));
+    bcgs_status s = BCGS_OK;
+    if (done == DONE_BREAKDOWN) s = BCGS_BREAKDOWN;
+    else if (done == DONE_MAXIT || done == DONE_RUNNING) s = BCGS_NOT_CONVERGED;
+    if (out) {
+        out->status = s;
+        out->converged = (done == DONE_OK);
+        out->iterations = iter;
+        int64_t Lb = c->lay.L / c->bpr;
+        out->degree_warning = (c->pc != BCGS_PC_NONE && 2 * (int64_t)c->degree > Lb) ? 1 : 0;
+        out->rel_residual = rel;
+        out->true_rel_residual = true_rel;
+        out->seconds =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - c->t0).count();
+    }
+    return s;
+}
+
+bcgs_status bcgs_solve(bcgs_ctx c, double rel_tol, int32_t max_iter, int32_t fixed_iters,
+                       bcgs_report* out)
+{
+    TRY(bcgs_begin(c, rel_tol, max_iter, fixed_iters));
+    if (fixed_iters > 0) {
+        TRY(bcgs_iterate(c, fixed_iters));
+    } else {
+        int32_t done = 0, iter = 0;
+        TRY(poll_state(c, &done, &iter));
+        while (done == DONE_RUNNING && c->launched < max_iter) {
+            int batch = std::min(c->poll, max_iter - c->launched);
+            TRY(bcgs_iterate(c, batch));
+            TRY(poll_state(c, &done, &iter));
+        }
+    }
+    return bcgs_finish(c, out);
+}
+
+int32_t bcgs_residual_history(bcgs_ctx c, double* host_out, int32_t cap)
+{
+    if (!c || !host_out || cap <= 0) return 0;
+    int32_t iter = 0;
+    if (cudaMemcpy(&iter, &c->st->iter, sizeof iter, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return 0;
+    int32_t m = std::min(cap, iter + 1);
+    if (cudaMemcpy(host_out, c->hist, sizeof(double) * m, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return 0;
+    return m;
+}
+
+int32_t bcgs_scalar_history(bcgs_ctx c, double* host_out, int32_t cap_iters)
+{
+    if (!c || !host_out || cap_iters <= 0) return 0;
+    int32_t iter = 0;
+    if (cudaMemcpy(&iter, &c->st->iter, sizeof iter, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return 0;
+    int32_t m = std::min(cap_iters, iter);
+    if (m > 0 && cudaMemcpy(host_out, c->scal, sizeof(double) * 8 * m,
+                            cudaMemcpyDeviceToHost) != cudaSuccess)
+        return 0;
+    return m;
+}
+
+bcgs_status bcgs_get_solution(bcgs_ctx c, double* x, int32_t mem)
+{
+    if (!c || !x) return BCGS_E_INVALID;
+    TRY(enter(c));
+    const size_t bytes = sizeof(double) * (size_t)npts(c);
+    CUDA_OK(c, cudaMemcpyAsync(x, F(c, V_X), bytes,
+                               mem == BCGS_MEM_HOST ? cudaMemcpyDeviceToHost
+                                                    : cudaMemcpyDeviceToDevice,
+                               c->s));
+    if (mem == BCGS_MEM_HOST) CUDA_OK(c, cudaStreamSynchronize(c->s));
+    return leave(c);
+}
+
+bcgs_status bcgs_apply_operator(bcgs_ctx c, const double* d_in, double* d_out,
+                                int32_t block_local)
+{
+    if (!c || !d_in || !d_out) return BCGS_E_INVALID;
+    TRY(enter(c));
+    const size_t bytes = sizeof(double) * (size_t)npts(c);
+    double* io = F(c, V_IO);
+    CUDA_OK(c, cudaMemcpyAsync(io, d_in, bytes, cudaMemcpyDeviceToDevice, c->s));
+    if (!block_local) TRY(halo(c, io));
+    else {
+        CUDA_OK(c, cudaMemsetAsync(io - c->lay.plane, 0, sizeof(double) * c->lay.plane, c->s));
+        CUDA_OK(c, cudaMemsetAsync(io + npts(c), 0, sizeof(double) * c->lay.plane, c->s));
+    }
+    ref::k_stencil_dot<0><<<stencil_grid(c), dim3(ref::BX, ref::BY), 0, c->s>>>(
+        io, nullptr, d_out, ref_grid(c, (int)(c->lay.L / c->bpr)), block_local, nullptr,
+        nullptr);
+    CUDA_OK(c, cudaGetLastError());
+    return leave(c);
+}
+
+bcgs_status bcgs_apply_preconditioner(bcgs_ctx c, const double* d_in, double* d_out)
+{
+    if (!c || !d_in || !d_out) return BCGS_E_INVALID;
+    TRY(validate_pc(c));
+    TRY(enter(c));
+    const size_t bytes = sizeof(double) * (size_t)npts(c);
+    double* io = F(c, V_IO);
+    CUDA_OK(c, cudaMemcpyAsync(io, d_in, bytes, cudaMemcpyDeviceToDevice, c->s));
+    double* o = F(c, V_W2);
+    if (c->kernels == 1 && fused::precond_supported(c))
+        TRY(fused::precond_apply(c, io, o));
+    else
+        TRY(precond_ref(c, io, o, nullptr));
+    CUDA_OK(c, cudaMemcpyAsync(d_out, o, bytes, cudaMemcpyDeviceToDevice, c->s));
+    return leave(c);
+}
+
+bcgs_status bcgs_dot(bcgs_ctx c, const double* d_a, const double* d_b, double* host_out)
+{
+    if (!c || !d_a || !d_b || !host_out) return BCGS_E_INVALID;
+    TRY(enter(c));
+    ref::k_dot2<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(d_a, d_b, nullptr, nullptr, npts(c), 1,
+                                                        c->part);
+    CUDA_OK(c, cudaGetLastError());
+    TRY(reduce<1>(c, kEwBlocks, STAGE_DOT));
+    CUDA_OK(c, cudaMemcpyAsync(c->h_pinned, c->st->scratch, sizeof(double),
+                               cudaMemcpyDeviceToHost, c->s));
+    CUDA_OK(c, cudaStreamSynchronize(c->s));
+    *host_out = ((double*)c->h_pinned)[0];
+    return leave(c);
+}
+
+int32_t bcgs_kernel_times(bcgs_ctx c, char* names_out, int32_t names_cap, double* ms_out,
+                          int64_t* calls_out, double* bytes_out, int32_t cap)
+{
+    if (!c) return 0;
+    harvest(c);
+    std::string names;
+    int m = std::min<int>(cap, KC_COUNT);
+    for (int i = 0; i < KC_COUNT; ++i) {
+        names += kClassName[i];
+        names += '\n';
+        if (i < m) {
+            if (ms_out) ms_out[i] = c->ktime[i];
+            if (calls_out) calls_out[i] = c->kcalls[i];
+            if (bytes_out) bytes_out[i] = c->kbytes[i];
+        }
+    }
+    if (names_out && names_cap > 0) {
+        strncpy(names_out, names.c_str(), names_cap - 1);
+        names_out[names_cap - 1] = 0;
+    }
+    return m;
+}
+
+void bcgs_kernel_times_reset(bcgs_ctx c)
+{
+    if (!c) return;
+    harvest(c);
+    for (int i = 0; i < KC_COUNT; ++i) {
+        c->ktime[i] = 0.0;
+        c->kcalls[i] = 0;
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,226 @@
+"""GPU-vs-oracle parity through the C ABI (libbcgs.so), on seeded synthetic inputs.
+
+Bars (BASELINE.json north_star): per-iteration relative residuals within 1e-9 over the first
+20 iterations, converged solution within 1e-8 relative L2, iteration count to 1e-8 within
+±1.  With the arithmetic contract the expected outcome is bitwise identity;
+single-operator tests demand it.
+"""
+import numpy as np
+import pytest
+
+import synth_inputs as si
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+KERNELS = [0, 1]          # 0 = reference kernels, 1 = fused / temporally blocked
+
+
+@pytest.fixture(scope="module")
+def bc():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2503_08935_b200 import bcgs
+    bcgs.load()
+    return bcgs
+
+
+def make(bc, n, h=None, kernels=1, **pc):
+    n3 = (n,) * 3 if np.isscalar(n) else tuple(n)
+    h = si.unit_cube_h(n3[0]) if h is None else h
+    s = bc.Solver(n3, h)
+    s.set_option(bc.OPT_KERNELS, kernels)
+    if pc:
+        s.set_preconditioner(**pc)
+    return s, n3, h
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+# --------------------------------------------------------------------------- single steps
+
+@pytest.mark.parametrize("n", [8, (37, 29, 23), 64])
+def test_rhs_random_bitwise(bc, orc, n):
+    """R16 device generator == oracle generator: with M = I, iteration 1 gives
+    x1 = α b + ω s, which exposes every bit of b (history, scalars and x compared)."""
+    out = compare_solve(bc, orc, n, pc="none", k=0, fixed=1)
+    assert_parity(*out)
+
+
+@pytest.mark.parametrize("n", [(33, 17, 20), 48, (64, 64, 40)])
+@pytest.mark.parametrize("block_local,bpr", [(0, 1), (1, 2), (1, 4)])
+def test_operator_bitwise(bc, orc, n, block_local, bpr):
+    s, n3, h = make(bc, n, pc="none", degree=0, blocks_per_rank=1)
+    s.set_preconditioner("gnocomm", 1, blocks_per_rank=bpr)
+    v = np.random.default_rng(1).standard_normal(n3[::-1])
+    out = host(s.apply_operator(dev(v), block_local=bool(block_local)))
+    ref = orc.apply_A(v, h, bpr if block_local else 1)
+    assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("kernels", KERNELS)
+@pytest.mark.parametrize("pc,k,bpr", [("gnocomm", 0, 1), ("gnocomm", 1, 1), ("gnocomm", 2, 2),
+                                      ("gnocomm", 4, 1), ("gnocomm", 4, 4), ("bj", 3, 2),
+                                      ("bj", 7, 1), ("gnocomm", 8, 2)])
+@pytest.mark.parametrize("n", [(40, 24, 32), (67, 45, 16)])
+def test_preconditioner_bitwise(bc, orc, n, pc, k, bpr, kernels):
+    s, n3, h = make(bc, n, kernels=kernels, pc=pc, degree=k, blocks_per_rank=bpr)
+    q = np.random.default_rng(2).standard_normal(n3[::-1])
+    out = host(s.apply_preconditioner(dev(q)))
+    ivl, _, _ = bc.chebyshev_constants(n3, h, bpr, pc, k)
+    ref = orc.apply_cheb(q, h, bpr, k, ivl[0], ivl[1])
+    assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("n", [(9, 7, 5), 64, (130, 66, 24)])
+def test_dot_equals_oracle(bc, orc, n):
+    s, n3, h = make(bc, n)
+    r = np.random.default_rng(3)
+    a = r.standard_normal(n3[::-1]) * 10.0 ** r.integers(-6, 6, n3[::-1])
+    b = r.standard_normal(n3[::-1])
+    assert s.dot(dev(a), dev(b)) == orc.dot(a, b)
+
+
+# --------------------------------------------------------------------------- whole solves
+
+def compare_solve(bc, orc, n, pc="gnocomm", k=4, bpr=1, kernels=1, tol=1e-8, fixed=0,
+                  rhs=None, max_it=5000):
+    s, n3, h = make(bc, n, kernels=kernels)
+    s.set_preconditioner(pc, k, blocks_per_rank=bpr)
+    if rhs is None:
+        s.set_rhs_random(si.SEED)
+        b = orc.rhs_random(n3[::-1], si.SEED)
+    else:
+        b, h = rhs
+        s.set_rhs(dev(b))
+    rep = s.solve(tol=tol, max_iter=max_it, fixed_iters=fixed)
+    g_hist = s.residual_history()
+    g_scal = s.scalar_history()
+    g_x = host(s.solution())
+    o = orc.bicgstab(b, h, pc=pc, k=k, nslab=bpr, tol=tol, max_it=max_it, fixed_it=fixed)
+    return rep, g_hist, g_scal, g_x, o
+
+
+def assert_parity(rep, g_hist, g_scal, g_x, o, bitwise=True):
+    assert rep["status_name"] == o.status
+    assert abs(rep["iterations"] - o.iterations) <= 1
+    m = min(21, len(g_hist), len(o.history))
+    rel = np.abs(g_hist[:m] - o.history[:m]) / np.abs(o.history[:m])
+    assert np.max(rel) <= 1e-9, rel
+    err = np.linalg.norm(g_x - o.x) / np.linalg.norm(o.x)
+    assert err <= 1e-8
+    if bitwise:
+        assert rep["iterations"] == o.iterations
+        assert np.array_equal(g_hist, o.history)
+        assert np.array_equal(g_scal, o.scalars)
+        assert np.array_equal(g_x, o.x)
+
+
+def test_c1_mms_polyexp_unpreconditioned(bc, orc):
+    """BASELINE config C1: 32³, manufactured solution, unpreconditioned, to 1e-8."""
+    f, u, h = si.mms_polyexp(32)
+    out = compare_solve(bc, orc, 32, pc="none", k=0, rhs=(f, h))
+    assert_parity(*out)
+    rep, x = out[0], out[3]
+    assert rep["converged"] and rep["true_rel_residual"] < 1e-7
+    err = np.linalg.norm(x - u) / np.linalg.norm(u)
+    assert err == pytest.approx(4.56e-4, rel=0.05)       # O(h²) discretisation error
+
+
+@pytest.mark.parametrize("kernels", KERNELS)
+@pytest.mark.parametrize("n,pc,k,bpr", [(32, "gnocomm", 4, 1), (48, "gnocomm", 4, 2),
+                                        (64, "gnocomm", 4, 4), (64, "bj", 4, 2),
+                                        ((40, 36, 48), "gnocomm", 3, 3), (32, "none", 0, 1),
+                                        (64, "gnocomm", 8, 1)])
+def test_solve_parity(bc, orc, n, pc, k, bpr, kernels):
+    assert_parity(*compare_solve(bc, orc, n, pc, k, bpr, kernels))
+
+
+@pytest.mark.parametrize("kernels", KERNELS)
+def test_solve_parity_128(bc, orc, kernels):
+    assert_parity(*compare_solve(bc, orc, 128, "gnocomm", 4, 1, kernels))
+
+
+@pytest.mark.parametrize("kernels", KERNELS)
+def test_c2_256_first_20_iterations(bc, orc, kernels):
+    """Config C2 (256³, Chebyshev degree 4): first 20 iterations, bitwise."""
+    assert_parity(*compare_solve(bc, orc, 256, "gnocomm", 4, 1, kernels, fixed=20))
+
+
+def test_c3_512_first_iterations(bc, orc):
+    """Config C3 at full size (512³, the bench launch configuration): 3 iterations, bitwise."""
+    assert_parity(*compare_solve(bc, orc, 512, "gnocomm", 4, 1, 1, fixed=3))
+
+
+def test_graph_replay_matches_direct(bc):
+    outs = []
+    for graph in (0, 1):
+        s, n3, h = make(bc, 64, pc="gnocomm", degree=4)
+        s.set_option(bc.OPT_GRAPH, graph)
+        s.set_rhs_random(7)
+        rep = s.solve(tol=1e-8)
+        outs.append((rep["iterations"], s.residual_history(), host(s.solution())))
+    assert outs[0][0] == outs[1][0]
+    assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][2], outs[1][2])
+
+
+def test_boundary_values_and_initial_guess(bc, orc):
+    n, g = 24, 1.5
+    h = si.unit_cube_h(n)
+    s, n3, _ = make(bc, n, pc="gnocomm", degree=4)
+    for f in range(6):
+        s.set_boundary_value(f, g)
+    s.set_rhs(dev(np.zeros((n, n, n))))
+    rep = s.solve(tol=1e-12)
+    x = host(s.solution())
+    assert rep["converged"] and np.max(np.abs(x - g)) < 1e-9
+    b = orc.fold_boundary(np.zeros((n, n, n)), h, [g] * 6)
+    o = orc.bicgstab(b, h, pc="gnocomm", k=4, tol=1e-12)
+    assert np.array_equal(x, o.x)
+    # warm start from the exact solution: converged before the first iteration (R26)
+    x0 = np.full((n, n, n), g)
+    s.set_initial_guess(dev(x0))
+    rep2 = s.solve(tol=1e-8)
+    assert rep2["converged"] and rep2["iterations"] == 0
+    # perturbed warm start: bitwise parity with the oracle's r0 = b - A x0 path
+    x0 = x0 + 1e-3 * np.random.default_rng(4).standard_normal(x0.shape)
+    s.set_initial_guess(dev(x0))
+    rep3 = s.solve(tol=1e-10)
+    o3 = orc.bicgstab(b, h, pc="gnocomm", k=4, tol=1e-10, x0=x0)
+    assert rep3["iterations"] == o3.iterations
+    assert np.array_equal(s.residual_history(), o3.history)
+    assert np.array_equal(host(s.solution()), o3.x)
+
+
+def test_zero_rhs_and_breakdown_reporting(bc):
+    s, n3, h = make(bc, 16, pc="gnocomm", degree=2)
+    s.set_rhs(dev(np.zeros((16, 16, 16))))
+    rep = s.solve(tol=1e-8)
+    assert rep["converged"] and rep["iterations"] == 0
+    assert not host(s.solution()).any()
+
+
+def test_mms_sine_one_iteration(bc):
+    f, u, h = si.mms_sine(32)
+    s, n3, _ = make(bc, 32, pc="none", degree=0)
+    s.set_rhs(dev(f))
+    rep = s.solve(tol=1e-8)
+    assert rep["iterations"] == 1
+
+
+def test_recurrence_equals_true_residual_any_size(bc):
+    """Property that holds at any size: after a few iterations the recurrence residual
+    equals ||b - A x||/||b|| to rounding (checked at the bench size 512³ too)."""
+    for n in (96, 512):
+        s, n3, h = make(bc, n, pc="gnocomm", degree=4)
+        s.set_rhs_random(si.SEED)
+        rep = s.solve(fixed_iters=5)
+        assert rep["true_rel_residual"] == pytest.approx(rep["rel_residual"], rel=1e-6)
+        del s
+        torch.cuda.empty_cache()

@@ -416,3 +416,18 @@ def test_fixed_iteration_mode_and_history_shape(orc):
 def test_zero_rhs(orc):
     res = orc.bicgstab(np.zeros((3, 3, 3)), 0.25)
     assert res.status == "ok" and res.iterations == 0 and not res.x.any()
+
+
+def test_initial_guess_reading_r26(orc):
+    """R26: exact initial guess -> converged, 0 iterations; rel_0 = ||b - A x0|| / ||b||."""
+    n, h = 6, 1.0 / 7
+    b = orc.rhs_random((n, n, n), 4)
+    A = dense_ref.assemble(n, n, n, h)
+    xs = np.linalg.solve(A, b.ravel()).reshape(b.shape)
+    res = orc.bicgstab(b, h, x0=xs, tol=1e-8)
+    assert res.status == "ok" and res.iterations == 0
+    x0 = xs + 0.01 * np.random.default_rng(0).standard_normal(xs.shape)
+    res = orc.bicgstab(b, h, x0=x0, tol=1e-12)
+    rel0 = np.linalg.norm(b.ravel() - A @ x0.ravel()) / np.linalg.norm(b)
+    assert res.history[0] == pytest.approx(rel0, rel=1e-12)
+    assert np.linalg.norm(res.x - xs) / np.linalg.norm(xs) < 1e-9
