@@ -43,12 +43,13 @@ size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 struct Layout {
     int64_t nx, ny, nz, L, plane, vec_elems;   // vec_elems = (L + 2) * plane
     int64_t n_part;
-    size_t off_vec[13];
+    size_t off_vec[16];
     size_t off_state, off_hist, off_scal, off_part, off_rank, off_gath, total;
 };
 
 constexpr int V_X = 0, V_R = 1, V_RT = 2, V_P = 3, V_PH = 4, V_RH = 5, V_W = 6, V_T = 7,
-              V_B = 8, V_C1 = 9, V_C2 = 10, V_IO = 11, V_W2 = 12, V_COUNT = 13;
+              V_B = 8, V_C1 = 9, V_C2 = 10, V_IO = 11, V_W2 = 12, V_P2 = 13,
+              V_S = 14, V_COUNT = 15;
 
 int64_t stencil_blocks(int64_t nx, int64_t ny, int64_t L)
 {
@@ -758,8 +759,8 @@ bcgs_status bcgs_begin(bcgs_ctx c, double rel_tol, int32_t max_iter, int32_t fix
     CUDA_OK(c, cudaMemcpyAsync(F(c, V_RT), F(c, V_R), bytes, cudaMemcpyDeviceToDevice, c->s));
     CUDA_OK(c, cudaMemcpyAsync(F(c, V_P), F(c, V_R), bytes, cudaMemcpyDeviceToDevice, c->s));
     fused::on_begin(c);
-    ref::k_dot2<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(F(c, V_B), F(c, V_B), F(c, V_RT),
-                                                        F(c, V_R), n, 2, c->part);
+    ref::k_dot2<2><<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(F(c, V_B), F(c, V_B), F(c, V_RT),
+                                                           F(c, V_R), n, c->part);
     CUDA_OK(c, cudaGetLastError());
     TRY(reduce<2>(c, kEwBlocks, STAGE_SETUP));
     c->begun = 1;
@@ -802,8 +803,8 @@ bcgs_status bcgs_finish(bcgs_ctx c, bcgs_report* out)
         ref::k_stencil_dot<0><<<stencil_grid(c), dim3(ref::BX, ref::BY), 0, c->s>>>(
             F(c, V_X), nullptr, F(c, V_IO), ref_grid(c, (int)c->lay.L), 0, nullptr, nullptr);
         ref::k_residual0<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(F(c, V_B), F(c, V_IO), npts(c));
-        ref::k_dot2<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(F(c, V_IO), F(c, V_IO), nullptr,
-                                                            nullptr, npts(c), 1, c->part);
+        ref::k_dot2<1><<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(F(c, V_IO), F(c, V_IO), nullptr,
+                                                               nullptr, npts(c), c->part);
         TRY(reduce<1>(c, kEwBlocks, STAGE_DOT));
         double h[2];
         CUDA_OK(c, cudaMemcpyAsync(h, c->st->scratch, sizeof h, cudaMemcpyDeviceToHost, c->s));
@@ -929,8 +930,8 @@ bcgs_status bcgs_dot(bcgs_ctx c, const double* d_a, const double* d_b, double* h
 {
     if (!c || !d_a || !d_b || !host_out) return BCGS_E_INVALID;
     TRY(enter(c));
-    ref::k_dot2<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(d_a, d_b, nullptr, nullptr, npts(c), 1,
-                                                        c->part);
+    ref::k_dot2<1><<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(d_a, d_b, nullptr, nullptr, npts(c),
+                                                           c->part);
     CUDA_OK(c, cudaGetLastError());
     TRY(reduce<1>(c, kEwBlocks, STAGE_DOT));
     CUDA_OK(c, cudaMemcpyAsync(c->h_pinned, c->st->scratch, sizeof(double),

@@ -1,11 +1,172 @@
-// fused_driver.cuh -- driver side of the fused path (filled in by the performance path).
+// fused_driver.cuh -- host driver of the fused path.  One outer iteration:
+//   K1  k_cheb_tb<MODE_P>: p_i = r + β(p - ω w) (a14 of the previous iteration) and
+//       p̂ = M^-1 p_i (a2), one HBM pass (reads r, p, w; writes p_i, p̂)
+//   a3  halo(p̂)                        a4  w = A p̂, r~ᵀw      a5  α
+//   K2  k_cheb_tb<MODE_S>: s = r - α w (a6) and r̂ = M^-1 s (a7), one pass
+//   a8  halo(r̂)                        a9  t = A r̂, tᵀs, tᵀt  a10 ω
+//   a11+a12 x += α p̂ + ω r̂; r = s - ω t; r~ᵀr, rᵀr         a13 test, ρ, β
+// p is double-buffered (halo columns of neighbouring tiles read the old p while the new
+// one is written); the buffer is selected on the device from the iteration parity, so
+// one captured graph serves every iteration.
 #pragma once
+
 namespace fused {
-bcgs_status iteration(bcgs_ctx c) { return iteration_ref(c); }
-void on_begin(bcgs_ctx) {}
-bool precond_supported(bcgs_ctx) { return false; }
+
+template <int K> struct Tile;
+template <> struct Tile<1> { static constexpr int X = 32, Y = 16; };
+template <> struct Tile<2> { static constexpr int X = 32, Y = 16; };
+template <> struct Tile<3> { static constexpr int X = 32, Y = 16; };
+template <> struct Tile<4> { static constexpr int X = 32, Y = 16; };
+template <> struct Tile<5> { static constexpr int X = 32, Y = 8; };
+template <> struct Tile<6> { static constexpr int X = 32, Y = 8; };
+template <> struct Tile<7> { static constexpr int X = 16, Y = 8; };
+template <> struct Tile<8> { static constexpr int X = 16, Y = 8; };
+
+// a11 + a12 with s in its own buffer: x = (x + α p̂) + ω r̂; r = s - ω t; partials r~·r, r·r
+__global__ void k_update_xr_s(double* __restrict__ x, const double* __restrict__ ph,
+                              const double* __restrict__ rh, const double* __restrict__ s,
+                              double* __restrict__ r, const double* __restrict__ t,
+                              const double* __restrict__ rt, int64_t n, dd* __restrict__ part,
+                              const DevState* __restrict__ st)
+{
+    if (st->done) return;
+    const double alpha = st->alpha, omega = st->omega;
+    double p[2] = {0.0, 0.0}, q[2] = {0.0, 0.0};
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        x[c] = (x[c] + alpha * ph[c]) + omega * rh[c];
+        const double rn = s[c] - omega * t[c];
+        r[c] = rn;
+        dot2_acc(p[0], q[0], rt[c], rn);
+        dot2_acc(p[1], q[1], rn, rn);
+    }
+    block_reduce_dd<2>(p, q, part + (int64_t)blockIdx.x * 2);
+}
+
+template <int K, int MODE>
+bcgs_status launch_tb_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
+{
+    constexpr int TX = Tile<K>::X, TY = Tile<K>::Y;
+    using S = TbShape<K, TX, TY>;
+    auto kern = k_cheb_tb<K, TX, TY, MODE>;
+    static bool attr = false;
+    if (!attr) {
+        CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)S::smem));
+        attr = true;
+    }
+    dim3 grid((unsigned)((a.nx + TX - 1) / TX), (unsigned)((a.ny + TY - 1) / TY),
+              (unsigned)nchunk_total);
+    kern<<<grid, S::NT, S::smem, c->s>>>(a);
+    CUDA_OK(c, cudaGetLastError());
+    return BCGS_OK;
+}
+
+template <int MODE>
+bcgs_status launch_tb(bcgs_ctx c, TbArgs& a)
+{
+    const int k = c->degree;
+    a.nx = (int)c->lay.nx;
+    a.ny = (int)c->lay.ny;
+    a.Lb = (int)(c->lay.L / c->bpr);
+    a.h2inv = c->h2inv;
+    a.cz = c->cst[3];
+    a.g1 = c->cst[4];
+    a.A2 = c->cst[5];
+    a.B2 = c->cst[6];
+    for (int j = 0; j <= k; ++j) a.rho[j] = c->rho[j];
+    // z-chunking: enough CTAs for ~8 waves of 148 SMs, chunks of >= 16 planes
+    int tx = 32, ty = 16;
+    if (k >= 7) { tx = 16; ty = 8; } else if (k >= 5) { tx = 32; ty = 8; }
+    const int64_t tiles = ((a.nx + tx - 1) / tx) * (int64_t)((a.ny + ty - 1) / ty) * c->bpr;
+    int64_t want = (8 * kNumSMs + tiles - 1) / tiles;
+    want = std::max<int64_t>(1, std::min<int64_t>(want, (a.Lb + 15) / 16));
+    a.zch = (int)((a.Lb + want - 1) / want);
+    a.nchunk = (a.Lb + a.zch - 1) / a.zch;
+    const int nz = a.nchunk * c->bpr;
+    switch (k) {
+    case 1: return launch_tb_k<1, MODE>(c, a, nz);
+    case 2: return launch_tb_k<2, MODE>(c, a, nz);
+    case 3: return launch_tb_k<3, MODE>(c, a, nz);
+    case 4: return launch_tb_k<4, MODE>(c, a, nz);
+    case 5: return launch_tb_k<5, MODE>(c, a, nz);
+    case 6: return launch_tb_k<6, MODE>(c, a, nz);
+    case 7: return launch_tb_k<7, MODE>(c, a, nz);
+    case 8: return launch_tb_k<8, MODE>(c, a, nz);
+    }
+    return fail(c, BCGS_E_INVALID, "temporal blocking supports degree 1..%d", KMAX_TB);
+}
+
+bool precond_supported(bcgs_ctx c)
+{
+    return c->pc != BCGS_PC_NONE && c->degree >= 1 && c->degree <= KMAX_TB;
+}
+
 bcgs_status precond_apply(bcgs_ctx c, const double* q, double* out)
 {
-    return precond_ref(c, q, out, nullptr);
+    TbArgs a{};
+    a.q = q;
+    a.out = out;
+    a.st = nullptr;
+    Prof pf(c, KC_FUSED_P1, 16.0 * npts(c));
+    return launch_tb<MODE_PLAIN>(c, a);
 }
+
+void on_begin(bcgs_ctx) {}
+
+bcgs_status iteration(bcgs_ctx c)
+{
+    const int64_t n = npts(c);
+    DevState* st = c->st;
+    ref::Grid g = ref_grid(c, (int)c->lay.L);
+    dim3 sg = stencil_grid(c), sb(ref::BX, ref::BY);
+    const int nsb = (int)(sg.x * sg.y * sg.z);
+    {   // K1: a14 (previous iteration) + a2
+        TbArgs a{};
+        a.r = F(c, V_R);
+        a.w = F(c, V_W);
+        a.p_a = F(c, V_P);
+        a.p_b = F(c, V_P2);
+        a.side_a = F(c, V_P);
+        a.side_b = F(c, V_P2);
+        a.out = F(c, V_PH);
+        a.st = st;
+        Prof pf(c, KC_FUSED_P1, 40.0 * n);
+        TRY(launch_tb<MODE_P>(c, a));
+    }
+    TRY(halo(c, F(c, V_PH)));
+    {
+        Prof pf(c, KC_STENCIL1, 24.0 * n);
+        ref::k_stencil_dot<1><<<sg, sb, 0, c->s>>>(F(c, V_PH), F(c, V_RT), F(c, V_W), g, 0,
+                                                  c->part, st);
+    }
+    TRY(reduce<1>(c, nsb, STAGE_ALPHA));
+    {   // K2: a6 + a7
+        TbArgs a{};
+        a.r = F(c, V_R);
+        a.w = F(c, V_W);
+        a.side_a = F(c, V_S);
+        a.out = F(c, V_RH);
+        a.st = st;
+        Prof pf(c, KC_FUSED_P2, 32.0 * n);
+        TRY(launch_tb<MODE_S>(c, a));
+    }
+    TRY(halo(c, F(c, V_RH)));
+    {
+        Prof pf(c, KC_STENCIL2, 24.0 * n);
+        ref::k_stencil_dot<2><<<sg, sb, 0, c->s>>>(F(c, V_RH), F(c, V_S), F(c, V_T), g, 0,
+                                                  c->part, st);
+    }
+    TRY(reduce<2>(c, nsb, STAGE_OMEGA));
+    {
+        Prof pf(c, KC_FUSED_XR, 64.0 * n);
+        k_update_xr_s<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(
+            F(c, V_X), F(c, V_PH), F(c, V_RH), F(c, V_S), F(c, V_R), F(c, V_T), F(c, V_RT), n,
+            c->part, st);
+    }
+    TRY(reduce<2>(c, kEwBlocks, STAGE_RHO));
+    CUDA_OK(c, cudaGetLastError());
+    return BCGS_OK;
+}
+
 }  // namespace fused

@@ -174,18 +174,19 @@ __global__ void k_residual0(const double* __restrict__ b, double* __restrict__ r
     EW_LOOP(n) r[c] = b[c] - r[c];
 }
 
-// setup dots: ND = 2: {b·b, r·r}
+// stand-alone dots: ND = 1: {a0·b0}; ND = 2: {a0·b0, a1·b1} (setup: {b·b, r~·r0})
+template <int ND>
 __global__ void k_dot2(const double* __restrict__ a0, const double* __restrict__ b0,
                        const double* __restrict__ a1, const double* __restrict__ b1, int64_t n,
-                       int nd, dd* __restrict__ part)
+                       dd* __restrict__ part)
 {
-    double p[2] = {0.0, 0.0}, s[2] = {0.0, 0.0};
+    double p[ND] = {}, s[ND] = {};
     EW_LOOP(n)
     {
         dot2_acc(p[0], s[0], a0[c], b0[c]);
-        if (nd > 1) dot2_acc(p[1], s[1], a1[c], b1[c]);
+        if (ND > 1) dot2_acc(p[ND - 1], s[ND - 1], a1[c], b1[c]);
     }
-    block_reduce_dd<2>(p, s, part + (int64_t)blockIdx.x * 2);
+    block_reduce_dd<ND>(p, s, part + (int64_t)blockIdx.x * ND);
 }
 
 // a6, KernelBiCGS2: s = r - α w  (in place on r)
