@@ -86,10 +86,11 @@ __global__ void __launch_bounds__(TbShape<K, TX, TY>::NT, 1) k_cheb_tb(TbArgs a)
     const int64_t plane = (int64_t)a.nx * a.ny;
     const int64_t col = in_dom ? gx + (int64_t)a.nx * gy : 0;
 
-    double qw[K + 1];
+    constexpr int QW = (K + 1 > 3) ? K + 1 : 3;   // q at planes t .. t-max(K,2)
+    double qw[QW];
     double win[K][3];   // levels 1..K-1: planes (newest, newest-1, newest-2)
 #pragma unroll
-    for (int d = 0; d <= K; ++d) qw[d] = 0.0;
+    for (int d = 0; d < QW; ++d) qw[d] = 0.0;
 #pragma unroll
     for (int j = 0; j < K; ++j) win[j][0] = win[j][1] = win[j][2] = 0.0;
 
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(TbShape<K, TX, TY>::NT, 1) k_cheb_tb(TbArgs a)
         }
         load(t + 1);
 #pragma unroll
-        for (int d = K; d > 0; --d) qw[d] = qw[d - 1];
+        for (int d = QW - 1; d > 0; --d) qw[d] = qw[d - 1];
         qw[0] = q0;
 
         const double* prev = sm + ((t - 1) & 1) * (K * NT);
