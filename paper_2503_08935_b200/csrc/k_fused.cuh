@@ -3,7 +3,7 @@
 // k_cheb_tb applies all K Chebyshev sweeps of Alg. 2 / Alg. 4 to a
 // slab block in ONE pass over HBM: a CTA owns a TX x TY column tile (plus a K-wide halo that
 // it recomputes) and marches a z-wavefront through its z-chunk; level j (sweep j) trails
-// level j-1 by one plane.  z-neighbours live in per-thread register windows, in-plane
+// level j-1 by one plane.  z-neighbours live in per-thread register rings, in-plane
 // neighbours in a double-buffered shared-memory plane per level (one __syncthreads per
 // z-step).  Zero ghosts at block cuts / physical faces (R8, Eq. 12-14) are exact zeros.
 //
@@ -41,81 +41,57 @@ struct TbArgs {
 template <int K, int TX, int TY>
 struct TbShape {
     static constexpr int EX = TX + 2 * K, EY = TY + 2 * K, NT = EX * EY;
-    static constexpr size_t smem = sizeof(double) * 2 * K * NT;
+    static constexpr int PAD = EX + 1;        // guard: halo lanes may read tid±EX safely
+    static constexpr int PLANE = NT + 2 * PAD;
+    static constexpr size_t smem = sizeof(double) * 2 * K * PLANE;
 };
 
+// Per-thread wavefront state.  Register windows are rings indexed by the compile-time
+// phase PH of the (fully unrolled) z-step, so no register moves are needed:
+//   q ring (QW >= max(K+1, 3) planes, multiple of 3): q(t-d) at slot (PH-d) mod QW
+//   win[j] (levels 1..K-1, 3 planes):                x_j(newest-d) at slot (PH-d) mod 3
 template <int K, int TX, int TY, int MODE>
-__global__ void __launch_bounds__(TbShape<K, TX, TY>::NT, 1) k_cheb_tb(TbArgs a)
-{
+struct TbThread {
     using S = TbShape<K, TX, TY>;
-    constexpr int EX = S::EX, NT = S::NT;
-    extern __shared__ double sm[];   // [2][K][NT]
+    static constexpr int EX = S::EX, NT = S::NT, PLANE = S::PLANE;
+    static constexpr int QW = ((K + 1 + 2) / 3) * 3 < 3 ? 3 : ((K + 1 + 2) / 3) * 3;
+    static constexpr int U = QW;                 // unroll length: multiple of QW and of 3
 
-    const DevState* st = a.st;
-    if (st && st->done) return;
-    double alpha = 0.0, beta = 0.0, omega = 0.0;
-    bool first = false;
-    const double* pin = nullptr;
-    double* side = nullptr;
-    if (MODE == MODE_P) {
-        const int par = st->iter & 1;
-        first = (st->iter == 0);
-        beta = st->beta;
-        omega = st->omega;
-        pin = par ? a.p_b : a.p_a;
-        side = par ? a.side_a : a.side_b;
-    } else if (MODE == MODE_S) {
-        alpha = st->alpha;
-        side = a.side_a;
-    }
-
-    const int tid = threadIdx.x;
-    const int ex = tid % EX, ey = tid / EX;
-    const int gx = blockIdx.x * TX + ex - K, gy = blockIdx.y * TY + ey - K;
-    const bool in_dom = gx >= 0 && gx < a.nx && gy >= 0 && gy < a.ny;
-    // Chebyshev distance of this column outside the output tile (<= 0 inside)
-    const int dist = max(max(K - ex, ex - (K + TX - 1)), max(K - ey, ey - (K + TY - 1)));
-    const bool in_tile = in_dom && dist <= 0;
-
-    const int blk = blockIdx.z / a.nchunk, ch = blockIdx.z % a.nchunk;
-    const int b0 = blk * a.Lb, b1 = b0 + a.Lb;
-    const int c0 = b0 + ch * a.zch, c1 = min(b1, c0 + a.zch);
-    if (c0 >= b1) return;
-    const int t0 = max(b0, c0 - K), t1 = c1 - 1 + K;
-
-    const int64_t plane = (int64_t)a.nx * a.ny;
-    const int64_t col = in_dom ? gx + (int64_t)a.nx * gy : 0;
-
-    constexpr int QW = (K + 1 > 3) ? K + 1 : 3;   // q at planes t .. t-max(K,2)
     double qw[QW];
-    double win[K][3];   // levels 1..K-1: planes (newest, newest-1, newest-2)
-#pragma unroll
-    for (int d = 0; d < QW; ++d) qw[d] = 0.0;
-#pragma unroll
-    for (int j = 0; j < K; ++j) win[j][0] = win[j][1] = win[j][2] = 0.0;
+    double win[K > 1 ? K : 2][3];
+    double nr, np, nw;                           // prefetched level-0 operands of plane t+1
+    const TbArgs* a;
+    double* sm;
+    int tid, b0, b1, c0, c1;
+    int64_t col, plane;
+    unsigned actmask;                            // bit j: level j needed at this column
+    bool in_dom, in_tile, first;
+    double alpha, beta, omega;
+    const double* pin;
+    double* side;
 
-    // prefetch of the level-0 operands of plane t (one step ahead)
-    double nr = 0.0, np = 0.0, nw = 0.0;
-    auto load = [&](int t) {
+    __device__ __forceinline__ void load(int t)
+    {
         if (in_dom && t < b1) {
             const int64_t c = col + plane * t;
             if (MODE == MODE_PLAIN) {
-                nr = __ldg(a.q + c);
+                nr = __ldg(a->q + c);
             } else if (MODE == MODE_P) {
                 np = __ldg(pin + c);
                 if (!first) {
-                    nr = __ldg(a.r + c);
-                    nw = __ldg(a.w + c);
+                    nr = __ldg(a->r + c);
+                    nw = __ldg(a->w + c);
                 }
             } else {
-                nr = __ldg(a.r + c);
-                nw = __ldg(a.w + c);
+                nr = __ldg(a->r + c);
+                nw = __ldg(a->w + c);
             }
         }
-    };
-    load(t0);
+    }
 
-    for (int t = t0; t <= t1; ++t) {
+    template <int PH>
+    __device__ __forceinline__ void step(int t)
+    {
         // ---- level 0: q at plane t (zero outside the block / domain)
         double q0 = 0.0;
         if (in_dom && t < b1) {
@@ -125,49 +101,138 @@ __global__ void __launch_bounds__(TbShape<K, TX, TY>::NT, 1) k_cheb_tb(TbArgs a)
             if (MODE != MODE_PLAIN && in_tile && t >= c0 && t < c1) side[col + plane * t] = q0;
         }
         load(t + 1);
-#pragma unroll
-        for (int d = QW - 1; d > 0; --d) qw[d] = qw[d - 1];
-        qw[0] = q0;
-
-        const double* prev = sm + ((t - 1) & 1) * (K * NT);
-        // ---- levels 1..K: level j computes plane m = t - j
+        qw[PH % QW] = q0;
+        const double* prev = sm + S::PAD + ((t - 1) & 1) * (K * PLANE);
+        // ---- levels 1..K: level j computes plane m = t - j (branch-free, masked)
 #pragma unroll
         for (int j = 1; j <= K; ++j) {
             const int m = t - j;
-            double v = 0.0;
-            if (in_dom && dist <= K - j && m >= b0 && m < b1) {
-                const double* pl = prev + (j - 1) * NT;
-                const double xm = pl[tid - 1], xp = pl[tid + 1];
-                const double ym = pl[tid - EX], yp = pl[tid + EX];
-                double zm, zc, zp;   // x_{j-1} at planes m-1, m, m+1
-                if (j == 1) {
-                    zp = qw[0]; zc = qw[1]; zm = qw[2];
-                } else {
-                    zp = win[j - 1][0]; zc = win[j - 1][1]; zm = win[j - 1][2];
-                }
-                const double Sv = (6.0 * zc - (((((xm + xp) + ym) + yp) + zm) + zp)) * a.h2inv;
-                const double qc = qw[j];
-                if (j == 1) {
-                    v = a.g1 * ((2.0 * qc) - (Sv * a.cz));
-                } else {
-                    const double z2 = (j == 2) ? qc * a.cz : win[j - 2][2];
-                    v = a.rho[j] * (((a.A2 * zc) + (a.B2 * (qc - Sv))) - (a.rho[j - 1] * z2));
-                }
+            const double* pl = prev + (j - 1) * PLANE;
+            const double xm = pl[tid - 1], xp = pl[tid + 1];
+            const double ym = pl[tid - EX], yp = pl[tid + EX];
+            double zm, zc, zp;   // x_{j-1} at planes m-1, m, m+1
+            if (j == 1) {
+                zp = qw[PH % QW];
+                zc = qw[(PH + QW - 1) % QW];
+                zm = qw[(PH + QW - 2) % QW];
+            } else {
+                zp = win[j - 1][PH % 3];
+                zc = win[j - 1][(PH + 2) % 3];
+                zm = win[j - 1][(PH + 1) % 3];
             }
+            const double Sv = (6.0 * zc - (((((xm + xp) + ym) + yp) + zm) + zp)) * a->h2inv;
+            const double qc = qw[(PH + QW - j) % QW];
+            double v;
+            if (j == 1) {
+                v = a->g1 * ((2.0 * qc) - (Sv * a->cz));
+            } else {
+                const double z2 = (j == 2) ? qc * a->cz : win[j - 2][(PH + 1) % 3];
+                v = a->rho[j] * (((a->A2 * zc) + (a->B2 * (qc - Sv))) - (a->rho[j - 1] * z2));
+            }
+            const bool act = ((actmask >> j) & 1u) && (unsigned)(m - b0) < (unsigned)(b1 - b0);
+            v = act ? v : 0.0;
             if (j < K) {
-                win[j][2] = win[j][1];
-                win[j][1] = win[j][0];
-                win[j][0] = v;
+                win[j][PH % 3] = v;
             } else if (in_tile && m >= c0 && m < c1) {
-                a.out[col + plane * m] = v;
+                a->out[col + plane * m] = v;
             }
         }
         // ---- publish the newest plane of levels 0..K-1 for the next step
-        double* cur = sm + (t & 1) * (K * NT);
-        cur[tid] = qw[0];
+        double* cur = sm + S::PAD + (t & 1) * (K * PLANE);
+        cur[tid] = q0;
 #pragma unroll
-        for (int j = 1; j < K; ++j) cur[j * NT + tid] = win[j][0];
+        for (int j = 1; j < K; ++j) cur[j * PLANE + tid] = win[j][PH % 3];
         __syncthreads();
+    }
+};
+
+template <int K, int TX, int TY, int MODE>
+__global__ void __launch_bounds__(TbShape<K, TX, TY>::NT, 1) k_cheb_tb(TbArgs a)
+{
+    using T = TbThread<K, TX, TY, MODE>;
+    constexpr int EX = T::EX, U = T::U;
+    extern __shared__ double sm[];   // [2][K][PAD + NT + PAD]
+
+    const DevState* st = a.st;
+    if (st && st->done) return;
+    T th;
+    th.a = &a;
+    th.sm = sm;
+    th.nr = th.np = th.nw = 0.0;
+    th.alpha = th.beta = th.omega = 0.0;
+    th.first = false;
+    th.pin = nullptr;
+    th.side = nullptr;
+    if (MODE == MODE_P) {
+        const int par = st->iter & 1;
+        th.first = (st->iter == 0);
+        th.beta = st->beta;
+        th.omega = st->omega;
+        th.pin = par ? a.p_b : a.p_a;
+        th.side = par ? a.side_a : a.side_b;
+    } else if (MODE == MODE_S) {
+        th.alpha = st->alpha;
+        th.side = a.side_a;
+    }
+    const int tid = threadIdx.x;
+    th.tid = tid;
+    const int ex = tid % EX, ey = tid / EX;
+    const int gx = blockIdx.x * TX + ex - K, gy = blockIdx.y * TY + ey - K;
+    th.in_dom = gx >= 0 && gx < a.nx && gy >= 0 && gy < a.ny;
+    // Chebyshev distance of this column outside the output tile (<= 0 inside)
+    const int dist = max(max(K - ex, ex - (K + TX - 1)), max(K - ey, ey - (K + TY - 1)));
+    th.in_tile = th.in_dom && dist <= 0;
+    th.actmask = 0;
+#pragma unroll
+    for (int j = 1; j <= K; ++j)
+        if (th.in_dom && dist <= K - j) th.actmask |= 1u << j;
+
+    const int blk = blockIdx.z / a.nchunk, ch = blockIdx.z % a.nchunk;
+    th.b0 = blk * a.Lb;
+    th.b1 = th.b0 + a.Lb;
+    th.c0 = th.b0 + ch * a.zch;
+    th.c1 = min(th.b1, th.c0 + a.zch);
+    if (th.c0 >= th.b1) return;
+    const int t0 = max(th.b0, th.c0 - K), t1 = th.c1 - 1 + K;
+    th.plane = (int64_t)a.nx * a.ny;
+    th.col = th.in_dom ? gx + (int64_t)a.nx * gy : 0;
+#pragma unroll
+    for (int d = 0; d < T::QW; ++d) th.qw[d] = 0.0;
+#pragma unroll
+    for (int j = 0; j < (K > 1 ? K : 2); ++j) th.win[j][0] = th.win[j][1] = th.win[j][2] = 0.0;
+    // zero both buffers (plane t0-1 and the guards) so every neighbour read is a finite 0
+    for (int i = tid; i < 2 * K * T::PLANE; i += blockDim.x) sm[i] = 0.0;
+    __syncthreads();
+
+    th.load(t0);
+    int t = t0;
+    for (; t + U - 1 <= t1; t += U) {
+        th.template step<0>(t);
+        th.template step<1 % U>(t + 1);
+        th.template step<2 % U>(t + 2);
+        if (U > 3) {
+            th.template step<3 % U>(t + 3);
+            th.template step<4 % U>(t + 4);
+            th.template step<5 % U>(t + 5);
+        }
+        if (U > 6) {
+            th.template step<6 % U>(t + 6);
+            th.template step<7 % U>(t + 7);
+            th.template step<8 % U>(t + 8);
+        }
+    }
+    // remainder (< U steps); phases continue from 0
+    if (t <= t1) th.template step<0>(t);
+    if (t + 1 <= t1) th.template step<1 % U>(t + 1);
+    if (U > 3) {
+        if (t + 2 <= t1) th.template step<2 % U>(t + 2);
+        if (t + 3 <= t1) th.template step<3 % U>(t + 3);
+        if (t + 4 <= t1) th.template step<4 % U>(t + 4);
+    }
+    if (U > 6) {
+        if (t + 5 <= t1) th.template step<5 % U>(t + 5);
+        if (t + 6 <= t1) th.template step<6 % U>(t + 6);
+        if (t + 7 <= t1) th.template step<7 % U>(t + 7);
     }
 }
 
