@@ -81,7 +81,9 @@ typedef enum {
                                /*     launch); 1 = fused / temporally blocked (default)   */
     BCGS_OPT_GRAPH = 1,        /* 1 = replay iterations from a captured CUDA graph        */
     BCGS_OPT_PROFILE = 2,      /* 1 = CUDA events around every kernel (bcgs_kernel_times) */
-    BCGS_OPT_POLL = 3          /* iterations launched between done-flag polls (tol mode)  */
+    BCGS_OPT_POLL = 3,         /* iterations launched between done-flag polls (tol mode)  */
+    BCGS_OPT_TB_VARIANT = 4    /* temporally blocked kernel layout (tuning): 2 = square   */
+                               /* tile, 3 = warp-row RY=2 (default), 4 = warp-row RY=4    */
 } bcgs_option;
 
 typedef struct {

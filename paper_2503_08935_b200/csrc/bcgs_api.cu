@@ -106,7 +106,7 @@ struct bcgs_ctx_s {
     dd *part = nullptr, *rank_out = nullptr, *gath = nullptr;
     double* h_pinned = nullptr;    // small pinned buffer for flag polls
     // options
-    int kernels = 1, use_graph = 0, profile = 0, poll = 8;
+    int kernels = 1, use_graph = 0, profile = 0, poll = 8, tb_variant = 3;
     // preconditioner
     bcgs_pc pc = BCGS_PC_NONE;
     int degree = 0, bpr = 1;
@@ -653,6 +653,7 @@ bcgs_status bcgs_set_option(bcgs_ctx c, int32_t option, int64_t value)
     case BCGS_OPT_GRAPH: c->use_graph = (int)value; break;
     case BCGS_OPT_PROFILE: c->profile = (int)value; break;
     case BCGS_OPT_POLL: c->poll = std::max<int>(1, (int)value); break;
+    case BCGS_OPT_TB_VARIANT: c->tb_variant = (int)value; break;
     default: return fail(c, BCGS_E_INVALID, "unknown option %d", option);
     }
     drop_graph(c);

@@ -62,6 +62,47 @@ bcgs_status launch_tb_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
     return BCGS_OK;
 }
 
+template <int K, int RY, int NW, int MODE>
+bcgs_status launch_tb3_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
+{
+    using S = Tb3Shape<K, RY, NW>;
+    auto kern = k_cheb_tb3<K, RY, NW, MODE>;
+    static bool attr = false;
+    if (!attr) {
+        CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)S::smem));
+        attr = true;
+    }
+    dim3 grid((unsigned)((a.nx + S::TX - 1) / S::TX), (unsigned)((a.ny + S::TY - 1) / S::TY),
+              (unsigned)nchunk_total);
+    kern<<<grid, NW * 32, S::smem, c->s>>>(a);
+    CUDA_OK(c, cudaGetLastError());
+    return BCGS_OK;
+}
+
+// tile (TX, TY) of a kernel variant for degree k
+void variant_tile(int variant, int k, int* tx, int* ty)
+{
+    if (variant == 2 || k > 5) {
+        *tx = 32; *ty = 16;
+        if (k >= 7) { *tx = 16; *ty = 8; } else if (k >= 5) { *tx = 32; *ty = 8; }
+    } else if (variant == 4) {
+        *tx = 32 - 2 * k; *ty = 32 - 2 * k;      // RY = 4, NW = 8
+    } else {
+        *tx = 32 - 2 * k; *ty = 32 - 2 * k;      // RY = 2, NW = 16
+    }
+}
+
+template <int K, int MODE>
+bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz)
+{
+    if constexpr (K <= 5) {   // register budget: warp-row layouts up to K = 5
+        if (c->tb_variant == 4) return launch_tb3_k<K, 4, 8, MODE>(c, a, nz);
+        if (c->tb_variant == 3) return launch_tb3_k<K, 2, 16, MODE>(c, a, nz);
+    }
+    return launch_tb_k<K, MODE>(c, a, nz);
+}
+
 template <int MODE>
 bcgs_status launch_tb(bcgs_ctx c, TbArgs& a)
 {
@@ -76,8 +117,8 @@ bcgs_status launch_tb(bcgs_ctx c, TbArgs& a)
     a.B2 = c->cst[6];
     for (int j = 0; j <= k; ++j) a.rho[j] = c->rho[j];
     // z-chunking: enough CTAs for ~8 waves of 148 SMs, chunks of >= 16 planes
-    int tx = 32, ty = 16;
-    if (k >= 7) { tx = 16; ty = 8; } else if (k >= 5) { tx = 32; ty = 8; }
+    int tx, ty;
+    variant_tile(c->tb_variant, k, &tx, &ty);
     const int64_t tiles = ((a.nx + tx - 1) / tx) * (int64_t)((a.ny + ty - 1) / ty) * c->bpr;
     int64_t want = (8 * kNumSMs + tiles - 1) / tiles;
     want = std::max<int64_t>(1, std::min<int64_t>(want, (a.Lb + 15) / 16));
@@ -85,14 +126,14 @@ bcgs_status launch_tb(bcgs_ctx c, TbArgs& a)
     a.nchunk = (a.Lb + a.zch - 1) / a.zch;
     const int nz = a.nchunk * c->bpr;
     switch (k) {
-    case 1: return launch_tb_k<1, MODE>(c, a, nz);
-    case 2: return launch_tb_k<2, MODE>(c, a, nz);
-    case 3: return launch_tb_k<3, MODE>(c, a, nz);
-    case 4: return launch_tb_k<4, MODE>(c, a, nz);
-    case 5: return launch_tb_k<5, MODE>(c, a, nz);
-    case 6: return launch_tb_k<6, MODE>(c, a, nz);
-    case 7: return launch_tb_k<7, MODE>(c, a, nz);
-    case 8: return launch_tb_k<8, MODE>(c, a, nz);
+    case 1: return launch_variant<1, MODE>(c, a, nz);
+    case 2: return launch_variant<2, MODE>(c, a, nz);
+    case 3: return launch_variant<3, MODE>(c, a, nz);
+    case 4: return launch_variant<4, MODE>(c, a, nz);
+    case 5: return launch_variant<5, MODE>(c, a, nz);
+    case 6: return launch_variant<6, MODE>(c, a, nz);
+    case 7: return launch_variant<7, MODE>(c, a, nz);
+    case 8: return launch_variant<8, MODE>(c, a, nz);
     }
     return fail(c, BCGS_E_INVALID, "temporal blocking supports degree 1..%d", KMAX_TB);
 }
