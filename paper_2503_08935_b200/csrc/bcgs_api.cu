@@ -5,6 +5,7 @@
 //
 // Built with --fmad=false (R17): no FMA contraction in any kernel; fma() appears only in
 // Dot2's TwoProd (dd.cuh).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -106,7 +107,7 @@ struct bcgs_ctx_s {
     dd *part = nullptr, *rank_out = nullptr, *gath = nullptr;
     double* h_pinned = nullptr;    // small pinned buffer for flag polls
     // options
-    int kernels = 1, use_graph = 0, profile = 0, poll = 8, tb_variant = 3;
+    int kernels = 1, use_graph = 0, profile = 0, poll = 8, tb_variant = 5;
     // preconditioner
     bcgs_pc pc = BCGS_PC_NONE;
     int degree = 0, bpr = 1;

@@ -476,6 +476,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_cheb_tb3(TbArgs a)
     }
 }
 
+}  // namespace fused
+#include "k_tb4.cuh"
+namespace fused {
+
 // ----------------------------------------------------------------------------- host side
 inline int64_t max_blocks(int64_t, int64_t, int64_t) { return 0; }
 inline bool supported(int64_t, int64_t, int64_t, int, int degree, bool has_pc)

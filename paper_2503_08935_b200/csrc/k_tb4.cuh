@@ -1,0 +1,364 @@
+// k_tb4.cuh -- TMA-fed warp-row temporally blocked Chebyshev kernel (sm_100a).
+//
+// Same wavefront / arithmetic as k_cheb_tb3 (k_fused.cuh), plus:
+//  * level-0 operands (q, or r/p/w) of plane t+1..t+NS-1 are staged in shared memory by the
+//    Tensor Memory Accelerator (cp.async.bulk.tensor.3d, one elected thread, mbarrier
+//    completion) -> no exposed DRAM latency on the z-march; out-of-grid columns of the box
+//    are zero-filled by TMA;
+//  * steps are specialised at compile time: in the steady state of an interior tile no
+//    zero-ghost masking is evaluated (masks are only needed next to the physical faces, the
+//    block cuts and the first/last K planes of a block).
+// Values outside a level's halo are never read by an active point (the halo shrinks by one
+// per level), so unmasked lanes may hold arbitrary finite values there.
+#pragma once
+#include <cuda.h>
+
+namespace fused {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            uint64_t* bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
+struct TbMaps {
+    CUtensorMap q, r, w, pa, pb;   // 3-D maps (nx, ny, L) of the slab fields, box (32, EY, 1)
+};
+
+template <int K, int RY, int NW, int NS>
+struct Tb4Shape {
+    static constexpr int EX = 32, EY = NW * RY, TX = EX - 2 * K, TY = EY - 2 * K;
+    static constexpr int PAD = EX;
+    static constexpr int PLANE = EX * EY + 2 * PAD;       // level plane incl. guard rows
+    static constexpr int BOX = EX * EY;                   // staged input box (doubles)
+    static constexpr int QW = ((K + 1 + 2) / 3) * 3 < 3 ? 3 : ((K + 1 + 2) / 3) * 3;
+    static constexpr size_t level_bytes = sizeof(double) * 2 * K * PLANE;
+    static constexpr size_t stage_bytes = sizeof(double) * (size_t)NS * 3 * BOX;
+    static constexpr size_t smem = level_bytes + stage_bytes + 128;
+};
+
+template <int K, int RY, int NW, int NS, int MODE>
+struct Tb4Thread {
+    using S = Tb4Shape<K, RY, NW, NS>;
+    static constexpr int EX = S::EX, TX = S::TX, TY = S::TY, PLANE = S::PLANE, QW = S::QW,
+                         BOX = S::BOX;
+
+    double qw[QW][RY];
+    double win[K > 1 ? K : 2][3][RY];
+    const TbArgs* a;
+    const TbMaps* maps;
+    double* sm;        // level planes
+    double* stg;       // [NS][3][BOX] staged inputs
+    uint64_t* bar;     // [NS]
+    int lane, ey0, b0, b1, c0, c1, t0, t1, wdy, tx0, ty0;
+    int64_t col[RY], plane;
+    unsigned actmask[RY];
+    bool in_dom[RY], in_tile[RY], first;
+    double alpha, beta, omega;
+    const CUtensorMap* pmap;
+    double* side;
+
+    static constexpr int ninputs() { return MODE == MODE_PLAIN ? 1 : (MODE == MODE_P ? 3 : 2); }
+
+    __device__ __forceinline__ void issue(int tt)
+    {   // thread 0: stage the level-0 operands of plane tt
+        const int s = (tt - t0) % NS;
+        double* d = stg + (size_t)s * 3 * BOX;
+        if (MODE == MODE_PLAIN) {
+            mbar_expect_tx(&bar[s], BOX * 8);
+            tma_load_3d(d, &maps->q, tx0, ty0, tt, &bar[s]);
+        } else if (MODE == MODE_P) {
+            if (first) {
+                mbar_expect_tx(&bar[s], BOX * 8);
+                tma_load_3d(d, pmap, tx0, ty0, tt, &bar[s]);
+            } else {
+                mbar_expect_tx(&bar[s], 3 * BOX * 8);
+                tma_load_3d(d, pmap, tx0, ty0, tt, &bar[s]);
+                tma_load_3d(d + BOX, &maps->r, tx0, ty0, tt, &bar[s]);
+                tma_load_3d(d + 2 * BOX, &maps->w, tx0, ty0, tt, &bar[s]);
+            }
+        } else {
+            mbar_expect_tx(&bar[s], 2 * BOX * 8);
+            tma_load_3d(d + BOX, &maps->r, tx0, ty0, tt, &bar[s]);
+            tma_load_3d(d + 2 * BOX, &maps->w, tx0, ty0, tt, &bar[s]);
+        }
+    }
+
+    template <int PH, bool MASK>
+    __device__ __forceinline__ void step(int t)
+    {
+        // ---- level 0 from the TMA stage of plane t
+        double q0[RY];
+        if (t < b1) {
+            const int s = (t - t0) % NS;
+            mbar_wait(&bar[s], ((t - t0) / NS) & 1);
+            const double* d = stg + (size_t)s * 3 * BOX + ey0 * EX + lane;
+#pragma unroll
+            for (int r = 0; r < RY; ++r) {
+                double v;
+                if (MODE == MODE_PLAIN) {
+                    v = d[r * EX];
+                } else if (MODE == MODE_P) {
+                    const double pv = d[r * EX];
+                    v = first ? pv : d[BOX + r * EX] + beta * (pv - omega * d[2 * BOX + r * EX]);
+                } else {
+                    v = d[BOX + r * EX] - alpha * d[2 * BOX + r * EX];
+                }
+                if (MASK) v = in_dom[r] ? v : 0.0;
+                q0[r] = v;
+                if (MODE != MODE_PLAIN && in_tile[r] && t >= c0 && t < c1)
+                    side[col[r] + plane * t] = v;
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < RY; ++r) q0[r] = 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < RY; ++r) qw[PH % QW][r] = q0[r];
+        const double* prev = sm + S::PAD + ((t - 1) & 1) * (K * PLANE);
+#pragma unroll
+        for (int j = 1; j <= K; ++j) {
+            const int m = t - j;
+            if (wdy <= K - j) {                       // warp-uniform level skip
+                const double* pl = prev + (j - 1) * PLANE + ey0 * EX + lane;
+                bool mok = true;
+                if (MASK) mok = (unsigned)(m - b0) < (unsigned)(b1 - b0);
+                double v[RY];
+#pragma unroll
+                for (int r = 0; r < RY; ++r) {
+                    double zm, zc, zp, yc_m, yc_p;
+                    if (j == 1) {
+                        zp = qw[PH % QW][r];
+                        zc = qw[(PH + QW - 1) % QW][r];
+                        zm = qw[(PH + QW - 2) % QW][r];
+                        yc_m = r > 0 ? qw[(PH + QW - 1) % QW][r > 0 ? r - 1 : 0] : pl[(r - 1) * EX];
+                        yc_p = r < RY - 1 ? qw[(PH + QW - 1) % QW][r < RY - 1 ? r + 1 : 0]
+                                          : pl[(r + 1) * EX];
+                    } else {
+                        zp = win[j - 1][PH % 3][r];
+                        zc = win[j - 1][(PH + 2) % 3][r];
+                        zm = win[j - 1][(PH + 1) % 3][r];
+                        yc_m = r > 0 ? win[j - 1][(PH + 2) % 3][r > 0 ? r - 1 : 0] : pl[(r - 1) * EX];
+                        yc_p = r < RY - 1 ? win[j - 1][(PH + 2) % 3][r < RY - 1 ? r + 1 : 0]
+                                          : pl[(r + 1) * EX];
+                    }
+                    const double xm = pl[r * EX - 1], xp = pl[r * EX + 1];
+                    const double Sv =
+                        (6.0 * zc - (((((xm + xp) + yc_m) + yc_p) + zm) + zp)) * a->h2inv;
+                    const double qc = qw[(PH + QW - j) % QW][r];
+                    double vv;
+                    if (j == 1) {
+                        vv = a->g1 * ((2.0 * qc) - (Sv * a->cz));
+                    } else {
+                        const double z2 = (j == 2) ? qc * a->cz : win[j - 2][(PH + 1) % 3][r];
+                        vv = a->rho[j] *
+                             (((a->A2 * zc) + (a->B2 * (qc - Sv))) - (a->rho[j - 1] * z2));
+                    }
+                    if (MASK) vv = (((actmask[r] >> j) & 1u) && mok) ? vv : 0.0;
+                    v[r] = vv;
+                }
+#pragma unroll
+                for (int r = 0; r < RY; ++r) {
+                    if (j < K) win[j][PH % 3][r] = v[r];
+                    else if (in_tile[r] && m >= c0 && m < c1) a->out[col[r] + plane * m] = v[r];
+                }
+            }
+        }
+        double* cur = sm + S::PAD + (t & 1) * (K * PLANE) + ey0 * EX + lane;
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+            cur[r * EX] = q0[r];
+#pragma unroll
+            for (int j = 1; j < K; ++j) cur[j * PLANE + r * EX] = win[j][PH % 3][r];
+        }
+        __syncthreads();
+        // the stage of plane t is free again: refill it with plane t + NS
+        if (threadIdx.x == 0 && t + NS < b1 && t + NS <= t1) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(t + NS);
+        }
+    }
+
+    // steps [tb, te) (te - tb a multiple of U unless FULL == false)
+    template <bool MASK>
+    __device__ __forceinline__ void run_blocks(int tb, int nblk)
+    {
+        constexpr int U = QW;
+        for (int b = 0; b < nblk; ++b, tb += U) {
+            step<0, MASK>(tb);
+            step<1 % U, MASK>(tb + 1);
+            step<2 % U, MASK>(tb + 2);
+            if (U > 3) {
+                step<3 % U, MASK>(tb + 3);
+                step<4 % U, MASK>(tb + 4);
+                step<5 % U, MASK>(tb + 5);
+            }
+            if (U > 6) {
+                step<6 % U, MASK>(tb + 6);
+                step<7 % U, MASK>(tb + 7);
+                step<8 % U, MASK>(tb + 8);
+            }
+        }
+    }
+
+    // remainder of < U steps starting at phase 0
+    __device__ __forceinline__ void run_tail(int t, int n)
+    {
+        constexpr int U = QW;
+        if (n > 0) step<0, true>(t);
+        if (n > 1) step<1 % U, true>(t + 1);
+        if (U > 3) {
+            if (n > 2) step<2 % U, true>(t + 2);
+            if (n > 3) step<3 % U, true>(t + 3);
+            if (n > 4) step<4 % U, true>(t + 4);
+        }
+        if (U > 6) {
+            if (n > 5) step<5 % U, true>(t + 5);
+            if (n > 6) step<6 % U, true>(t + 6);
+            if (n > 7) step<7 % U, true>(t + 7);
+        }
+    }
+};
+
+template <int K, int RY, int NW, int NS, int MODE>
+__global__ void __launch_bounds__(NW * 32, 1) k_cheb_tb4(const __grid_constant__ TbArgs a,
+                                                       const __grid_constant__ TbMaps maps)
+{
+    using T = Tb4Thread<K, RY, NW, NS, MODE>;
+    using S = Tb4Shape<K, RY, NW, NS>;
+    constexpr int TX = S::TX, TY = S::TY, U = S::QW;
+    extern __shared__ __align__(128) double smraw[];
+
+    const DevState* st = a.st;
+    if (st && st->done) return;
+    T th;
+    th.a = &a;
+    th.maps = &maps;
+    th.stg = smraw;                                              // 128-B aligned TMA boxes
+    th.sm = smraw + (size_t)NS * 3 * S::BOX;
+    th.bar = reinterpret_cast<uint64_t*>(th.sm + 2 * K * S::PLANE);
+    th.alpha = th.beta = th.omega = 0.0;
+    th.first = false;
+    th.pmap = nullptr;
+    th.side = nullptr;
+    if (MODE == MODE_P) {
+        const int par = st->iter & 1;
+        th.first = (st->iter == 0);
+        th.beta = st->beta;
+        th.omega = st->omega;
+        th.pmap = par ? &maps.pb : &maps.pa;
+        th.side = par ? a.side_a : a.side_b;
+    } else if (MODE == MODE_S) {
+        th.alpha = st->alpha;
+        th.side = a.side_a;
+    }
+    const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
+    th.lane = lane;
+    th.ey0 = wy * RY;
+    th.tx0 = blockIdx.x * TX - K;
+    th.ty0 = blockIdx.y * TY - K;
+    const int gx = th.tx0 + lane;
+    const int dx = max(K - lane, lane - (K + TX - 1));
+    int wdy = 1 << 20;
+#pragma unroll
+    for (int r = 0; r < RY; ++r) {
+        const int ey = th.ey0 + r;
+        const int gy = th.ty0 + ey;
+        const int dy = max(K - ey, ey - (K + TY - 1));
+        wdy = min(wdy, dy);
+        const int dist = max(dx, dy);
+        th.in_dom[r] = gx >= 0 && gx < a.nx && gy >= 0 && gy < a.ny;
+        th.in_tile[r] = th.in_dom[r] && dist <= 0;
+        th.col[r] = th.in_dom[r] ? gx + (int64_t)a.nx * gy : 0;
+        unsigned msk = 0;
+#pragma unroll
+        for (int j = 1; j <= K; ++j)
+            if (th.in_dom[r] && dist <= K - j) msk |= 1u << j;
+        th.actmask[r] = msk;
+    }
+    th.wdy = wdy;
+    const int blk = blockIdx.z / a.nchunk, ch = blockIdx.z % a.nchunk;
+    th.b0 = blk * a.Lb;
+    th.b1 = th.b0 + a.Lb;
+    th.c0 = th.b0 + ch * a.zch;
+    th.c1 = min(th.b1, th.c0 + a.zch);
+    if (th.c0 >= th.b1) return;
+    th.t0 = max(th.b0, th.c0 - K);
+    th.t1 = th.c1 - 1 + K;
+    th.plane = (int64_t)a.nx * a.ny;
+#pragma unroll
+    for (int d = 0; d < S::QW; ++d)
+#pragma unroll
+        for (int r = 0; r < RY; ++r) th.qw[d][r] = 0.0;
+#pragma unroll
+    for (int j = 0; j < (K > 1 ? K : 2); ++j)
+#pragma unroll
+        for (int r = 0; r < RY; ++r) th.win[j][0][r] = th.win[j][1][r] = th.win[j][2][r] = 0.0;
+    for (int i = threadIdx.x; i < 2 * K * S::PLANE; i += blockDim.x) th.sm[i] = 0.0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(&th.bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int tt = th.t0; tt < th.t0 + NS && tt < th.b1 && tt <= th.t1; ++tt) th.issue(tt);
+
+    // interior tile: the extended tile lies inside the grid -> masks only near block ends
+    const bool interior = th.tx0 >= 0 && th.tx0 + 32 <= a.nx && th.ty0 >= 0 &&
+                          th.ty0 + S::EY <= a.ny;
+    const int nsteps = th.t1 - th.t0 + 1;
+    const int NB = nsteps / U, tail = nsteps - NB * U;
+    int t = th.t0;
+    if (interior) {
+        // masked prologue while a level's plane is below the block (t - K < b0), masked
+        // epilogue once planes beyond the block appear (t >= b1); unmasked in between.
+        const int pro_end = max(th.t0, th.b0 + K);          // first step that may be unmasked
+        const int epi_beg = min(th.t1 + 1, th.b1);          // first step that must be masked
+        const int npro = min(NB, (pro_end - th.t0 + U - 1) / U);
+        th.template run_blocks<true>(t, npro);
+        t += npro * U;
+        const int nmid = max(0, min(NB - npro, (epi_beg - t) / U));
+        th.template run_blocks<false>(t, nmid);
+        t += nmid * U;
+        th.template run_blocks<true>(t, NB - npro - nmid);
+        t += (NB - npro - nmid) * U;
+    } else {
+        th.template run_blocks<true>(t, NB);
+        t += NB * U;
+    }
+    th.run_tail(t, tail);
+}
+
+}  // namespace fused
