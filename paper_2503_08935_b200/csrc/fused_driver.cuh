@@ -155,7 +155,9 @@ void variant_tile(int variant, int k, int* tx, int* ty)
     if (variant == 2 || k > 5) {
         *tx = 32; *ty = 16;
         if (k >= 7) { *tx = 16; *ty = 8; } else if (k >= 5) { *tx = 32; *ty = 8; }
-    } else if (variant == 4 || variant == 5) {
+    } else if (variant == 5) {
+        *tx = 32 - 2 * ((k + 1) / 2 * 2); *ty = 32 - 2 * k;   // TMA: even x-halo
+    } else if (variant == 4) {
         *tx = 32 - 2 * k; *ty = 32 - 2 * k;      // RY = 4, NW = 8
     } else {
         *tx = 32 - 2 * k; *ty = 32 - 2 * k;      // RY = 2, NW = 16

@@ -59,7 +59,10 @@ struct TbMaps {
 
 template <int K, int RY, int NW, int NS>
 struct Tb4Shape {
-    static constexpr int EX = 32, EY = NW * RY, TX = EX - 2 * K, TY = EY - 2 * K;
+    // x-halo HX = K rounded up to even: TMA needs 16-byte aligned box starts, so the first
+    // staged column (tile x0 - HX) must be even.  For odd K the outermost column is unused.
+    static constexpr int HX = (K + 1) / 2 * 2;
+    static constexpr int EX = 32, EY = NW * RY, TX = EX - 2 * HX, TY = EY - 2 * K;
     static constexpr int PAD = EX;
     static constexpr int PLANE = EX * EY + 2 * PAD;       // level plane incl. guard rows
     static constexpr int BOX = EX * EY;                   // staged input box (doubles)
@@ -287,10 +290,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_cheb_tb4(const __grid_constant__
     const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
     th.lane = lane;
     th.ey0 = wy * RY;
-    th.tx0 = blockIdx.x * TX - K;
+    constexpr int HX = S::HX;
+    th.tx0 = blockIdx.x * TX - HX;
     th.ty0 = blockIdx.y * TY - K;
     const int gx = th.tx0 + lane;
-    const int dx = max(K - lane, lane - (K + TX - 1));
+    const int dx = max(HX - lane, lane - (HX + TX - 1));
     int wdy = 1 << 20;
 #pragma unroll
     for (int r = 0; r < RY; ++r) {
