@@ -9,8 +9,8 @@
  * written independently from the paper and from the arithmetic contract in DESIGN.md §3.
  *
  * Style: plain loops, one stencil sweep per pass, one vector operation per pass, fp64,
- * compiled with -ffp-contract=off (no FMA contraction; fma() appears only in TwoProd, where
- * it is exact by construction).  OpenMP is used only over z-planes of element-wise passes
+ * compiled with -ffp-contract=off: the compiler contracts nothing; the contract's fused
+ * multiply-adds (DESIGN.md §3 R17/R18/R20, and Dot2's TwoProd) are written as explicit fma().  OpenMP is used only over z-planes of element-wise passes
  * (order-independent) and for per-plane dot partials that are combined in ascending z.
  *
  * Citations: "P:n" = line n of the paper's LaTeX source.  Section / equation /
@@ -89,7 +89,7 @@ void orc_fold_boundary(int64_t nx, int64_t ny, int64_t nz, double h, const doubl
 /* ------------------------------------------------------------------------------------------
  * The operator.  P:95-100 (Eq. 6): P = I⊗I⊗D_x/Δx² + I⊗D_y/Δy²⊗I + D_z/Δz²⊗I⊗I with D from
  * Eq. 4.  With uniform spacing h the row for unknown c reads
- *     (A v)_c = (6 v_c - (((((v_xm + v_xp) + v_ym) + v_yp) + v_zm) + v_zp)) * h2inv,
+ *     (A v)_c = fma(6, v_c, -(((((v_xm + v_xp) + v_ym) + v_yp) + v_zm) + v_zp)) * h2inv,
  * h2inv = 1/(h*h), out-of-domain neighbours = +0.0 (homogeneous Dirichlet).
  * nslab > 1 gives the block-diagonal operator Σ_s R_s^T (R_s A R_s^T) R_s of Eq. 12-14
  * (P:185-205): z is cut into nslab equal slabs and neighbours across a cut are also +0.0.
@@ -115,7 +115,7 @@ void orc_apply_A(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab,
                 double zm = cut_lo ? 0.0 : v[c - pl];
                 double zp = cut_hi ? 0.0 : v[c + pl];
                 double nb = ((((xm + xp) + ym) + yp) + zm) + zp;
-                out[c] = (6.0 * v[c] - nb) * h2inv;
+                out[c] = fma(6.0, v[c], -nb) * h2inv;      /* (6 v_c - nb) / h^2, R17 */
             }
     }
 }
@@ -260,7 +260,7 @@ int orc_apply_cheb(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, 
 #pragma omp parallel for schedule(static)
     for (int64_t c = 0; c < n; ++c) {
         z[c] = q[c] * cz;
-        y[c] = g1 * ((2.0 * q[c]) - (S[c] * cz));
+        y[c] = g1 * fma(-S[c], cz, 2.0 * q[c]);     /* g1 (2b - (A b) cz), R18 */
     }
     /* KernelCI2 for i = 2..iterMax, with the pointer swaps of P:361-362 */
     for (int j = 2; j <= k; ++j) {
@@ -268,7 +268,7 @@ int orc_apply_cheb(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, 
         double rc_ = rho[j], ro_ = rho[j - 1];
 #pragma omp parallel for schedule(static)
         for (int64_t c = 0; c < n; ++c)
-            w[c] = rc_ * (((A2 * y[c]) + (B2 * (q[c] - S[c]))) - (ro_ * z[c]));
+            w[c] = rc_ * fma(-ro_, z[c], fma(A2, y[c], B2 * (q[c] - S[c])));   /* R18 */
         double* tmp = z; z = y; y = w; w = tmp;   /* z <- y, y <- w */
     }
     /* KernelCI3: x = w (after the swap, the last w is in y) */
@@ -375,7 +375,7 @@ int orc_bicgstab(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, in
         if (sc) sc[1] = alpha;
         /* KernelBiCGS2: r = r - α w   (the half-step residual, "s") */
 #pragma omp parallel for schedule(static)
-        for (int64_t c = 0; c < n; ++c) r[c] = r[c] - alpha * w[c];
+        for (int64_t c = 0; c < n; ++c) r[c] = fma(-alpha, w[c], r[c]);
         /* solve M r̂ = r */
         if (pc == 0) memcpy(rh, r, sizeof(double) * (size_t)n);
         else orc_apply_cheb(nx, ny, nz, h, nslab, k, a_iv, b_iv, r, rh);
@@ -387,10 +387,10 @@ int orc_bicgstab(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, in
         if (sc) { sc[2] = ts; sc[3] = tt; sc[4] = omega; }
         /* KernelBiCGS4: x = x + α p̂ + ω r̂ */
 #pragma omp parallel for schedule(static)
-        for (int64_t c = 0; c < n; ++c) x[c] = (x[c] + alpha * ph[c]) + omega * rh[c];
+        for (int64_t c = 0; c < n; ++c) x[c] = fma(omega, rh[c], fma(alpha, ph[c], x[c]));
         /* KernelBiCGS5: r = r - ω t, r0ᵀr, rᵀr; MPI5 */
 #pragma omp parallel for schedule(static)
-        for (int64_t c = 0; c < n; ++c) r[c] = r[c] - omega * t[c];
+        for (int64_t c = 0; c < n; ++c) r[c] = fma(-omega, t[c], r[c]);
         double rho_new = orc_dot(pl, nz, rt, r);
         double rr = orc_dot(pl, nz, r, r);
         double rel = sqrt(rr) / nb;
@@ -414,7 +414,7 @@ int orc_bicgstab(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, in
         if (sc) sc[7] = beta;
         /* KernelBiCGS6: p = r + β (p - ω w) */
 #pragma omp parallel for schedule(static)
-        for (int64_t c = 0; c < n; ++c) p[c] = r[c] + beta * (p[c] - omega * w[c]);
+        for (int64_t c = 0; c < n; ++c) p[c] = fma(beta, fma(-omega, w[c], p[c]), r[c]);
     }
 done:
     *iters_out = it;

@@ -34,8 +34,8 @@ __global__ void k_update_xr_s(double* __restrict__ x, const double* __restrict__
     double p[2] = {0.0, 0.0}, q[2] = {0.0, 0.0};
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
          c += (int64_t)gridDim.x * blockDim.x) {
-        x[c] = (x[c] + alpha * ph[c]) + omega * rh[c];
-        const double rn = s[c] - omega * t[c];
+        x[c] = upd_x(x[c], ph[c], rh[c], alpha, omega);
+        const double rn = upd_r(s[c], t[c], omega);
         r[c] = rn;
         dot2_acc(p[0], q[0], rt[c], rn);
         dot2_acc(p[1], q[1], rn, rn);

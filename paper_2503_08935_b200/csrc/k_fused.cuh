@@ -16,6 +16,7 @@
 #pragma once
 #include <stdint.h>
 
+#include "expr.cuh"
 #include "state.cuh"
 
 namespace fused {
@@ -96,8 +97,8 @@ struct TbThread {
         double q0 = 0.0;
         if (in_dom && t < b1) {
             if (MODE == MODE_PLAIN) q0 = nr;
-            else if (MODE == MODE_P) q0 = first ? np : nr + beta * (np - omega * nw);
-            else q0 = nr - alpha * nw;
+            else if (MODE == MODE_P) q0 = first ? np : upd_p(nr, np, nw, beta, omega);
+            else q0 = upd_s(nr, nw, alpha);
             if (MODE != MODE_PLAIN && in_tile && t >= c0 && t < c1) side[col + plane * t] = q0;
         }
         load(t + 1);
@@ -120,14 +121,14 @@ struct TbThread {
                 zc = win[j - 1][(PH + 2) % 3];
                 zm = win[j - 1][(PH + 1) % 3];
             }
-            const double Sv = (6.0 * zc - (((((xm + xp) + ym) + yp) + zm) + zp)) * a->h2inv;
+            const double Sv = stencil_row(zc, xm, xp, ym, yp, zm, zp, a->h2inv);
             const double qc = qw[(PH + QW - j) % QW];
             double v;
             if (j == 1) {
-                v = a->g1 * ((2.0 * qc) - (Sv * a->cz));
+                v = cheb_first(qc, Sv, a->g1, a->cz);
             } else {
                 const double z2 = (j == 2) ? qc * a->cz : win[j - 2][(PH + 1) % 3];
-                v = a->rho[j] * (((a->A2 * zc) + (a->B2 * (qc - Sv))) - (a->rho[j - 1] * z2));
+                v = cheb_step(qc, Sv, zc, z2, a->rho[j], a->rho[j - 1], a->A2, a->B2);
             }
             const bool act = ((actmask >> j) & 1u) && (unsigned)(m - b0) < (unsigned)(b1 - b0);
             v = act ? v : 0.0;
@@ -302,8 +303,8 @@ struct Tb3Thread {
             q0[r] = 0.0;
             if (in_dom[r] && t < b1) {
                 if (MODE == MODE_PLAIN) q0[r] = nr[r];
-                else if (MODE == MODE_P) q0[r] = first ? np[r] : nr[r] + beta * (np[r] - omega * nw[r]);
-                else q0[r] = nr[r] - alpha * nw[r];
+                else if (MODE == MODE_P) q0[r] = first ? np[r] : upd_p(nr[r], np[r], nw[r], beta, omega);
+                else q0[r] = upd_s(nr[r], nw[r], alpha);
                 if (MODE != MODE_PLAIN && in_tile[r] && t >= c0 && t < c1)
                     side[col[r] + plane * t] = q0[r];
             }
@@ -339,16 +340,14 @@ struct Tb3Thread {
                                           : pl[(r + 1) * EX];
                     }
                     const double xm = pl[r * EX - 1], xp = pl[r * EX + 1];
-                    const double Sv =
-                        (6.0 * zc - (((((xm + xp) + yc_m) + yc_p) + zm) + zp)) * a->h2inv;
+                    const double Sv = stencil_row(zc, xm, xp, yc_m, yc_p, zm, zp, a->h2inv);
                     const double qc = qw[(PH + QW - j) % QW][r];
                     double vv;
                     if (j == 1) {
-                        vv = a->g1 * ((2.0 * qc) - (Sv * a->cz));
+                        vv = cheb_first(qc, Sv, a->g1, a->cz);
                     } else {
                         const double z2 = (j == 2) ? qc * a->cz : win[j - 2][(PH + 1) % 3][r];
-                        vv = a->rho[j] *
-                             (((a->A2 * zc) + (a->B2 * (qc - Sv))) - (a->rho[j - 1] * z2));
+                        vv = cheb_step(qc, Sv, zc, z2, a->rho[j], a->rho[j - 1], a->A2, a->B2);
                     }
                     const bool act = ((actmask[r] >> j) & 1u) && mok;
                     v[r] = act ? vv : 0.0;

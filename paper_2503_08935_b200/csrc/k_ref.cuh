@@ -7,6 +7,7 @@
 // z-neighbours).  Stencil (R17): (6 c - (((((xm+xp)+ym)+yp)+zm)+zp)) * h2inv.
 #pragma once
 #include "dd.cuh"
+#include "expr.cuh"
 #include "state.cuh"
 
 namespace ref {
@@ -66,8 +67,7 @@ __device__ __forceinline__ double stencil_at(const double* __restrict__ v, int64
     const double xp = (i < nx - 1) ? v[c + 1] : 0.0;
     const double ym = (j > 0) ? v[c - nx] : 0.0;
     const double yp = (j < ny - 1) ? v[c + nx] : 0.0;
-    const double nb = ((((xm + xp) + ym) + yp) + vzm) + vzp;
-    return (6.0 * v[c] - nb) * h2inv;
+    return stencil_row(v[c], xm, xp, ym, yp, vzm, vzp, h2inv);
 }
 
 // ------------------------------------------------------------------- a4 / a9 (+ apply_A)
@@ -140,10 +140,10 @@ __global__ void __launch_bounds__(BX * BY) k_cheb_sweep(const double* __restrict
         const double qc = q[c];
         double o;
         if (first) {
-            o = cc.g1 * ((2.0 * qc) - (S * cc.cz));
+            o = cheb_first(qc, S, cc.g1, cc.cz);
         } else {
             const double zc = x2 ? x2[c] : qc * cc.cz;
-            o = rho_j * (((cc.A2 * v[c]) + (cc.B2 * (qc - S))) - (rho_jm1 * zc));
+            o = cheb_step(qc, S, v[c], zc, rho_j, rho_jm1, cc.A2, cc.B2);
         }
         out[c] = o;
     }
@@ -195,7 +195,7 @@ __global__ void k_axpy_s(double* __restrict__ r, const double* __restrict__ w, i
 {
     if (st->done) return;
     const double alpha = st->alpha;
-    EW_LOOP(n) r[c] = r[c] - alpha * w[c];
+    EW_LOOP(n) r[c] = upd_s(r[c], w[c], alpha);
 }
 
 // a11 + a12, KernelBiCGS4/5: x = (x + α p̂) + ω r̂; r = s - ω t;
@@ -210,8 +210,8 @@ __global__ void k_update_xr(double* __restrict__ x, const double* __restrict__ p
     double p[2] = {0.0, 0.0}, s[2] = {0.0, 0.0};
     EW_LOOP(n)
     {
-        x[c] = (x[c] + alpha * ph[c]) + omega * rh[c];
-        const double rn = r[c] - omega * t[c];
+        x[c] = upd_x(x[c], ph[c], rh[c], alpha, omega);
+        const double rn = upd_r(r[c], t[c], omega);
         r[c] = rn;
         dot2_acc(p[0], s[0], rt[c], rn);
         dot2_acc(p[1], s[1], rn, rn);
@@ -226,7 +226,7 @@ __global__ void k_update_p(double* __restrict__ p, const double* __restrict__ r,
 {
     if (st->done) return;
     const double beta = st->beta, omega = st->omega;
-    EW_LOOP(n) p[c] = r[c] + beta * (p[c] - omega * w[c]);
+    EW_LOOP(n) p[c] = upd_p(r[c], p[c], w[c], beta, omega);
 }
 
 }  // namespace ref

@@ -135,9 +135,9 @@ struct Tb4Thread {
                     v = d[r * EX];
                 } else if (MODE == MODE_P) {
                     const double pv = d[r * EX];
-                    v = first ? pv : d[BOX + r * EX] + beta * (pv - omega * d[2 * BOX + r * EX]);
+                    v = first ? pv : upd_p(d[BOX + r * EX], pv, d[2 * BOX + r * EX], beta, omega);
                 } else {
-                    v = d[BOX + r * EX] - alpha * d[2 * BOX + r * EX];
+                    v = upd_s(d[BOX + r * EX], d[2 * BOX + r * EX], alpha);
                 }
                 if (MASK) v = in_dom[r] ? v : 0.0;
                 q0[r] = v;
@@ -178,16 +178,14 @@ struct Tb4Thread {
                                           : pl[(r + 1) * EX];
                     }
                     const double xm = pl[r * EX - 1], xp = pl[r * EX + 1];
-                    const double Sv =
-                        (6.0 * zc - (((((xm + xp) + yc_m) + yc_p) + zm) + zp)) * a->h2inv;
+                    const double Sv = stencil_row(zc, xm, xp, yc_m, yc_p, zm, zp, a->h2inv);
                     const double qc = qw[(PH + QW - j) % QW][r];
                     double vv;
                     if (j == 1) {
-                        vv = a->g1 * ((2.0 * qc) - (Sv * a->cz));
+                        vv = cheb_first(qc, Sv, a->g1, a->cz);
                     } else {
                         const double z2 = (j == 2) ? qc * a->cz : win[j - 2][(PH + 1) % 3][r];
-                        vv = a->rho[j] *
-                             (((a->A2 * zc) + (a->B2 * (qc - Sv))) - (a->rho[j - 1] * z2));
+                        vv = cheb_step(qc, Sv, zc, z2, a->rho[j], a->rho[j - 1], a->A2, a->B2);
                     }
                     if (MASK) vv = (((actmask[r] >> j) & 1u) && mok) ? vv : 0.0;
                     v[r] = vv;
