@@ -22,33 +22,53 @@ def sources():
                   [os.path.join(ROOT, "include", "bcgs.h")])
 
 
-def nvcc_cmd(out: str) -> list[str]:
-    nccl = nccl_dir()
-    return ["nvcc", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-            # R17: no FMA contraction anywhere (bitwise parity with the oracle)
-            "--fmad=false", "-std=c++17",
-            "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v", "-shared",
-            "-o", out, SRC,
-            "-I", os.path.join(nccl, "include"), "-L", os.path.join(nccl, "lib"),
-            "-l:libnccl.so.2", "-Xlinker", "-rpath," + os.path.join(nccl, "lib")]
+CU_SOURCES = ["bcgs_api.cu"] + [f"tb_k{k}.cu" for k in range(1, 9)]
+NVCC_FLAGS = ["-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+              # R17: no FMA contraction except the contract's explicit fma()
+              "--fmad=false", "-std=c++17",
+              "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v"]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, jobs: int = 0) -> str:
+    """Compile the translation units in parallel, link libbcgs.so (in-tree)."""
+    import concurrent.futures as cf
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     newest = max(os.path.getmtime(p) for p in sources())
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = nvcc_cmd(tmp)
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    nccl = nccl_dir()
+    objdir = os.path.join(PKG, "lib", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    inc = ["-I", os.path.join(nccl, "include")]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmd = ["nvcc", *NVCC_FLAGS, *inc, "-c", "-o", obj, os.path.join(PKG, "csrc", src)]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, cmd, r
+
+    jobs = jobs or min(len(CU_SOURCES), os.cpu_count() or 4)
+    with cf.ThreadPoolExecutor(jobs) as ex:
+        results = list(ex.map(compile_one, CU_SOURCES))
     log = os.path.join(PKG, "lib", "ptxas.log")
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        for src, obj, cmd, r in results:
+            f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+    bad = [r for r in results if r[3].returncode != 0]
+    if bad:
+        for src, obj, cmd, r in bad:
+            sys.stderr.write(f"--- {src}\n" + r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed building libbcgs.so (see %s)" % log)
+    tmp = LIB + f".tmp{os.getpid()}"
+    link = ["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp,
+            *[r[1] for r in results], "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2",
+            "-Xlinker", "-rpath," + os.path.join(nccl, "lib")]
+    r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libbcgs.so (see %s)" % log)
+        raise RuntimeError("link of libbcgs.so failed")
     if verbose:
-        sys.stdout.write(r.stderr)
+        sys.stdout.write(open(log).read())
     os.replace(tmp, LIB)
     return LIB
 

@@ -1,0 +1,160 @@
+// ctx.cuh -- solver context, workspace layout and error plumbing shared by every
+// translation unit of libbcgs.so (bcgs_api.cu = driver, tb_k*.cu = blocked kernels).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bcgs.h"
+#include "dd.cuh"
+#include "state.cuh"
+#include "ref_shapes.cuh"
+#include "k_fused.cuh"
+
+constexpr int kNumSMs = 148;
+constexpr int kEwBlocks = kNumSMs * 8;   // element-wise grid: fixed -> deterministic partials
+constexpr size_t kAlign = 256;
+
+enum KClass {
+    KC_PRECOND = 0, KC_STENCIL1, KC_AXPY, KC_STENCIL2, KC_UPDATE_XR, KC_UPDATE_P,
+    KC_FINALIZE, KC_HALO, KC_ALLGATHER, KC_SCALARS, KC_FUSED_P1, KC_FUSED_P2, KC_FUSED_XR,
+    KC_COUNT
+};
+inline const char* kClassName[KC_COUNT] = {
+    "precond_sweep", "stencil_dot1", "axpy_s", "stencil_dot2", "update_xr", "update_p",
+    "finalize", "halo", "allgather", "scalars", "fused_p_cheb", "fused_s_cheb", "fused_xr"};
+
+inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+struct Layout {
+    int64_t nx, ny, nz, L, plane, vec_elems;   // vec_elems = (L + 2) * plane
+    int64_t n_part;
+    size_t off_vec[16];
+    size_t off_state, off_hist, off_scal, off_part, off_rank, off_gath, total;
+};
+
+constexpr int V_X = 0, V_R = 1, V_RT = 2, V_P = 3, V_PH = 4, V_RH = 5, V_W = 6, V_T = 7,
+              V_B = 8, V_C1 = 9, V_C2 = 10, V_IO = 11, V_W2 = 12, V_P2 = 13,
+              V_S = 14, V_COUNT = 15;
+
+inline int64_t stencil_blocks(int64_t nx, int64_t ny, int64_t L)
+{
+    return ((nx + ref::BX - 1) / ref::BX) * ((ny + ref::BY - 1) / ref::BY) *
+           ((L + ref::ZC - 1) / ref::ZC);
+}
+
+inline bool make_layout(const bcgs_grid_desc* g, int32_t nranks, Layout* lay)
+{
+    if (!g || nranks < 1) return false;
+    lay->nx = g->n[0];
+    lay->ny = g->n[1];
+    lay->nz = g->n[2];
+    if (lay->nx < 1 || lay->ny < 1 || lay->nz < 1 || lay->nz % nranks) return false;
+    lay->L = lay->nz / nranks;
+    lay->plane = lay->nx * lay->ny;
+    lay->vec_elems = (lay->L + 2) * lay->plane;
+    lay->n_part = std::max<int64_t>(
+        {stencil_blocks(lay->nx, lay->ny, lay->L), (int64_t)kEwBlocks, fused::max_blocks(lay->nx, lay->ny, lay->L)});
+    size_t off = 0;
+    for (int v = 0; v < V_COUNT; ++v) {
+        lay->off_vec[v] = off;
+        off = align_up(off + sizeof(double) * (size_t)lay->vec_elems);
+    }
+    lay->off_state = off; off = align_up(off + sizeof(DevState));
+    lay->off_hist = off;  off = align_up(off + sizeof(double) * (BCGS_HIST_CAP + 1));
+    lay->off_scal = off;  off = align_up(off + sizeof(double) * 8 * BCGS_HIST_CAP);
+    lay->off_part = off;  off = align_up(off + sizeof(dd) * 2 * (size_t)lay->n_part);
+    lay->off_rank = off;  off = align_up(off + sizeof(dd) * 2);
+    lay->off_gath = off;  off = align_up(off + sizeof(dd) * 2 * (size_t)nranks);
+    lay->total = off;
+    return true;
+}
+
+struct EvRec {
+    int cls;
+    cudaEvent_t a, b;
+    double bytes;
+};
+
+struct bcgs_ctx_s {
+    Layout lay;
+    double h = 0.0, h2inv = 0.0;
+    int rank = 0, nranks = 1, device = 0;
+    cudaStream_t user = nullptr, s = nullptr;
+    cudaEvent_t join = nullptr;
+    ncclComm_t comm = nullptr;
+    char* ws = nullptr;
+    double* vec[V_COUNT] = {};     // interior plane 0 of each field
+    DevState* st = nullptr;
+    double *hist = nullptr, *scal = nullptr;
+    dd *part = nullptr, *rank_out = nullptr, *gath = nullptr;
+    double* h_pinned = nullptr;    // small pinned buffer for flag polls
+    // options
+    int kernels = 1, use_graph = 0, profile = 0, poll = 8, tb_variant = 5;
+    // preconditioner
+    bcgs_pc pc = BCGS_PC_NONE;
+    int degree = 0, bpr = 1;
+    double c_min = 10.0, c_max = 1.0 - 1e-4, ov_a = 0.0, ov_b = 0.0;
+    double ivl[2] = {0, 0}, cst[7] = {}, rho[BCGS_MAX_DEGREE + 2] = {};
+    int have_x0 = 0;
+    double face[6] = {0, 0, 0, 0, 0, 0};
+    // solve bookkeeping
+    int begun = 0, launched = 0, fixed = 0, max_iter = 0;
+    double tol = 0.0;
+    std::chrono::steady_clock::time_point t0;
+    // graph
+    cudaGraphExec_t gexec = nullptr;
+    int graph_key = -1;
+    // profiling
+    std::vector<EvRec> pending;
+    std::vector<cudaEvent_t> free_ev;
+    double ktime[KC_COUNT] = {}, kbytes[KC_COUNT] = {};
+    int64_t kcalls[KC_COUNT] = {};
+    std::string err;
+};
+
+inline bcgs_status fail(bcgs_ctx c, bcgs_status s, const char* fmt, ...)
+{
+    if (c) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        c->err = buf;
+    }
+    return s;
+}
+
+#define CUDA_OK(c, call)                                                                    \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return fail((c), BCGS_E_CUDA, "%s failed: %s (%s:%d)", #call,                   \
+                        cudaGetErrorString(e_), __FILE__, __LINE__);                       \
+    } while (0)
+
+#define NCCL_OK(c, call)                                                                    \
+    do {                                                                                    \
+        ncclResult_t r_ = (call);                                                           \
+        if (r_ != ncclSuccess)                                                              \
+            return fail((c), BCGS_E_NCCL, "%s failed: %s", #call, ncclGetErrorString(r_)); \
+    } while (0)
+
+inline double* F(bcgs_ctx c, int v) { return c->vec[v]; }
+inline int64_t npts(bcgs_ctx c) { return c->lay.L * c->lay.plane; }
+
+#define TRY(x)                        \
+    do {                              \
+        bcgs_status s_ = (x);         \
+        if (s_ != BCGS_OK) return s_; \
+    } while (0)

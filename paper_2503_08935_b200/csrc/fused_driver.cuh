@@ -12,16 +12,6 @@
 
 namespace fused {
 
-template <int K> struct Tile;
-template <> struct Tile<1> { static constexpr int X = 32, Y = 16; };
-template <> struct Tile<2> { static constexpr int X = 32, Y = 16; };
-template <> struct Tile<3> { static constexpr int X = 32, Y = 16; };
-template <> struct Tile<4> { static constexpr int X = 32, Y = 16; };
-template <> struct Tile<5> { static constexpr int X = 32, Y = 8; };
-template <> struct Tile<6> { static constexpr int X = 32, Y = 8; };
-template <> struct Tile<7> { static constexpr int X = 16, Y = 8; };
-template <> struct Tile<8> { static constexpr int X = 16, Y = 8; };
-
 // a11 + a12 with s in its own buffer: x = (x + α p̂) + ω r̂; r = s - ω t; partials r~·r, r·r
 __global__ void k_update_xr_s(double* __restrict__ x, const double* __restrict__ ph,
                               const double* __restrict__ rh, const double* __restrict__ s,
@@ -43,136 +33,19 @@ __global__ void k_update_xr_s(double* __restrict__ x, const double* __restrict__
     block_reduce_dd<2>(p, q, part + (int64_t)blockIdx.x * 2);
 }
 
-template <int K, int MODE>
-bcgs_status launch_tb_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
-{
-    constexpr int TX = Tile<K>::X, TY = Tile<K>::Y;
-    using S = TbShape<K, TX, TY>;
-    auto kern = k_cheb_tb<K, TX, TY, MODE>;
-    static bool attr = false;
-    if (!attr) {
-        CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)S::smem));
-        attr = true;
-    }
-    dim3 grid((unsigned)((a.nx + TX - 1) / TX), (unsigned)((a.ny + TY - 1) / TY),
-              (unsigned)nchunk_total);
-    kern<<<grid, S::NT, S::smem, c->s>>>(a);
-    CUDA_OK(c, cudaGetLastError());
-    return BCGS_OK;
-}
-
-template <int K, int RY, int NW, int MODE>
-bcgs_status launch_tb3_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
-{
-    using S = Tb3Shape<K, RY, NW>;
-    auto kern = k_cheb_tb3<K, RY, NW, MODE>;
-    static bool attr = false;
-    if (!attr) {
-        CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)S::smem));
-        attr = true;
-    }
-    dim3 grid((unsigned)((a.nx + S::TX - 1) / S::TX), (unsigned)((a.ny + S::TY - 1) / S::TY),
-              (unsigned)nchunk_total);
-    kern<<<grid, NW * 32, S::smem, c->s>>>(a);
-    CUDA_OK(c, cudaGetLastError());
-    return BCGS_OK;
-}
-
-// ---- TMA tensor maps (cuTensorMapEncodeTiled through the runtime's driver entry point)
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn()
-{
-    static EncodeTiledFn fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-                cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = (EncodeTiledFn)p;
-    }
-    return fn;
-}
-
-// 3-D map over a slab field (nx, ny, L) of doubles, box (32, box_y, 1); OOB -> zeros
-bool make_map(CUtensorMap* m, const double* base, int64_t nx, int64_t ny, int64_t L, int box_y)
-{
-    EncodeTiledFn fn = encode_fn();
-    if (!fn || (nx * 8) % 16 || ((uintptr_t)base % 16)) return false;
-    cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)L};
-    cuuint64_t strides[2] = {(cuuint64_t)(nx * 8), (cuuint64_t)(nx * ny * 8)};
-    cuuint32_t box[3] = {32, (cuuint32_t)box_y, 1};
-    cuuint32_t es[3] = {1, 1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box,
-              es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
-           CUDA_SUCCESS;
-}
-
-bool tma_ok(bcgs_ctx c) { return encode_fn() != nullptr && c->lay.nx % 2 == 0; }
-
-template <int K, int RY, int NW, int NS, int MODE>
-bcgs_status launch_tb4_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
-{
-    using S = Tb4Shape<K, RY, NW, NS>;
-    auto kern = k_cheb_tb4<K, RY, NW, NS, MODE>;
-    static bool attr = false;
-    if (!attr) {
-        CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)S::smem));
-        attr = true;
-    }
-    TbMaps maps;
-    memset(&maps, 0, sizeof maps);
-    const int64_t nx = c->lay.nx, ny = c->lay.ny, L = c->lay.L;
-    bool ok = true;
-    if (MODE == MODE_PLAIN) ok = make_map(&maps.q, a.q, nx, ny, L, S::EY);
-    if (MODE != MODE_PLAIN) {
-        ok = make_map(&maps.r, a.r, nx, ny, L, S::EY) && make_map(&maps.w, a.w, nx, ny, L, S::EY);
-        if (MODE == MODE_P)
-            ok = ok && make_map(&maps.pa, a.p_a, nx, ny, L, S::EY) &&
-                 make_map(&maps.pb, a.p_b, nx, ny, L, S::EY);
-    }
-    if (!ok) return fail(c, BCGS_E_CUDA, "cuTensorMapEncodeTiled failed");
-    dim3 grid((unsigned)((a.nx + S::TX - 1) / S::TX), (unsigned)((a.ny + S::TY - 1) / S::TY),
-              (unsigned)nchunk_total);
-    kern<<<grid, NW * 32, S::smem, c->s>>>(a, maps);
-    CUDA_OK(c, cudaGetLastError());
-    return BCGS_OK;
-}
-
 // tile (TX, TY) of a kernel variant for degree k
 void variant_tile(int variant, int k, int* tx, int* ty)
 {
     if (variant == 2 || k > 5) {
         *tx = 32; *ty = 16;
         if (k >= 7) { *tx = 16; *ty = 8; } else if (k >= 5) { *tx = 32; *ty = 8; }
-    } else if (variant == 5) {
+    } else if (variant == 5 || variant == 6) {
         *tx = 32 - 2 * ((k + 1) / 2 * 2); *ty = 32 - 2 * k;   // TMA: even x-halo
     } else if (variant == 4) {
         *tx = 32 - 2 * k; *ty = 32 - 2 * k;      // RY = 4, NW = 8
     } else {
         *tx = 32 - 2 * k; *ty = 32 - 2 * k;      // RY = 2, NW = 16
     }
-}
-
-template <int K, int MODE>
-bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz)
-{
-    if constexpr (K <= 5) {   // register budget: warp-row layouts up to K = 5
-        if (c->tb_variant == 5 && tma_ok(c)) return launch_tb4_k<K, 2, 16, 4, MODE>(c, a, nz);
-        if (c->tb_variant == 4) return launch_tb3_k<K, 4, 8, MODE>(c, a, nz);
-        if (c->tb_variant == 3) return launch_tb3_k<K, 2, 16, MODE>(c, a, nz);
-    }
-    return launch_tb_k<K, MODE>(c, a, nz);
 }
 
 template <int MODE>
@@ -283,3 +156,4 @@ bcgs_status iteration(bcgs_ctx c)
 }
 
 }  // namespace fused
+

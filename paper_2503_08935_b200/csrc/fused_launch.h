@@ -1,0 +1,13 @@
+// fused_launch.h -- launch_variant<K, MODE> is defined in tb_launch.cuh and explicitly
+// instantiated once per degree K in tb_k<K>.cu (parallel compilation).
+#pragma once
+namespace fused {
+template <int K, int MODE>
+bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz);
+#define BCGS_TB_EXTERN(K)                                                  \
+    extern template bcgs_status launch_variant<K, 0>(bcgs_ctx, TbArgs&, int); \
+    extern template bcgs_status launch_variant<K, 1>(bcgs_ctx, TbArgs&, int); \
+    extern template bcgs_status launch_variant<K, 2>(bcgs_ctx, TbArgs&, int);
+BCGS_TB_EXTERN(1) BCGS_TB_EXTERN(2) BCGS_TB_EXTERN(3) BCGS_TB_EXTERN(4)
+BCGS_TB_EXTERN(5) BCGS_TB_EXTERN(6) BCGS_TB_EXTERN(7) BCGS_TB_EXTERN(8)
+}  // namespace fused

@@ -8,18 +8,10 @@
 #pragma once
 #include "dd.cuh"
 #include "expr.cuh"
+#include "ref_shapes.cuh"
 #include "state.cuh"
 
 namespace ref {
-
-constexpr int BX = 32, BY = 8, ZC = 16;   // stencil tile and z-chunk per CTA
-constexpr int EW_THREADS = 256;
-
-struct Grid {
-    int nx, ny, L;     // local extents (L = planes of this rank)
-    int Lb;            // preconditioner block thickness (L / blocks_per_rank)
-    double h2inv;
-};
 
 // ------------------------------------------------------------------- random RHS (R16)
 __global__ void k_rhs_random(double* __restrict__ b, int64_t n, int64_t g0, uint64_t seed)

@@ -1,0 +1,162 @@
+// tb_launch.cuh -- host launchers of the temporally blocked kernel variants.  Included
+// only by the per-degree translation units tb_k<K>.cu, which instantiate launch_variant<K,.>;
+// the driver (bcgs_api.cu) sees the extern declarations in fused_launch.h.
+#pragma once
+#include "ctx.cuh"
+
+namespace fused {
+
+template <int K> struct Tile;
+template <> struct Tile<1> { static constexpr int X = 32, Y = 16; };
+template <> struct Tile<2> { static constexpr int X = 32, Y = 16; };
+template <> struct Tile<3> { static constexpr int X = 32, Y = 16; };
+template <> struct Tile<4> { static constexpr int X = 32, Y = 16; };
+template <> struct Tile<5> { static constexpr int X = 32, Y = 8; };
+template <> struct Tile<6> { static constexpr int X = 32, Y = 8; };
+template <> struct Tile<7> { static constexpr int X = 16, Y = 8; };
+template <> struct Tile<8> { static constexpr int X = 16, Y = 8; };
+
+template <int K, int MODE>
+bcgs_status launch_tb_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
+{
+    constexpr int TX = Tile<K>::X, TY = Tile<K>::Y;
+    using S = TbShape<K, TX, TY>;
+    auto kern = k_cheb_tb<K, TX, TY, MODE>;
+    static bool attr = false;
+    if (!attr) {
+        CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)S::smem));
+        attr = true;
+    }
+    dim3 grid((unsigned)((a.nx + TX - 1) / TX), (unsigned)((a.ny + TY - 1) / TY),
+              (unsigned)nchunk_total);
+    kern<<<grid, S::NT, S::smem, c->s>>>(a);
+    CUDA_OK(c, cudaGetLastError());
+    return BCGS_OK;
+}
+
+template <int K, int RY, int NW, int MODE>
+bcgs_status launch_tb3_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
+{
+    using S = Tb3Shape<K, RY, NW>;
+    auto kern = k_cheb_tb3<K, RY, NW, MODE>;
+    static bool attr = false;
+    if (!attr) {
+        CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)S::smem));
+        attr = true;
+    }
+    dim3 grid((unsigned)((a.nx + S::TX - 1) / S::TX), (unsigned)((a.ny + S::TY - 1) / S::TY),
+              (unsigned)nchunk_total);
+    kern<<<grid, NW * 32, S::smem, c->s>>>(a);
+    CUDA_OK(c, cudaGetLastError());
+    return BCGS_OK;
+}
+
+// ---- TMA tensor maps (cuTensorMapEncodeTiled through the runtime's driver entry point)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline EncodeTiledFn encode_fn()
+{
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)p;
+    }
+    return fn;
+}
+
+// 3-D map over a slab field (nx, ny, L) of doubles, box (32, box_y, 1); OOB -> zeros
+inline bool make_map(CUtensorMap* m, const double* base, int64_t nx, int64_t ny, int64_t L, int box_y)
+{
+    EncodeTiledFn fn = encode_fn();
+    if (!fn || (nx * 8) % 16 || ((uintptr_t)base % 16)) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)L};
+    cuuint64_t strides[2] = {(cuuint64_t)(nx * 8), (cuuint64_t)(nx * ny * 8)};
+    cuuint32_t box[3] = {32, (cuuint32_t)box_y, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box,
+              es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
+}
+
+inline bool tma_ok(bcgs_ctx c) { return encode_fn() != nullptr && c->lay.nx % 2 == 0; }
+
+inline bool make_maps(bcgs_ctx c, TbMaps* maps, const TbArgs& a, int mode, int box_y)
+{
+    memset(maps, 0, sizeof *maps);
+    const int64_t nx = c->lay.nx, ny = c->lay.ny, L = c->lay.L;
+    if (mode == MODE_PLAIN) return make_map(&maps->q, a.q, nx, ny, L, box_y);
+    bool ok = make_map(&maps->r, a.r, nx, ny, L, box_y) && make_map(&maps->w, a.w, nx, ny, L, box_y);
+    if (mode == MODE_P)
+        ok = ok && make_map(&maps->pa, a.p_a, nx, ny, L, box_y) &&
+             make_map(&maps->pb, a.p_b, nx, ny, L, box_y);
+    return ok;
+}
+
+template <int K, int RY, int NW, int NS, int MODE>
+bcgs_status launch_tb4_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
+{
+    using S = Tb4Shape<K, RY, NW, NS>;
+    auto kern = k_cheb_tb4<K, RY, NW, NS, MODE>;
+    static bool attr = false;
+    if (!attr) {
+        CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)S::smem));
+        attr = true;
+    }
+    TbMaps maps;
+    if (!make_maps(c, &maps, a, MODE, S::EY))
+        return fail(c, BCGS_E_CUDA, "cuTensorMapEncodeTiled failed");
+    dim3 grid((unsigned)((a.nx + S::TX - 1) / S::TX), (unsigned)((a.ny + S::TY - 1) / S::TY),
+              (unsigned)nchunk_total);
+    kern<<<grid, NW * 32, S::smem, c->s>>>(a, maps);
+    CUDA_OK(c, cudaGetLastError());
+    return BCGS_OK;
+}
+
+template <int K, int RY, int NW, int NS, int MODE>
+bcgs_status launch_tb5_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
+{
+    using S = Tb5Shape<K, RY, NW, NS>;
+    static_assert(S::smem <= 227 * 1024, "tb5 shared memory budget");
+    auto kern = k_cheb_tb5<K, RY, NW, NS, MODE>;
+    static bool attr = false;
+    if (!attr) {
+        CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)S::smem));
+        attr = true;
+    }
+    TbMaps maps;
+    if (!make_maps(c, &maps, a, MODE, S::EY))
+        return fail(c, BCGS_E_CUDA, "cuTensorMapEncodeTiled failed");
+    dim3 grid((unsigned)((a.nx + S::TX - 1) / S::TX), (unsigned)((a.ny + S::TY - 1) / S::TY),
+              (unsigned)nchunk_total);
+    kern<<<grid, NW * 32, S::smem, c->s>>>(a, maps);
+    CUDA_OK(c, cudaGetLastError());
+    return BCGS_OK;
+}
+
+template <int K, int MODE>
+bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz)
+{
+    if constexpr (K <= 5) {   // register budget: warp-row layouts up to K = 5
+        if (c->tb_variant == 6 && tma_ok(c))
+            return launch_tb5_k<K, 2, 16, (K <= 4 ? 4 : 3), MODE>(c, a, nz);
+        if (c->tb_variant == 5 && tma_ok(c)) return launch_tb4_k<K, 2, 16, 4, MODE>(c, a, nz);
+        if (c->tb_variant == 3) return launch_tb3_k<K, 2, 16, MODE>(c, a, nz);
+    }
+    return launch_tb_k<K, MODE>(c, a, nz);
+}
+
+}  // namespace fused
