@@ -82,7 +82,9 @@ struct Tb5Thread {
         return sm + S::PAD + b * (K * PLANE);
     }
 
-    template <int PH, bool MASK>
+    // FULL: every level is active in every row of this warp (warp-uniform), so the level
+    // loop has no branches and the K independent levels can be interleaved (ILP).
+    template <int PH, bool MASK, bool FULL = false>
     __device__ __forceinline__ void step(int t)
     {
         // ---- level 0 from the TMA stage of plane t
@@ -120,7 +122,7 @@ struct Tb5Thread {
 #pragma unroll
         for (int j = K; j >= 1; --j) {
             const int m = t - 2 * j + 1;
-            if (wdy <= K - j) {
+            if (FULL || wdy <= K - j) {
                 const double* pl = (j == 1 ? pub1 : pub2 + (j - 1) * PLANE) + ey0 * EX + lane;
                 bool mok = true;
                 if (MASK) mok = (unsigned)(m - b0) < (unsigned)(b1 - b0);
@@ -163,7 +165,7 @@ struct Tb5Thread {
                     else if (in_tile[r] && m >= c0 && m < c1) a->out[col[r] + plane * m] = v[r];
                     if (j < K) vnew[j][r] = v[r];
                 }
-            } else if (j < K) {
+            } else if (!FULL && j < K) {
 #pragma unroll
                 for (int r = 0; r < RY; ++r) {
                     win[j][PH % 4][r] = 0.0;
@@ -185,29 +187,37 @@ struct Tb5Thread {
         }
     }
 
+    template <bool MASK, bool FULL>
+    __device__ __forceinline__ void run_blocks_f(int tb, int nblk)
+    {
+        for (int b = 0; b < nblk; ++b, tb += QW) {
+            step<0, MASK, FULL>(tb);
+            step<1 % QW, MASK, FULL>(tb + 1);
+            step<2 % QW, MASK, FULL>(tb + 2);
+            if (QW > 3) {
+                step<3 % QW, MASK, FULL>(tb + 3);
+            }
+            if (QW > 4) {
+                step<4 % QW, MASK, FULL>(tb + 4);
+                step<5 % QW, MASK, FULL>(tb + 5);
+                step<6 % QW, MASK, FULL>(tb + 6);
+                step<7 % QW, MASK, FULL>(tb + 7);
+            }
+            if (QW > 8) {
+                step<8 % QW, MASK, FULL>(tb + 8);
+                step<9 % QW, MASK, FULL>(tb + 9);
+                step<10 % QW, MASK, FULL>(tb + 10);
+                step<11 % QW, MASK, FULL>(tb + 11);
+            }
+        }
+    }
+
     template <bool MASK>
     __device__ __forceinline__ void run_blocks(int tb, int nblk)
     {
-        for (int b = 0; b < nblk; ++b, tb += QW) {
-            step<0, MASK>(tb);
-            step<1 % QW, MASK>(tb + 1);
-            step<2 % QW, MASK>(tb + 2);
-            if (QW > 3) {
-                step<3 % QW, MASK>(tb + 3);
-            }
-            if (QW > 4) {
-                step<4 % QW, MASK>(tb + 4);
-                step<5 % QW, MASK>(tb + 5);
-                step<6 % QW, MASK>(tb + 6);
-                step<7 % QW, MASK>(tb + 7);
-            }
-            if (QW > 8) {
-                step<8 % QW, MASK>(tb + 8);
-                step<9 % QW, MASK>(tb + 9);
-                step<10 % QW, MASK>(tb + 10);
-                step<11 % QW, MASK>(tb + 11);
-            }
-        }
+        // warp-uniform dispatch; both paths execute one CTA barrier per step
+        if (!MASK && wdy <= 0) run_blocks_f<MASK, true>(tb, nblk);
+        else run_blocks_f<MASK, false>(tb, nblk);
     }
 
     __device__ __forceinline__ void run_tail(int t, int n)
