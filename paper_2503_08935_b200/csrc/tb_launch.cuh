@@ -125,35 +125,14 @@ bcgs_status launch_tb4_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
     return BCGS_OK;
 }
 
-template <int K, int RY, int NW, int NS, int MODE>
-bcgs_status launch_tb5_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
-{
-    using S = Tb5Shape<K, RY, NW, NS>;
-    static_assert(S::smem <= 227 * 1024, "tb5 shared memory budget");
-    auto kern = k_cheb_tb5<K, RY, NW, NS, MODE>;
-    static bool attr = false;
-    if (!attr) {
-        CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)S::smem));
-        attr = true;
-    }
-    TbMaps maps;
-    if (!make_maps(c, &maps, a, MODE, S::EY))
-        return fail(c, BCGS_E_CUDA, "cuTensorMapEncodeTiled failed");
-    dim3 grid((unsigned)((a.nx + S::TX - 1) / S::TX), (unsigned)((a.ny + S::TY - 1) / S::TY),
-              (unsigned)nchunk_total);
-    kern<<<grid, NW * 32, S::smem, c->s>>>(a, maps);
-    CUDA_OK(c, cudaGetLastError());
-    return BCGS_OK;
-}
-
 template <int K, int MODE>
 bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz)
 {
     if constexpr (K <= 5) {   // register budget: warp-row layouts up to K = 5
-        if (c->tb_variant == 6 && tma_ok(c))
-            return launch_tb5_k<K, 2, 16, (K <= 4 ? 4 : 3), MODE>(c, a, nz);
         if (c->tb_variant == 5 && tma_ok(c)) return launch_tb4_k<K, 2, 16, 4, MODE>(c, a, nz);
+        if constexpr (K <= 4) {
+            if (c->tb_variant == 7 && tma_ok(c)) return launch_tb4_k<K, 2, 24, 3, MODE>(c, a, nz);
+        }
         if (c->tb_variant == 3) return launch_tb3_k<K, 2, 16, MODE>(c, a, nz);
     }
     return launch_tb_k<K, MODE>(c, a, nz);
