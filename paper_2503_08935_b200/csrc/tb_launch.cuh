@@ -132,6 +132,7 @@ bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz)
         if (c->tb_variant == 5 && tma_ok(c)) return launch_tb4_k<K, 2, 16, 4, MODE>(c, a, nz);
         if constexpr (K <= 4) {
             if (c->tb_variant == 7 && tma_ok(c)) return launch_tb4_k<K, 2, 24, 3, MODE>(c, a, nz);
+            if (c->tb_variant == 8 && tma_ok(c)) return launch_tb4_k<K, 1, 32, 4, MODE>(c, a, nz);
         }
         if (c->tb_variant == 3) return launch_tb3_k<K, 2, 16, MODE>(c, a, nz);
     }
