@@ -86,15 +86,9 @@ struct Tb4Thread {
     double* stg;       // [NS][3][BOX] staged inputs
     uint64_t* bar;     // [NS]
     int lane, ey0, b0, b1, c0, c1, t0, t1, wdy, tx0, ty0;
-    int col0;                 // in-plane offset of row 0 (rows r: col0 + r*nx)
-    int64_t plane;
-    // per row r, bits 8r..8r+7: bit 0 in_dom, bit 1 in_tile, bits 2..7 levels 1..K active
-    uint32_t flags;
-    bool first;
-    __device__ __forceinline__ bool in_dom(int r) const { return (flags >> (8 * r)) & 1u; }
-    __device__ __forceinline__ bool in_tile(int r) const { return (flags >> (8 * r + 1)) & 1u; }
-    __device__ __forceinline__ bool act(int r, int j) const { return (flags >> (8 * r + 1 + j)) & 1u; }
-    __device__ __forceinline__ int64_t colr(int r) const { return (int64_t)col0 + (int64_t)r * a->nx; }
+    int64_t col[RY], plane;
+    unsigned actmask[RY];
+    bool in_dom[RY], in_tile[RY], first;
     double alpha, beta, omega;
     const CUtensorMap* pmap;
     double* side;
@@ -145,10 +139,10 @@ struct Tb4Thread {
                 } else {
                     v = upd_s(d[BOX + r * EX], d[2 * BOX + r * EX], alpha);
                 }
-                if (MASK) v = in_dom(r) ? v : 0.0;
+                if (MASK) v = in_dom[r] ? v : 0.0;
                 q0[r] = v;
-                if (MODE != MODE_PLAIN && in_tile(r) && t >= c0 && t < c1)
-                    side[colr(r) + plane * t] = v;
+                if (MODE != MODE_PLAIN && in_tile[r] && t >= c0 && t < c1)
+                    side[col[r] + plane * t] = v;
             }
         } else {
 #pragma unroll
@@ -193,13 +187,13 @@ struct Tb4Thread {
                         const double z2 = (j == 2) ? qc * a->cz : win[j - 2][(PH + 1) % 3][r];
                         vv = cheb_step(qc, Sv, zc, z2, a->rho[j], a->rho[j - 1], a->A2, a->B2);
                     }
-                    if (MASK) vv = (act(r, j) && mok) ? vv : 0.0;
+                    if (MASK) vv = (((actmask[r] >> j) & 1u) && mok) ? vv : 0.0;
                     v[r] = vv;
                 }
 #pragma unroll
                 for (int r = 0; r < RY; ++r) {
                     if (j < K) win[j][PH % 3][r] = v[r];
-                    else if (in_tile(r) && m >= c0 && m < c1) a->out[colr(r) + plane * m] = v[r];
+                    else if (in_tile[r] && m >= c0 && m < c1) a->out[col[r] + plane * m] = v[r];
                 }
             }
         }
@@ -300,8 +294,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_cheb_tb4(const __grid_constant__
     const int gx = th.tx0 + lane;
     const int dx = max(HX - lane, lane - (HX + TX - 1));
     int wdy = 1 << 20;
-    uint32_t flags = 0;
-    th.col0 = gx + a.nx * (th.ty0 + th.ey0);   // only used for in-tile rows
 #pragma unroll
     for (int r = 0; r < RY; ++r) {
         const int ey = th.ey0 + r;
@@ -309,16 +301,16 @@ __global__ void __launch_bounds__(NW * 32, 1) k_cheb_tb4(const __grid_constant__
         const int dy = max(K - ey, ey - (K + TY - 1));
         wdy = min(wdy, dy);
         const int dist = max(dx, dy);
-        const bool dom = gx >= 0 && gx < a.nx && gy >= 0 && gy < a.ny;
-        uint32_t f = dom ? 1u : 0u;
-        if (dom && dist <= 0) f |= 2u;
+        th.in_dom[r] = gx >= 0 && gx < a.nx && gy >= 0 && gy < a.ny;
+        th.in_tile[r] = th.in_dom[r] && dist <= 0;
+        th.col[r] = th.in_dom[r] ? gx + (int64_t)a.nx * gy : 0;
+        unsigned msk = 0;
 #pragma unroll
         for (int j = 1; j <= K; ++j)
-            if (dom && dist <= K - j) f |= 1u << (1 + j);
-        flags |= f << (8 * r);
+            if (th.in_dom[r] && dist <= K - j) msk |= 1u << j;
+        th.actmask[r] = msk;
     }
     th.wdy = wdy;
-    th.flags = flags;
     const int blk = blockIdx.z / a.nchunk, ch = blockIdx.z % a.nchunk;
     th.b0 = blk * a.Lb;
     th.b1 = th.b0 + a.Lb;
