@@ -9,6 +9,7 @@
 // one is written); the buffer is selected on the device from the iteration parity, so
 // one captured graph serves every iteration.
 #pragma once
+#include "k_stream.cuh"
 
 namespace fused {
 
@@ -125,12 +126,20 @@ bcgs_status iteration(bcgs_ctx c)
         TRY(launch_tb<MODE_P>(c, a));
     }
     TRY(halo(c, F(c, V_PH)));
+    const bool vec = (c->lay.nx % 2) == 0;   // 16-byte rows: vectorised streaming kernels
+    const dim3 sg2 = stream::stencil2_grid(c->lay.nx, c->lay.ny, c->lay.L);
+    const dim3 sb2(stream::SBX, stream::SBY);
+    const int nsb2 = (int)(sg2.x * sg2.y * sg2.z);
     {
         Prof pf(c, KC_STENCIL1, 24.0 * n);
-        ref::k_stencil_dot<1><<<sg, sb, 0, c->s>>>(F(c, V_PH), F(c, V_RT), F(c, V_W), g, 0,
-                                                  c->part, st);
+        if (vec)
+            stream::k_stencil2_dot<1><<<sg2, sb2, 0, c->s>>>(F(c, V_PH), F(c, V_RT), F(c, V_W),
+                                                           g.nx, g.ny, g.L, g.h2inv, c->part, st);
+        else
+            ref::k_stencil_dot<1><<<sg, sb, 0, c->s>>>(F(c, V_PH), F(c, V_RT), F(c, V_W), g, 0,
+                                                      c->part, st);
     }
-    TRY(reduce<1>(c, nsb, STAGE_ALPHA));
+    TRY(reduce<1>(c, vec ? nsb2 : nsb, STAGE_ALPHA));
     {   // K2: a6 + a7
         TbArgs a{};
         a.r = F(c, V_R);
@@ -144,15 +153,25 @@ bcgs_status iteration(bcgs_ctx c)
     TRY(halo(c, F(c, V_RH)));
     {
         Prof pf(c, KC_STENCIL2, 24.0 * n);
-        ref::k_stencil_dot<2><<<sg, sb, 0, c->s>>>(F(c, V_RH), F(c, V_S), F(c, V_T), g, 0,
-                                                  c->part, st);
+        if (vec)
+            stream::k_stencil2_dot<2><<<sg2, sb2, 0, c->s>>>(F(c, V_RH), F(c, V_S), F(c, V_T),
+                                                           g.nx, g.ny, g.L, g.h2inv, c->part, st);
+        else
+            ref::k_stencil_dot<2><<<sg, sb, 0, c->s>>>(F(c, V_RH), F(c, V_S), F(c, V_T), g, 0,
+                                                      c->part, st);
     }
-    TRY(reduce<2>(c, nsb, STAGE_OMEGA));
+    TRY(reduce<2>(c, vec ? nsb2 : nsb, STAGE_OMEGA));
     {
         Prof pf(c, KC_FUSED_XR, 64.0 * n);
-        k_update_xr_s<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(
-            F(c, V_X), F(c, V_PH), F(c, V_RH), F(c, V_S), F(c, V_R), F(c, V_T), F(c, V_RT), n,
-            c->part, st);
+        if (vec)
+            stream::k_update_xr2<<<kEwBlocks, 256, 0, c->s>>>(
+                (double2*)F(c, V_X), (const double2*)F(c, V_PH), (const double2*)F(c, V_RH),
+                (const double2*)F(c, V_S), (double2*)F(c, V_R), (const double2*)F(c, V_T),
+                (const double2*)F(c, V_RT), n / 2, c->part, st);
+        else
+            k_update_xr_s<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(
+                F(c, V_X), F(c, V_PH), F(c, V_RH), F(c, V_S), F(c, V_R), F(c, V_T), F(c, V_RT),
+                n, c->part, st);
     }
     TRY(reduce<2>(c, kEwBlocks, STAGE_RHO));
     CUDA_OK(c, cudaGetLastError());

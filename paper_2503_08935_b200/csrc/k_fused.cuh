@@ -480,7 +480,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_cheb_tb3(TbArgs a)
 namespace fused {
 
 // ----------------------------------------------------------------------------- host side
-inline int64_t max_blocks(int64_t, int64_t, int64_t) { return 0; }
+inline int64_t max_blocks(int64_t nx, int64_t ny, int64_t L)
+{   // partial-sum slots of the stream::k_stencil2_dot grid (k_stream.cuh)
+    return ((nx / 2 + 31) / 32) * ((ny + 7) / 8) * ((L + 7) / 8);
+}
 inline bool supported(int64_t, int64_t, int64_t, int, int degree, bool has_pc)
 {
     return has_pc && degree >= 1 && degree <= KMAX_TB;

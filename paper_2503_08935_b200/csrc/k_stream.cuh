@@ -1,0 +1,139 @@
+// k_stream.cuh -- HBM-streaming kernels of the fused path, written for memory-level
+// parallelism: 16-byte (double2) loads, several independent loads in flight per thread
+// (all operands of an unrolled group are loaded before any arithmetic), grid sized to a
+// fixed multiple of the 148 SMs (deterministic partial-sum count).
+//   k_stencil2_dot<ND>: a4 / a9 (KernelBiCGS1 / KernelBiCGS3)
+//   k_update_xr2:       a11 + a12 (KernelBiCGS4 / KernelBiCGS5)
+// Same per-point expression trees as every other variant (expr.cuh); Dot2 reductions.
+#pragma once
+#include "dd.cuh"
+#include "expr.cuh"
+#include "state.cuh"
+
+namespace stream {
+
+constexpr int SBX = 32, SBY = 8, SZC = 8;   // threads (x pairs) x rows, planes per thread
+
+// w = A v (global operator; ghost planes hold halo data or zeros) and Dot2 partials of
+// a·w (ND >= 1) and w·w (ND == 2).  Each thread owns 2 adjacent x points of one row and
+// marches SZC planes; requires nx even (16-byte aligned rows).
+template <int ND>
+__global__ void __launch_bounds__(SBX * SBY) k_stencil2_dot(const double* __restrict__ v,
+                                                            const double* __restrict__ a,
+                                                            double* __restrict__ out, int nx,
+                                                            int ny, int L, double h2inv,
+                                                            dd* __restrict__ part,
+                                                            const DevState* __restrict__ st)
+{
+    if (st && st->done) return;
+    const int i = (blockIdx.x * SBX + threadIdx.x) * 2, j = blockIdx.y * SBY + threadIdx.y;
+    const int k0 = blockIdx.z * SZC, k1 = min(L, k0 + SZC);
+    constexpr int NDA = (ND > 0) ? ND : 1;
+    double p[NDA] = {}, s[NDA] = {};
+    if (i < nx && j < ny) {
+        const int64_t plane = (int64_t)nx * ny;
+        int64_t c = i + (int64_t)nx * j + plane * k0;
+        double2 zm = *reinterpret_cast<const double2*>(v + c - plane);
+        double2 zc = *reinterpret_cast<const double2*>(v + c);
+        const bool hxm = i > 0, hxp = i + 2 < nx, hym = j > 0, hyp = j < ny - 1;
+#pragma unroll 2
+        for (int k = k0; k < k1; ++k, c += plane) {
+            const double2 zp = *reinterpret_cast<const double2*>(v + c + plane);
+            const double xm = hxm ? __ldg(v + c - 1) : 0.0;
+            const double xp = hxp ? __ldg(v + c + 2) : 0.0;
+            const double2 ym = hym ? *reinterpret_cast<const double2*>(v + c - nx) : make_double2(0, 0);
+            const double2 yp = hyp ? *reinterpret_cast<const double2*>(v + c + nx) : make_double2(0, 0);
+            double2 av = make_double2(0, 0);
+            if (ND >= 1) av = __ldg(reinterpret_cast<const double2*>(a + c));
+            double2 o;
+            o.x = stencil_row(zc.x, xm, zc.y, ym.x, yp.x, zm.x, zp.x, h2inv);
+            o.y = stencil_row(zc.y, zc.x, xp, ym.y, yp.y, zm.y, zp.y, h2inv);
+            *reinterpret_cast<double2*>(out + c) = o;
+            if (ND >= 1) {
+                dot2_acc(p[0], s[0], av.x, o.x);
+                dot2_acc(p[0], s[0], av.y, o.y);
+            }
+            if (ND >= 2) {
+                dot2_acc(p[ND - 1], s[ND - 1], o.x, o.x);
+                dot2_acc(p[ND - 1], s[ND - 1], o.y, o.y);
+            }
+            zm = zc;
+            zc = zp;
+        }
+    }
+    if (ND > 0) {
+        const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+        block_reduce_dd<NDA>(p, s, part + (int64_t)bid * ND);
+    }
+}
+
+inline dim3 stencil2_grid(int64_t nx, int64_t ny, int64_t L)
+{
+    return dim3((unsigned)((nx / 2 + SBX - 1) / SBX), (unsigned)((ny + SBY - 1) / SBY),
+                (unsigned)((L + SZC - 1) / SZC));
+}
+
+// a11 + a12: x = fma(ω, r̂, fma(α, p̂, x)); r = fma(-ω, t, s); partials r~·r, r·r.
+// n2 = number of double2 elements; UNR double2 groups per thread per iteration.
+constexpr int XR_UNR = 2;
+__global__ void __launch_bounds__(256) k_update_xr2(double2* __restrict__ x,
+                                                    const double2* __restrict__ ph,
+                                                    const double2* __restrict__ rh,
+                                                    const double2* __restrict__ s,
+                                                    double2* __restrict__ r,
+                                                    const double2* __restrict__ t,
+                                                    const double2* __restrict__ rt, int64_t n2,
+                                                    dd* __restrict__ part,
+                                                    const DevState* __restrict__ st)
+{
+    if (st->done) return;
+    const double alpha = st->alpha, omega = st->omega;
+    double p[2] = {0.0, 0.0}, q[2] = {0.0, 0.0};
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; c + (XR_UNR - 1) * stride < n2; c += XR_UNR * stride) {
+        double2 vx[XR_UNR], vph[XR_UNR], vrh[XR_UNR], vs[XR_UNR], vt[XR_UNR], vrt[XR_UNR];
+#pragma unroll
+        for (int u = 0; u < XR_UNR; ++u) {
+            const int64_t e = c + u * stride;
+            vx[u] = x[e];
+            vph[u] = __ldg(ph + e);
+            vrh[u] = __ldg(rh + e);
+            vs[u] = __ldg(s + e);
+            vt[u] = __ldg(t + e);
+            vrt[u] = __ldg(rt + e);
+        }
+#pragma unroll
+        for (int u = 0; u < XR_UNR; ++u) {
+            const int64_t e = c + u * stride;
+            double2 xn, rn;
+            xn.x = upd_x(vx[u].x, vph[u].x, vrh[u].x, alpha, omega);
+            xn.y = upd_x(vx[u].y, vph[u].y, vrh[u].y, alpha, omega);
+            rn.x = upd_r(vs[u].x, vt[u].x, omega);
+            rn.y = upd_r(vs[u].y, vt[u].y, omega);
+            x[e] = xn;
+            r[e] = rn;
+            dot2_acc(p[0], q[0], vrt[u].x, rn.x);
+            dot2_acc(p[0], q[0], vrt[u].y, rn.y);
+            dot2_acc(p[1], q[1], rn.x, rn.x);
+            dot2_acc(p[1], q[1], rn.y, rn.y);
+        }
+    }
+    for (; c < n2; c += stride) {
+        const double2 vx = x[c], vph = ph[c], vrh = rh[c], vs = s[c], vt = t[c], vrt = rt[c];
+        double2 xn, rn;
+        xn.x = upd_x(vx.x, vph.x, vrh.x, alpha, omega);
+        xn.y = upd_x(vx.y, vph.y, vrh.y, alpha, omega);
+        rn.x = upd_r(vs.x, vt.x, omega);
+        rn.y = upd_r(vs.y, vt.y, omega);
+        x[c] = xn;
+        r[c] = rn;
+        dot2_acc(p[0], q[0], vrt.x, rn.x);
+        dot2_acc(p[0], q[0], vrt.y, rn.y);
+        dot2_acc(p[1], q[1], rn.x, rn.x);
+        dot2_acc(p[1], q[1], rn.y, rn.y);
+    }
+    block_reduce_dd<2>(p, q, part + (int64_t)blockIdx.x * 2);
+}
+
+}  // namespace stream
