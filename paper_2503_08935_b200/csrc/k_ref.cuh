@@ -237,9 +237,21 @@ __global__ void __launch_bounds__(1024) k_finalize(const dd* __restrict__ part, 
     double p[ND], s[ND];
 #pragma unroll
     for (int d = 0; d < ND; ++d) { p[d] = 0.0; s[d] = 0.0; }
-    const int per = (nparts + blockDim.x - 1) / blockDim.x;
-    const int b0 = threadIdx.x * per, b1 = min(nparts, b0 + per);
-    for (int b = b0; b < b1; ++b)
+    // thread t combines partials t, t + T, t + 2T, ... (coalesced; 8 loads in flight)
+    const int T = blockDim.x;
+    int b = threadIdx.x;
+    for (; b + 7 * T < nparts; b += 8 * T) {
+        dd v[8][ND];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int d = 0; d < ND; ++d) v[u][d] = part[(int64_t)(b + u * T) * ND + d];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int d = 0; d < ND; ++d) dd_add(p[d], s[d], v[u][d].hi, v[u][d].lo);
+    }
+    for (; b < nparts; b += T)
 #pragma unroll
         for (int d = 0; d < ND; ++d) dd_add(p[d], s[d], part[(int64_t)b * ND + d].hi,
                                             part[(int64_t)b * ND + d].lo);

@@ -8,7 +8,8 @@ rows = list(csv.reader(open(sys.argv[1])))
 i = [k for k, r in enumerate(rows) if r and r[0] == "ID"][0]
 h, data = rows[i], rows[i + 1:]
 ik, iv, iu = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
-scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+scale = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0,
+         "second": 1e3, "s": 1e3}
 tot, cnt = collections.Counter(), collections.Counter()
 for r in data:
     name = r[ik].split("(")[0].replace("void ", "")
