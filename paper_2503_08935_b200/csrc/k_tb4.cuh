@@ -119,9 +119,7 @@ struct Tb4Thread {
         }
     }
 
-    // FULL: warp-uniform, every row of this warp is inside every level's halo -> no level
-    // branches (straight-line code the scheduler can interleave across rows and levels)
-    template <int PH, bool MASK, bool FULL = false>
+    template <int PH, bool MASK>
     __device__ __forceinline__ void step(int t)
     {
         // ---- level 0 from the TMA stage of plane t
@@ -156,7 +154,7 @@ struct Tb4Thread {
 #pragma unroll
         for (int j = 1; j <= K; ++j) {
             const int m = t - j;
-            if (FULL || wdy <= K - j) {               // warp-uniform level skip
+            if (wdy <= K - j) {                       // warp-uniform level skip
                 const double* pl = prev + (j - 1) * PLANE + ey0 * EX + lane;
                 bool mok = true;
                 if (MASK) mok = (unsigned)(m - b0) < (unsigned)(b1 - b0);
@@ -214,34 +212,26 @@ struct Tb4Thread {
         }
     }
 
-    template <bool MASK, bool FULL>
-    __device__ __forceinline__ void run_blocks_f(int tb, int nblk)
-    {
-        constexpr int U = QW;
-        for (int b = 0; b < nblk; ++b, tb += U) {
-            step<0, MASK, FULL>(tb);
-            step<1 % U, MASK, FULL>(tb + 1);
-            step<2 % U, MASK, FULL>(tb + 2);
-            if (U > 3) {
-                step<3 % U, MASK, FULL>(tb + 3);
-                step<4 % U, MASK, FULL>(tb + 4);
-                step<5 % U, MASK, FULL>(tb + 5);
-            }
-            if (U > 6) {
-                step<6 % U, MASK, FULL>(tb + 6);
-                step<7 % U, MASK, FULL>(tb + 7);
-                step<8 % U, MASK, FULL>(tb + 8);
-            }
-        }
-    }
-
-    // nblk blocks of U steps; warps whose rows are all inside the output tile take the
-    // branch-free path in the unmasked steady state (both paths: one barrier per step)
+    // steps [tb, te) (te - tb a multiple of U unless FULL == false)
     template <bool MASK>
     __device__ __forceinline__ void run_blocks(int tb, int nblk)
     {
-        if (!MASK && wdy <= 0) run_blocks_f<false, true>(tb, nblk);
-        else run_blocks_f<MASK, false>(tb, nblk);
+        constexpr int U = QW;
+        for (int b = 0; b < nblk; ++b, tb += U) {
+            step<0, MASK>(tb);
+            step<1 % U, MASK>(tb + 1);
+            step<2 % U, MASK>(tb + 2);
+            if (U > 3) {
+                step<3 % U, MASK>(tb + 3);
+                step<4 % U, MASK>(tb + 4);
+                step<5 % U, MASK>(tb + 5);
+            }
+            if (U > 6) {
+                step<6 % U, MASK>(tb + 6);
+                step<7 % U, MASK>(tb + 7);
+                step<8 % U, MASK>(tb + 8);
+            }
+        }
     }
 
     // remainder of < U steps starting at phase 0
