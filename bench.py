@@ -99,6 +99,17 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def max_over_ranks(value: float, dist=None, device=None) -> float:
+    """Max of a per-rank float over all ranks (timings are reported as the slowest rank)."""
+    if dist is None or not dist.is_available() or not dist.is_initialized() \
+            or dist.get_world_size() == 1:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def cpu_baseline(n, pc, k, seed):
     """The oracle as it stands, on this host's cores, on a bounded sample of the workload:
     one outer iteration of the same 512³ problem (fixed_it = 1; includes the setup dots,
@@ -221,10 +232,7 @@ def main():
     tr1.record(stream)
     torch.cuda.synchronize()
     ms_iter = max(ms_total - tr0.elapsed_time(tr1), 1e-6) / args.steps
-    if world > 1:
-        t = torch.tensor([ms_iter], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_iter = float(t.item())
+    ms_iter = max_over_ranks(ms_iter, dist, dev)
 
     its = 1000.0 / ms_iter
     gdof = n ** 3 * its / 1e9
@@ -266,10 +274,7 @@ def main():
         s.lib.bcgs_get_solution(s.ctx, x_host.data_ptr(), bcgs.MEM_HOST)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([dt], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
+        dt = max_over_ranks(dt, dist, dev)
         e2e = {"value": args.steps / dt, "unit": "iters/s",
                "h2d_bytes_per_step": f_host.numel() * 8 / args.steps,
                "d2h_bytes_per_step": x_host.numel() * 8 / args.steps,

@@ -53,6 +53,7 @@ def lib() -> ctypes.CDLL:
         _lib.orc_apply_A.argtypes = [i64, i64, i64, f64, i64, P, P]
         _lib.orc_dot.restype = f64
         _lib.orc_dot.argtypes = [i64, i64, P, P]
+        _lib.orc_dot_pair.argtypes = [i64, i64, P, P, P]
         _lib.orc_mu.restype = f64
         _lib.orc_mu.argtypes = [i64, i64]
         _lib.orc_bounds.argtypes = [i64, i64, i64, f64, P, P]
@@ -119,6 +120,15 @@ def dot(a: np.ndarray, b: np.ndarray) -> float:
     else:
         plen, npl = a.size, 1
     return float(lib().orc_dot(plen, npl, _ptr(a), _ptr(b)))
+
+
+def dot_pair(a: np.ndarray, b: np.ndarray):
+    """Dot2 (hi, lo) pair of a (nz, ny, nx) field (R19 partial)."""
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    out = np.zeros(2)
+    lib().orc_dot_pair(a.shape[1] * a.shape[2], a.shape[0], _ptr(a), _ptr(b), _ptr(out))
+    return float(out[0]), float(out[1])
 
 
 def mu(n: int, i: int) -> float:

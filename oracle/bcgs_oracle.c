@@ -176,6 +176,21 @@ double orc_dot(int64_t plen, int64_t nplanes, const double* a, const double* b)
     return P + S;
 }
 
+/* Dot2 pair (hi, lo) of a field -- the per-rank partial a z-slab decomposition would
+ * contribute before the rank-ordered combination (R19). */
+void orc_dot_pair(int64_t plen, int64_t nplanes, const double* a, const double* b, double* out2)
+{
+    double P = 0.0, S = 0.0;
+    for (int64_t k = 0; k < nplanes; ++k) {
+        double hi, lo, q;
+        dot2_run(plen, a + k * plen, b + k * plen, &hi, &lo);
+        two_sum(P, hi, &P, &q);
+        S = S + (q + lo);
+    }
+    out2[0] = P;
+    out2[1] = S;
+}
+
 /* ------------------------------------------------------------------------------------------
  * Eigenvalue bounds.  Eq. 9: eigenvalues of D_n are 4 sin²(iπ/(2(n+1))).
  * Eqs. 10-11: λmin/λmax of P = Σ_axes min/max μ / Δ².

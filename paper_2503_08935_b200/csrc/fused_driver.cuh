@@ -66,13 +66,24 @@ bcgs_status launch_tb(bcgs_ctx c, TbArgs& a)
     a.A2 = c->cst[5];
     a.B2 = c->cst[6];
     for (int j = 0; j <= k; ++j) a.rho[j] = c->rho[j];
-    // z-chunking: enough CTAs for ~8 waves of 148 SMs, chunks of >= 16 planes
+    // z-chunking: each chunk re-computes ~2k warm-up/drain planes; more chunks fill the 148
+    // SMs (one CTA per SM) more evenly.  Pick the chunk count minimising
+    // waves * (planes per chunk + 2k).
     int tx, ty;
     variant_tile(c->tb_variant, k, &tx, &ty);
     const int64_t tiles = ((a.nx + tx - 1) / tx) * (int64_t)((a.ny + ty - 1) / ty) * c->bpr;
-    int64_t want = (8 * kNumSMs + tiles - 1) / tiles;
-    want = std::max<int64_t>(1, std::min<int64_t>(want, (a.Lb + 15) / 16));
-    a.zch = (int)((a.Lb + want - 1) / want);
+    int64_t best_n = 1;
+    double best = 1e300;
+    for (int64_t nch = 1; nch <= std::max<int64_t>(1, a.Lb / 8); ++nch) {
+        const int64_t zc = (a.Lb + nch - 1) / nch;
+        const int64_t waves = (tiles * nch + kNumSMs - 1) / kNumSMs;
+        const double cost = (double)waves * (double)(zc + 2 * k);
+        if (cost < best * 0.999) {
+            best = cost;
+            best_n = nch;
+        }
+    }
+    a.zch = (int)((a.Lb + best_n - 1) / best_n);
     a.nchunk = (a.Lb + a.zch - 1) / a.zch;
     const int nz = a.nchunk * c->bpr;
     switch (k) {
