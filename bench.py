@@ -27,6 +27,17 @@ sys.path.insert(0, ROOT)
 
 METRIC = "fp64 Bi-CGSTAB iters/s & GDoF/s at 512^3; % of HBM roofline"
 ALG_BYTES_PER_PT = 200.0   # compulsory bytes per point per outer iteration
+# FP64 flops per point of one launch of the fused Chebyshev kernels at degree k:
+# sweep 1: 12, sweep 2: 16, sweeps 3..k: 15 each; + the fused vector update (p: 4, s: 2)
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+
+
+def _cheb_flops(k):
+    return 0 if k == 0 else 12 + (16 if k >= 2 else 0) + 15 * max(0, k - 2)
+
+
+FLOPS_PER_PT = {"fused_p_cheb": lambda k: _cheb_flops(k) + 4,
+                "fused_s_cheb": lambda k: _cheb_flops(k) + 2}
 
 
 def parse():
@@ -259,6 +270,15 @@ def main():
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_source": peak_src,
                 "share_of_step": d["ms"] / (ms_iter * args.steps)}
+        if dom_name in FLOPS_PER_PT:
+            # the temporally blocked Chebyshev kernels are FP64-ALU heavy: report that roof too
+            fl = FLOPS_PER_PT[dom_name](k) * pts_local
+            roof["alu"] = {"bound": "alu", "achieved": fl / (per_launch_ms * 1e-3) / 1e12,
+                           "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                           "frac": fl / (per_launch_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                           "flops_per_pt": FLOPS_PER_PT[dom_name](k),
+                           "peak_source": "148 SMs x 64 FP64 lanes x 2 (FMA) x 1.965 GHz "
+                                          "(DESIGN.md §5)"}
     launches = sum(v["calls"] for kname, v in ktimes.items() if kname not in ("halo", "allgather"))
 
     # e2e through the public API with host buffers: set_rhs(host) + solve(K) + x -> host
