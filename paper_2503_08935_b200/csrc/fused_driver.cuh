@@ -42,6 +42,8 @@ void variant_tile(int variant, int k, int* tx, int* ty)
         if (k >= 7) { *tx = 16; *ty = 8; } else if (k >= 5) { *tx = 32; *ty = 8; }
     } else if (variant == 5 || variant == 6) {
         *tx = 32 - 2 * ((k + 1) / 2 * 2); *ty = 32 - 2 * k;   // TMA: even x-halo
+    } else if (variant == 9 && k <= 4) {
+        *tx = 64 - 2 * ((k + 1) / 2 * 2); *ty = 24 - 2 * k;   // 2x2 register tiles, 12 warps
     } else if (variant == 8 && k <= 4) {
         *tx = 32 - 2 * ((k + 1) / 2 * 2); *ty = 32 - 2 * k;   // 32 warps, RY = 1
     } else if (variant == 7 && k <= 4) {

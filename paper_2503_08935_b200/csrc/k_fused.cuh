@@ -477,6 +477,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_cheb_tb3(TbArgs a)
 
 }  // namespace fused
 #include "k_tb4.cuh"
+#include "k_tb6.cuh"
 namespace fused {
 
 // ----------------------------------------------------------------------------- host side

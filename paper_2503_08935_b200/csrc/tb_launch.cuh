@@ -76,13 +76,14 @@ inline EncodeTiledFn encode_fn()
 }
 
 // 3-D map over a slab field (nx, ny, L) of doubles, box (32, box_y, 1); OOB -> zeros
-inline bool make_map(CUtensorMap* m, const double* base, int64_t nx, int64_t ny, int64_t L, int box_y)
+inline bool make_map(CUtensorMap* m, const double* base, int64_t nx, int64_t ny, int64_t L, int box_y,
+                     int box_x = 32)
 {
     EncodeTiledFn fn = encode_fn();
     if (!fn || (nx * 8) % 16 || ((uintptr_t)base % 16)) return false;
     cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)L};
     cuuint64_t strides[2] = {(cuuint64_t)(nx * 8), (cuuint64_t)(nx * ny * 8)};
-    cuuint32_t box[3] = {32, (cuuint32_t)box_y, 1};
+    cuuint32_t box[3] = {(cuuint32_t)box_x, (cuuint32_t)box_y, 1};
     cuuint32_t es[3] = {1, 1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box,
               es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -92,16 +93,40 @@ inline bool make_map(CUtensorMap* m, const double* base, int64_t nx, int64_t ny,
 
 inline bool tma_ok(bcgs_ctx c) { return encode_fn() != nullptr && c->lay.nx % 2 == 0; }
 
-inline bool make_maps(bcgs_ctx c, TbMaps* maps, const TbArgs& a, int mode, int box_y)
+inline bool make_maps(bcgs_ctx c, TbMaps* maps, const TbArgs& a, int mode, int box_y,
+                      int box_x = 32)
 {
     memset(maps, 0, sizeof *maps);
     const int64_t nx = c->lay.nx, ny = c->lay.ny, L = c->lay.L;
-    if (mode == MODE_PLAIN) return make_map(&maps->q, a.q, nx, ny, L, box_y);
-    bool ok = make_map(&maps->r, a.r, nx, ny, L, box_y) && make_map(&maps->w, a.w, nx, ny, L, box_y);
+    if (mode == MODE_PLAIN) return make_map(&maps->q, a.q, nx, ny, L, box_y, box_x);
+    bool ok = make_map(&maps->r, a.r, nx, ny, L, box_y, box_x) &&
+              make_map(&maps->w, a.w, nx, ny, L, box_y, box_x);
     if (mode == MODE_P)
-        ok = ok && make_map(&maps->pa, a.p_a, nx, ny, L, box_y) &&
-             make_map(&maps->pb, a.p_b, nx, ny, L, box_y);
+        ok = ok && make_map(&maps->pa, a.p_a, nx, ny, L, box_y, box_x) &&
+             make_map(&maps->pb, a.p_b, nx, ny, L, box_y, box_x);
     return ok;
+}
+
+template <int K, int RY, int NW, int NS, int MODE>
+bcgs_status launch_tb6_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
+{
+    using S = Tb6Shape<K, RY, NW, NS>;
+    static_assert(S::smem <= 227 * 1024, "tb6 shared memory budget");
+    auto kern = k_cheb_tb6<K, RY, NW, NS, MODE>;
+    static bool attr = false;
+    if (!attr) {
+        CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)S::smem));
+        attr = true;
+    }
+    TbMaps maps;
+    if (!make_maps(c, &maps, a, MODE, S::EY, S::EX))
+        return fail(c, BCGS_E_CUDA, "cuTensorMapEncodeTiled failed");
+    dim3 grid((unsigned)((a.nx + S::TX - 1) / S::TX), (unsigned)((a.ny + S::TY - 1) / S::TY),
+              (unsigned)nchunk_total);
+    kern<<<grid, NW * 32, S::smem, c->s>>>(a, maps);
+    CUDA_OK(c, cudaGetLastError());
+    return BCGS_OK;
 }
 
 template <int K, int RY, int NW, int NS, int MODE>
@@ -133,6 +158,7 @@ bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz)
         if constexpr (K <= 4) {
             if (c->tb_variant == 7 && tma_ok(c)) return launch_tb4_k<K, 2, 24, 3, MODE>(c, a, nz);
             if (c->tb_variant == 8 && tma_ok(c)) return launch_tb4_k<K, 1, 32, 4, MODE>(c, a, nz);
+            if (c->tb_variant == 9 && tma_ok(c)) return launch_tb6_k<K, 2, 12, 3, MODE>(c, a, nz);
         }
         if (c->tb_variant == 3) return launch_tb3_k<K, 2, 16, MODE>(c, a, nz);
     }
