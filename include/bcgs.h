@@ -124,6 +124,14 @@ bcgs_status bcgs_nccl_unique_id(void* out128);
 bcgs_status bcgs_create(const bcgs_grid_desc* grid, int32_t rank, int32_t nranks,
                         const void* nccl_unique_id, int32_t cuda_device, void* d_workspace,
                         size_t ws_bytes, void* cuda_stream, bcgs_ctx* out);
+/* In-process multi-rank group on ONE device (testing transport): creates nranks contexts
+ * (ranks 0..nranks-1 of the z-slab decomposition) whose halo exchanges and reductions are
+ * device copies between their workspaces instead of NCCL.  Each context must then be driven
+ * by its own host thread (exchanges block on a host barrier).  d_workspaces[r] as for
+ * bcgs_create; outs[r] receives rank r's context. */
+bcgs_status bcgs_create_local(const bcgs_grid_desc* grid, int32_t nranks, int32_t cuda_device,
+                              void* const* d_workspaces, size_t ws_bytes, void* cuda_stream,
+                              bcgs_ctx* outs);
 void bcgs_destroy(bcgs_ctx ctx);
 const char* bcgs_last_error(bcgs_ctx ctx);
 bcgs_status bcgs_set_option(bcgs_ctx ctx, int32_t option, int64_t value);

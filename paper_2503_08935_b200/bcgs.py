@@ -28,7 +28,8 @@ MAX_DEGREE = 64
 # Every symbol include/bcgs.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "bcgs_abi_version", "bcgs_status_string", "bcgs_workspace_bytes",
-    "bcgs_chebyshev_constants", "bcgs_nccl_unique_id", "bcgs_create", "bcgs_destroy",
+    "bcgs_chebyshev_constants", "bcgs_nccl_unique_id", "bcgs_create", "bcgs_create_local",
+    "bcgs_destroy",
     "bcgs_last_error", "bcgs_set_option", "bcgs_set_rhs_random", "bcgs_set_rhs",
     "bcgs_set_boundary_value", "bcgs_set_initial_guess", "bcgs_set_preconditioner",
     "bcgs_set_eigen_bounds", "bcgs_solve", "bcgs_begin", "bcgs_iterate", "bcgs_finish",
@@ -81,6 +82,8 @@ def load() -> ctypes.CDLL:
         "bcgs_nccl_unique_id": (i32, [P]),
         "bcgs_create": (i32, [ctypes.POINTER(GridDesc), i32, i32, P, i32, P, ctypes.c_size_t,
                               P, ctypes.POINTER(P)]),
+        "bcgs_create_local": (i32, [ctypes.POINTER(GridDesc), i32, i32, ctypes.POINTER(P),
+                                    ctypes.c_size_t, P, ctypes.POINTER(P)]),
         "bcgs_destroy": (None, [P]),
         "bcgs_last_error": (ctypes.c_char_p, [P]),
         "bcgs_set_option": (i32, [P, i32, i64]),
@@ -151,7 +154,8 @@ class Solver:
     """One rank's context.  `n` = global unknowns (int or (nx, ny, nz)), `h` = spacing."""
 
     def __init__(self, n, h: float, *, rank: int = 0, nranks: int = 1,
-                 nccl_id: bytes | None = None, device: int | None = None, stream=None):
+                 nccl_id: bytes | None = None, device: int | None = None, stream=None,
+                 _ctx=None, _workspace=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("bcgs.Solver needs a CUDA device (no CPU fallback)")
@@ -163,6 +167,10 @@ class Solver:
         self.L = self.n[2] // nranks
         self.shape = (self.L, self.n[1], self.n[0])
         self.desc = grid_desc(self.n, h)
+        if _ctx is not None:                       # member of a local group
+            self.ctx, self.workspace = _ctx, _workspace
+            self.stream = stream
+            return
         nbytes = self.lib.bcgs_workspace_bytes(ctypes.byref(self.desc), nranks)
         if nbytes == 0:
             raise BcgsError(E_CONFIG, f"grid {self.n} not divisible into {nranks} z-slabs")
@@ -306,3 +314,25 @@ class Solver:
 
     def kernel_times_reset(self):
         self.lib.bcgs_kernel_times_reset(self.ctx)
+
+
+def local_group(n, h: float, nranks: int, device: int | None = None) -> list:
+    """nranks Solver contexts on ONE GPU exchanging halos / reductions by device copies
+    (bcgs_create_local).  Drive each from its own thread."""
+    import torch
+    lib = load()
+    device = torch.cuda.current_device() if device is None else device
+    desc = grid_desc(n, h)
+    nbytes = lib.bcgs_workspace_bytes(ctypes.byref(desc), nranks)
+    if nbytes == 0:
+        raise BcgsError(E_CONFIG, "grid not divisible into z-slabs")
+    wss = [torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{device}") for _ in range(nranks)]
+    ptrs = (ctypes.c_void_p * nranks)(*[w.data_ptr() for w in wss])
+    outs = (ctypes.c_void_p * nranks)()
+    stream = torch.cuda.current_stream(device)
+    st = lib.bcgs_create_local(ctypes.byref(desc), nranks, device, ptrs, nbytes,
+                               stream.cuda_stream, outs)
+    if st:
+        raise BcgsError(st, "bcgs_create_local")
+    return [Solver(n, h, rank=r, nranks=nranks, device=device, stream=stream,
+                   _ctx=ctypes.c_void_p(outs[r]), _workspace=wss[r]) for r in range(nranks)]

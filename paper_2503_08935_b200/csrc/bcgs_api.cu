@@ -141,11 +141,48 @@ __global__ void k_init_state(DevState* st, double tol, int max_iter, int fixed)
 }
 
 // ------------------------------------------------------------------ communication
+// Face-halo exchange of a field (a3 / a8, MPI1 / MPI3 P:278): send plane 0 to rank-1
+// and plane L-1 to rank+1, receive the ghost planes -1 and L.  NCCL, or the in-process
+// peer transport of bcgs_create_local.
+bcgs_status local_exchange_begin(bcgs_ctx c)
+{
+    CUDA_OK(c, cudaEventRecord(c->ev_ready, c->s));
+    c->lg->bar.wait();   // every rank has recorded its producer event
+    return BCGS_OK;
+}
+
+bcgs_status local_exchange_end(bcgs_ctx c, bool all)
+{
+    CUDA_OK(c, cudaEventRecord(c->ev_done, c->s));
+    c->lg->bar.wait();   // every rank has issued its copies
+    for (int r = 0; r < c->nranks; ++r)
+        if (r != c->rank && (all || r == c->rank - 1 || r == c->rank + 1))
+            CUDA_OK(c, cudaStreamWaitEvent(c->s, c->lg->ctxs[r]->ev_done, 0));
+    return BCGS_OK;
+}
+
 bcgs_status halo(bcgs_ctx c, double* v)
 {
     if (c->nranks == 1) return BCGS_OK;
     Prof pf(c, KC_HALO, 0.0);
     const size_t pl = (size_t)c->lay.plane;
+    if (c->lg) {
+        const ptrdiff_t off = (char*)v - c->ws;   // same layout on every rank
+        TRY(local_exchange_begin(c));
+        for (int d = -1; d <= 1; d += 2) {
+            const int nb = c->rank + d;
+            if (nb < 0 || nb >= c->nranks) continue;
+            bcgs_ctx p = c->lg->ctxs[nb];
+            const double* pv = (const double*)(p->ws + off);
+            CUDA_OK(c, cudaStreamWaitEvent(c->s, p->ev_ready, 0));
+            // from rank-1: its plane L-1 -> my ghost -1; from rank+1: its plane 0 -> ghost L
+            const double* src = d < 0 ? pv + (c->lay.L - 1) * pl : pv;
+            double* dst = d < 0 ? v - pl : v + c->lay.L * pl;
+            CUDA_OK(c, cudaMemcpyAsync(dst, src, pl * sizeof(double), cudaMemcpyDeviceToDevice,
+                                       c->s));
+        }
+        return local_exchange_end(c, false);
+    }
     NCCL_OK(c, ncclGroupStart());
     if (c->rank > 0) {
         NCCL_OK(c, ncclSend(v, pl, ncclDouble, c->rank - 1, c->comm, c->s));
@@ -159,6 +196,24 @@ bcgs_status halo(bcgs_ctx c, double* v)
     return BCGS_OK;
 }
 
+// All-gather of every rank's ND Dot2 pairs (MPI2/4/5).
+bcgs_status allgather_pairs(bcgs_ctx c, int nd)
+{
+    Prof pf(c, KC_ALLGATHER, 0.0);
+    if (c->lg) {
+        TRY(local_exchange_begin(c));
+        for (int r = 0; r < c->nranks; ++r) {
+            bcgs_ctx p = c->lg->ctxs[r];
+            if (r != c->rank) CUDA_OK(c, cudaStreamWaitEvent(c->s, p->ev_ready, 0));
+            CUDA_OK(c, cudaMemcpyAsync(c->gath + (size_t)r * nd, p->rank_out, nd * sizeof(dd),
+                                       cudaMemcpyDeviceToDevice, c->s));
+        }
+        return local_exchange_end(c, true);
+    }
+    NCCL_OK(c, ncclAllGather(c->rank_out, c->gath, 2 * nd, ncclDouble, c->comm, c->s));
+    return BCGS_OK;
+}
+
 // Reduce `nparts` partial pairs of ND dots, then run the scalar stage.
 template <int ND>
 bcgs_status reduce(bcgs_ctx c, int nparts, int stage)
@@ -169,10 +224,7 @@ bcgs_status reduce(bcgs_ctx c, int nparts, int stage)
                                               c->rank_out, c->nranks);
     }
     if (c->nranks > 1) {
-        {
-            Prof pf(c, KC_ALLGATHER, 0.0);
-            NCCL_OK(c, ncclAllGather(c->rank_out, c->gath, 2 * ND, ncclDouble, c->comm, c->s));
-        }
+        TRY(allgather_pairs(c, ND));
         Prof pf(c, KC_SCALARS, 0.0);
         k_scalars<ND><<<1, 1, 0, c->s>>>(c->gath, c->nranks, stage, c->st, c->hist, c->scal);
     }
@@ -293,7 +345,7 @@ bcgs_status iteration(bcgs_ctx c)
 
 bcgs_status enqueue_iterations(bcgs_ctx c, int n)
 {
-    if (c->use_graph && !c->profile) {
+    if (c->use_graph && !c->profile && !c->lg) {
         if (!c->gexec) {
             cudaGraph_t graph;
             CUDA_OK(c, cudaStreamBeginCapture(c->s, cudaStreamCaptureModeThreadLocal));
@@ -428,13 +480,14 @@ bcgs_status bcgs_nccl_unique_id(void* out128)
     return BCGS_OK;
 }
 
-bcgs_status bcgs_create(const bcgs_grid_desc* grid, int32_t rank, int32_t nranks,
-                        const void* nccl_unique_id, int32_t cuda_device, void* d_workspace,
-                        size_t ws_bytes, void* cuda_stream, bcgs_ctx* out)
+static bcgs_status create_ctx(const bcgs_grid_desc* grid, int32_t rank, int32_t nranks,
+                              const void* nccl_unique_id, LocalGroup* lg, int32_t cuda_device,
+                              void* d_workspace, size_t ws_bytes, void* cuda_stream,
+                              bcgs_ctx* out)
 {
     if (!grid || !out || nranks < 1 || rank < 0 || rank >= nranks) return BCGS_E_INVALID;
     if (!(grid->h > 0.0)) return BCGS_E_INVALID;
-    if (nranks > 1 && !nccl_unique_id) return BCGS_E_INVALID;
+    if (nranks > 1 && !nccl_unique_id && !lg) return BCGS_E_INVALID;
     Layout lay;
     if (!make_layout(grid, nranks, &lay)) return BCGS_E_CONFIG;
     if (lay.nx > (1 << 30) || lay.ny > (1 << 30)) return BCGS_E_CONFIG;
@@ -449,11 +502,16 @@ bcgs_status bcgs_create(const bcgs_grid_desc* grid, int32_t rank, int32_t nranks
     c->device = cuda_device;
     c->user = (cudaStream_t)cuda_stream;
     c->ws = (char*)d_workspace;
+    c->lg = lg;
     *out = c;
     CUDA_OK(c, cudaSetDevice(cuda_device));
     CUDA_OK(c, cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
     CUDA_OK(c, cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
     CUDA_OK(c, cudaMallocHost(&c->h_pinned, 64));
+    if (lg) {
+        CUDA_OK(c, cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
+        CUDA_OK(c, cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
+    }
     for (int v = 0; v < V_COUNT; ++v)
         c->vec[v] = (double*)(c->ws + lay.off_vec[v]) + lay.plane;
     c->st = (DevState*)(c->ws + lay.off_state);
@@ -464,12 +522,39 @@ bcgs_status bcgs_create(const bcgs_grid_desc* grid, int32_t rank, int32_t nranks
     c->gath = (dd*)(c->ws + lay.off_gath);
     TRY(enter(c));
     CUDA_OK(c, cudaMemsetAsync(c->ws, 0, lay.total, c->s));   // zero ghost planes + state
-    if (nranks > 1) {
+    if (nranks > 1 && !lg) {
         ncclUniqueId id;
         memcpy(&id, nccl_unique_id, sizeof id);
         NCCL_OK(c, ncclCommInitRank(&c->comm, nranks, id, rank));
     }
     TRY(leave(c));
+    if (lg) CUDA_OK(c, cudaStreamSynchronize(c->s));
+    return BCGS_OK;
+}
+
+bcgs_status bcgs_create(const bcgs_grid_desc* grid, int32_t rank, int32_t nranks,
+                        const void* nccl_unique_id, int32_t cuda_device, void* d_workspace,
+                        size_t ws_bytes, void* cuda_stream, bcgs_ctx* out)
+{
+    return create_ctx(grid, rank, nranks, nccl_unique_id, nullptr, cuda_device, d_workspace,
+                      ws_bytes, cuda_stream, out);
+}
+
+bcgs_status bcgs_create_local(const bcgs_grid_desc* grid, int32_t nranks, int32_t cuda_device,
+                              void* const* d_workspaces, size_t ws_bytes, void* cuda_stream,
+                              bcgs_ctx* outs)
+{
+    if (!grid || !outs || !d_workspaces || nranks < 2) return BCGS_E_INVALID;
+    LocalGroup* lg = new LocalGroup();
+    lg->n = nranks;
+    lg->bar.n = nranks;
+    lg->ctxs.assign(nranks, nullptr);
+    for (int r = 0; r < nranks; ++r) {
+        bcgs_status st = create_ctx(grid, r, nranks, nullptr, lg, cuda_device, d_workspaces[r],
+                                    ws_bytes, cuda_stream, &outs[r]);
+        if (st != BCGS_OK) return st;
+        lg->ctxs[r] = outs[r];
+    }
     return BCGS_OK;
 }
 
@@ -482,6 +567,16 @@ void bcgs_destroy(bcgs_ctx c)
     drop_graph(c);
     for (auto e : c->free_ev) cudaEventDestroy(e);
     if (c->comm) ncclCommDestroy(c->comm);
+    if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+    if (c->ev_done) cudaEventDestroy(c->ev_done);
+    if (c->lg) {
+        bool last = true;
+        for (auto& p : c->lg->ctxs) {
+            if (p == c) p = nullptr;
+            if (p) last = false;
+        }
+        if (last) delete c->lg;
+    }
     if (c->join) cudaEventDestroy(c->join);
     if (c->s) cudaStreamDestroy(c->s);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);

@@ -7,6 +7,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -85,6 +87,34 @@ struct EvRec {
     double bytes;
 };
 
+// In-process peer transport (bcgs_create_local): P contexts on one device, each driven by
+// its own host thread; exchanges are device copies between the contexts' workspaces,
+// ordered by events and a host barrier (the NCCL path's single-GPU twin, for testing).
+struct HostBarrier {
+    std::mutex m;
+    std::condition_variable cv;
+    int n = 0, count = 0;
+    long gen = 0;
+    void wait()
+    {
+        std::unique_lock<std::mutex> lk(m);
+        const long g = gen;
+        if (++count == n) {
+            count = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+
+struct LocalGroup {
+    int n = 0;
+    std::vector<bcgs_ctx_s*> ctxs;
+    HostBarrier bar;
+};
+
 struct bcgs_ctx_s {
     Layout lay;
     double h = 0.0, h2inv = 0.0;
@@ -119,6 +149,8 @@ struct bcgs_ctx_s {
     std::vector<cudaEvent_t> free_ev;
     double ktime[KC_COUNT] = {}, kbytes[KC_COUNT] = {};
     int64_t kcalls[KC_COUNT] = {};
+    LocalGroup* lg = nullptr;         // in-process peers (testing transport)
+    cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
     std::string err;
 };
 
