@@ -46,19 +46,21 @@ struct Prof {
     bcgs_ctx c;
     int cls;
     double bytes;
+    cudaStream_t s;
     cudaEvent_t a = nullptr;
-    Prof(bcgs_ctx c_, int cls_, double bytes_) : c(c_), cls(cls_), bytes(bytes_)
+    Prof(bcgs_ctx c_, int cls_, double bytes_, cudaStream_t s_ = nullptr)
+        : c(c_), cls(cls_), bytes(bytes_), s(s_ ? s_ : c_->s)
     {
         if (c->profile) {
             a = get_ev(c);
-            cudaEventRecord(a, c->s);
+            cudaEventRecord(a, s);
         }
     }
     ~Prof()
     {
         if (c->profile) {
             cudaEvent_t b = get_ev(c);
-            cudaEventRecord(b, c->s);
+            cudaEventRecord(b, s);
             c->pending.push_back({cls, a, b, bytes});
         }
     }
@@ -144,16 +146,16 @@ __global__ void k_init_state(DevState* st, double tol, int max_iter, int fixed)
 // Face-halo exchange of a field (a3 / a8, MPI1 / MPI3 P:278): send plane 0 to rank-1
 // and plane L-1 to rank+1, receive the ghost planes -1 and L.  NCCL, or the in-process
 // peer transport of bcgs_create_local.
-bcgs_status local_exchange_begin(bcgs_ctx c)
+bcgs_status local_exchange_begin(bcgs_ctx c, cudaStream_t hs)
 {
-    CUDA_OK(c, cudaEventRecord(c->ev_ready, c->s));
+    CUDA_OK(c, cudaEventRecord(c->ev_ready, hs));
     c->lg->bar.wait();   // every rank has recorded its producer event
     return BCGS_OK;
 }
 
-bcgs_status local_exchange_end(bcgs_ctx c, bool all)
+bcgs_status local_exchange_end(bcgs_ctx c, bool all, cudaStream_t hs)
 {
-    CUDA_OK(c, cudaEventRecord(c->ev_done, c->s));
+    CUDA_OK(c, cudaEventRecord(c->ev_done, hs));
     c->lg->bar.wait();   // every rank has issued its copies
     for (int r = 0; r < c->nranks; ++r)
         if (r != c->rank && (all || r == c->rank - 1 || r == c->rank + 1))
@@ -161,54 +163,56 @@ bcgs_status local_exchange_end(bcgs_ctx c, bool all)
     return BCGS_OK;
 }
 
-bcgs_status halo(bcgs_ctx c, double* v)
+bcgs_status halo_on(bcgs_ctx c, double* v, cudaStream_t hs)
 {
     if (c->nranks == 1) return BCGS_OK;
-    Prof pf(c, KC_HALO, 0.0);
+    Prof pf(c, KC_HALO, 0.0, hs);
     const size_t pl = (size_t)c->lay.plane;
     if (c->lg) {
         const ptrdiff_t off = (char*)v - c->ws;   // same layout on every rank
-        TRY(local_exchange_begin(c));
+        TRY(local_exchange_begin(c, hs));
         for (int d = -1; d <= 1; d += 2) {
             const int nb = c->rank + d;
             if (nb < 0 || nb >= c->nranks) continue;
             bcgs_ctx p = c->lg->ctxs[nb];
             const double* pv = (const double*)(p->ws + off);
-            CUDA_OK(c, cudaStreamWaitEvent(c->s, p->ev_ready, 0));
+            CUDA_OK(c, cudaStreamWaitEvent(hs, p->ev_ready, 0));
             // from rank-1: its plane L-1 -> my ghost -1; from rank+1: its plane 0 -> ghost L
             const double* src = d < 0 ? pv + (c->lay.L - 1) * pl : pv;
             double* dst = d < 0 ? v - pl : v + c->lay.L * pl;
             CUDA_OK(c, cudaMemcpyAsync(dst, src, pl * sizeof(double), cudaMemcpyDeviceToDevice,
-                                       c->s));
+                                       hs));
         }
-        return local_exchange_end(c, false);
+        return local_exchange_end(c, false, hs);
     }
     NCCL_OK(c, ncclGroupStart());
     if (c->rank > 0) {
-        NCCL_OK(c, ncclSend(v, pl, ncclDouble, c->rank - 1, c->comm, c->s));
-        NCCL_OK(c, ncclRecv(v - pl, pl, ncclDouble, c->rank - 1, c->comm, c->s));
+        NCCL_OK(c, ncclSend(v, pl, ncclDouble, c->rank - 1, c->comm, hs));
+        NCCL_OK(c, ncclRecv(v - pl, pl, ncclDouble, c->rank - 1, c->comm, hs));
     }
     if (c->rank < c->nranks - 1) {
-        NCCL_OK(c, ncclSend(v + (c->lay.L - 1) * pl, pl, ncclDouble, c->rank + 1, c->comm, c->s));
-        NCCL_OK(c, ncclRecv(v + c->lay.L * pl, pl, ncclDouble, c->rank + 1, c->comm, c->s));
+        NCCL_OK(c, ncclSend(v + (c->lay.L - 1) * pl, pl, ncclDouble, c->rank + 1, c->comm, hs));
+        NCCL_OK(c, ncclRecv(v + c->lay.L * pl, pl, ncclDouble, c->rank + 1, c->comm, hs));
     }
     NCCL_OK(c, ncclGroupEnd());
     return BCGS_OK;
 }
+
+bcgs_status halo(bcgs_ctx c, double* v) { return halo_on(c, v, c->s); }
 
 // All-gather of every rank's ND Dot2 pairs (MPI2/4/5).
 bcgs_status allgather_pairs(bcgs_ctx c, int nd)
 {
     Prof pf(c, KC_ALLGATHER, 0.0);
     if (c->lg) {
-        TRY(local_exchange_begin(c));
+        TRY(local_exchange_begin(c, c->s));
         for (int r = 0; r < c->nranks; ++r) {
             bcgs_ctx p = c->lg->ctxs[r];
             if (r != c->rank) CUDA_OK(c, cudaStreamWaitEvent(c->s, p->ev_ready, 0));
             CUDA_OK(c, cudaMemcpyAsync(c->gath + (size_t)r * nd, p->rank_out, nd * sizeof(dd),
                                        cudaMemcpyDeviceToDevice, c->s));
         }
-        return local_exchange_end(c, true);
+        return local_exchange_end(c, true, c->s);
     }
     NCCL_OK(c, ncclAllGather(c->rank_out, c->gath, 2 * nd, ncclDouble, c->comm, c->s));
     return BCGS_OK;
@@ -508,6 +512,11 @@ static bcgs_status create_ctx(const bcgs_grid_desc* grid, int32_t rank, int32_t 
     CUDA_OK(c, cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
     CUDA_OK(c, cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
     CUDA_OK(c, cudaMallocHost(&c->h_pinned, 64));
+    if (nranks > 1) {
+        CUDA_OK(c, cudaStreamCreateWithFlags(&c->s_comm, cudaStreamNonBlocking));
+        CUDA_OK(c, cudaEventCreateWithFlags(&c->ev_pre, cudaEventDisableTiming));
+        CUDA_OK(c, cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
+    }
     if (lg) {
         CUDA_OK(c, cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
         CUDA_OK(c, cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
@@ -568,6 +577,9 @@ void bcgs_destroy(bcgs_ctx c)
     for (auto e : c->free_ev) cudaEventDestroy(e);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+    if (c->ev_pre) cudaEventDestroy(c->ev_pre);
+    if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+    if (c->s_comm) cudaStreamDestroy(c->s_comm);
     if (c->ev_done) cudaEventDestroy(c->ev_done);
     if (c->lg) {
         bool last = true;

@@ -151,6 +151,8 @@ struct bcgs_ctx_s {
     int64_t kcalls[KC_COUNT] = {};
     LocalGroup* lg = nullptr;         // in-process peers (testing transport)
     cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
+    cudaStream_t s_comm = nullptr;              // halo stream (nranks > 1), overlapped
+    cudaEvent_t ev_pre = nullptr, ev_halo = nullptr;
     std::string err;
 };
 

@@ -118,6 +118,40 @@ bcgs_status precond_apply(bcgs_ctx c, const double* q, double* out)
 
 void on_begin(bcgs_ctx) {}
 
+// a3 + a4 (a8 + a9): halo exchange of v overlapped with the stencil+dot of the interior
+// planes 1..L-2 (side stream + events), then the two boundary planes once the ghost planes
+// have arrived.  Writes the Dot2 partials of all launches contiguously; *nparts = count.
+template <int ND>
+bcgs_status halo_stencil(bcgs_ctx c, double* v, const double* a, double* out, int kc,
+                         int* nparts)
+{
+    const int nx = (int)c->lay.nx, ny = (int)c->lay.ny, L = (int)c->lay.L;
+    const dim3 sb(stream::SBX, stream::SBY);
+    int nb = 0;
+    auto launch = [&](int kb, int ke) {
+        const dim3 g = stream::stencil2_grid(nx, ny, ke - kb);
+        stream::k_stencil2_dot<ND><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv,
+                                                       c->part + (int64_t)nb * ND, c->st);
+        nb += (int)(g.x * g.y * g.z);
+    };
+    Prof pf(c, kc, 24.0 * npts(c));
+    if (c->nranks == 1) {
+        launch(0, L);
+    } else {
+        CUDA_OK(c, cudaEventRecord(c->ev_pre, c->s));
+        CUDA_OK(c, cudaStreamWaitEvent(c->s_comm, c->ev_pre, 0));
+        TRY(halo_on(c, v, c->s_comm));
+        CUDA_OK(c, cudaEventRecord(c->ev_halo, c->s_comm));
+        if (L > 2) launch(1, L - 1);                       // interior, overlapped with the halo
+        CUDA_OK(c, cudaStreamWaitEvent(c->s, c->ev_halo, 0));
+        launch(0, 1);                                       // boundary planes
+        if (L > 1) launch(L - 1, L);
+    }
+    CUDA_OK(c, cudaGetLastError());
+    *nparts = nb;
+    return BCGS_OK;
+}
+
 bcgs_status iteration(bcgs_ctx c)
 {
     const int64_t n = npts(c);
@@ -138,21 +172,17 @@ bcgs_status iteration(bcgs_ctx c)
         Prof pf(c, KC_FUSED_P1, 40.0 * n);
         TRY(launch_tb<MODE_P>(c, a));
     }
-    TRY(halo(c, F(c, V_PH)));
     const bool vec = (c->lay.nx % 2) == 0;   // 16-byte rows: vectorised streaming kernels
-    const dim3 sg2 = stream::stencil2_grid(c->lay.nx, c->lay.ny, c->lay.L);
-    const dim3 sb2(stream::SBX, stream::SBY);
-    const int nsb2 = (int)(sg2.x * sg2.y * sg2.z);
-    {
+    int np1 = nsb, np2 = nsb;
+    if (vec) {
+        TRY(halo_stencil<1>(c, F(c, V_PH), F(c, V_RT), F(c, V_W), KC_STENCIL1, &np1));
+    } else {
+        TRY(halo(c, F(c, V_PH)));
         Prof pf(c, KC_STENCIL1, 24.0 * n);
-        if (vec)
-            stream::k_stencil2_dot<1><<<sg2, sb2, 0, c->s>>>(F(c, V_PH), F(c, V_RT), F(c, V_W),
-                                                           g.nx, g.ny, g.L, g.h2inv, c->part, st);
-        else
-            ref::k_stencil_dot<1><<<sg, sb, 0, c->s>>>(F(c, V_PH), F(c, V_RT), F(c, V_W), g, 0,
-                                                      c->part, st);
+        ref::k_stencil_dot<1><<<sg, sb, 0, c->s>>>(F(c, V_PH), F(c, V_RT), F(c, V_W), g, 0,
+                                                  c->part, st);
     }
-    TRY(reduce<1>(c, vec ? nsb2 : nsb, STAGE_ALPHA));
+    TRY(reduce<1>(c, np1, STAGE_ALPHA));
     {   // K2: a6 + a7
         TbArgs a{};
         a.r = F(c, V_R);
@@ -163,17 +193,15 @@ bcgs_status iteration(bcgs_ctx c)
         Prof pf(c, KC_FUSED_P2, 32.0 * n);
         TRY(launch_tb<MODE_S>(c, a));
     }
-    TRY(halo(c, F(c, V_RH)));
-    {
+    if (vec) {
+        TRY(halo_stencil<2>(c, F(c, V_RH), F(c, V_S), F(c, V_T), KC_STENCIL2, &np2));
+    } else {
+        TRY(halo(c, F(c, V_RH)));
         Prof pf(c, KC_STENCIL2, 24.0 * n);
-        if (vec)
-            stream::k_stencil2_dot<2><<<sg2, sb2, 0, c->s>>>(F(c, V_RH), F(c, V_S), F(c, V_T),
-                                                           g.nx, g.ny, g.L, g.h2inv, c->part, st);
-        else
-            ref::k_stencil_dot<2><<<sg, sb, 0, c->s>>>(F(c, V_RH), F(c, V_S), F(c, V_T), g, 0,
-                                                      c->part, st);
+        ref::k_stencil_dot<2><<<sg, sb, 0, c->s>>>(F(c, V_RH), F(c, V_S), F(c, V_T), g, 0,
+                                                  c->part, st);
     }
-    TRY(reduce<2>(c, vec ? nsb2 : nsb, STAGE_OMEGA));
+    TRY(reduce<2>(c, np2, STAGE_OMEGA));
     {
         Prof pf(c, KC_FUSED_XR, 64.0 * n);
         if (vec)

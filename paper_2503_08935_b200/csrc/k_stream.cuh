@@ -21,13 +21,13 @@ template <int ND>
 __global__ void __launch_bounds__(SBX * SBY) k_stencil2_dot(const double* __restrict__ v,
                                                             const double* __restrict__ a,
                                                             double* __restrict__ out, int nx,
-                                                            int ny, int L, double h2inv,
+                                                            int ny, int kb, int ke, double h2inv,
                                                             dd* __restrict__ part,
                                                             const DevState* __restrict__ st)
 {
     if (st && st->done) return;
     const int i = (blockIdx.x * SBX + threadIdx.x) * 2, j = blockIdx.y * SBY + threadIdx.y;
-    const int k0 = blockIdx.z * SZC, k1 = min(L, k0 + SZC);
+    const int k0 = kb + blockIdx.z * SZC, k1 = min(ke, k0 + SZC);
     constexpr int NDA = (ND > 0) ? ND : 1;
     double p[NDA] = {}, s[NDA] = {};
     if (i < nx && j < ny) {
@@ -67,10 +67,10 @@ __global__ void __launch_bounds__(SBX * SBY) k_stencil2_dot(const double* __rest
     }
 }
 
-inline dim3 stencil2_grid(int64_t nx, int64_t ny, int64_t L)
+inline dim3 stencil2_grid(int64_t nx, int64_t ny, int64_t nplanes)
 {
     return dim3((unsigned)((nx / 2 + SBX - 1) / SBX), (unsigned)((ny + SBY - 1) / SBY),
-                (unsigned)((L + SZC - 1) / SZC));
+                (unsigned)((nplanes + SZC - 1) / SZC));
 }
 
 // a11 + a12: x = fma(ω, r̂, fma(α, p̂, x)); r = fma(-ω, t, s); partials r~·r, r·r.
