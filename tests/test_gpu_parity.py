@@ -224,3 +224,30 @@ def test_recurrence_equals_true_residual_any_size(bc):
         assert rep["true_rel_residual"] == pytest.approx(rep["rel_residual"], rel=1e-6)
         del s
         torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+def test_c2_256_full_solve(bc, orc):
+    """Config C2 (256³, Chebyshev degree 4) solved to 1e-8: iterations, every residual and
+    the converged x bitwise equal to the oracle (bars: 1e-9 / 1e-8 / ±1)."""
+    assert_parity(*compare_solve(bc, orc, 256, "gnocomm", 4, 1, 1))
+
+
+def test_c4_512_block_jacobi_8_slabs(bc, orc):
+    """Config C4 at full size: BJ(CI) k=4 on 8 z-slabs (the 8-GPU decomposition emulated
+    with blocks_per_rank = 8), first 3 iterations bitwise."""
+    assert_parity(*compare_solve(bc, orc, 512, "bj", 4, 8, 1, fixed=3))
+
+
+def test_c5_1024_properties(bc):
+    """Config C5 size (1024³; 8 slabs as on 8 GPUs): properties that hold at any size --
+    the recurrence residual equals ||b - A x||/||b||, and residuals decrease."""
+    s, n3, h = make(bc, 1024, pc="gnocomm", degree=4, blocks_per_rank=8)
+    s.set_rhs_random(si.SEED)
+    rep = s.solve(fixed_iters=4)
+    hist = s.residual_history()
+    assert rep["true_rel_residual"] == pytest.approx(rep["rel_residual"], rel=1e-6)
+    assert np.all(np.diff(hist) < 0)
+    s.close()
+    del s
+    torch.cuda.empty_cache()
