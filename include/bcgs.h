@@ -79,7 +79,8 @@ typedef enum { BCGS_MEM_DEVICE = 0, BCGS_MEM_HOST = 1 } bcgs_mem;
 typedef enum {
     BCGS_OPT_KERNELS = 0,      /* 0 = reference kernels (one sweep per launch, one op per */
                                /*     launch); 1 = fused / temporally blocked (default)   */
-    BCGS_OPT_GRAPH = 1,        /* 1 = replay iterations from a captured CUDA graph        */
+    BCGS_OPT_GRAPH = 1,        /* 1 = replay iterations from a captured CUDA graph (default;*/
+                               /*     not while profiling or with bcgs_create_local)   */
     BCGS_OPT_PROFILE = 2,      /* 1 = CUDA events around every kernel (bcgs_kernel_times) */
     BCGS_OPT_POLL = 3,         /* iterations launched between done-flag polls (tol mode)  */
     BCGS_OPT_TB_VARIANT = 4    /* temporally blocked kernel layout (tuning): 2 = square   */

@@ -129,7 +129,7 @@ struct bcgs_ctx_s {
     dd *part = nullptr, *rank_out = nullptr, *gath = nullptr;
     double* h_pinned = nullptr;    // small pinned buffer for flag polls
     // options
-    int kernels = 1, use_graph = 0, profile = 0, poll = 8, tb_variant = 7;
+    int kernels = 1, use_graph = 1, profile = 0, poll = 8, tb_variant = 7;
     // preconditioner
     bcgs_pc pc = BCGS_PC_NONE;
     int degree = 0, bpr = 1;
