@@ -253,8 +253,8 @@ struct Tb4Thread {
     }
 };
 
-template <int K, int RY, int NW, int NS, int MODE>
-__global__ void __launch_bounds__(NW * 32, 1) k_cheb_tb4(const __grid_constant__ TbArgs a,
+template <int K, int RY, int NW, int NS, int MODE, int MINB = 1>
+__global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constant__ TbArgs a,
                                                        const __grid_constant__ TbMaps maps)
 {
     using T = Tb4Thread<K, RY, NW, NS, MODE>;

@@ -129,11 +129,11 @@ bcgs_status launch_tb6_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
     return BCGS_OK;
 }
 
-template <int K, int RY, int NW, int NS, int MODE>
+template <int K, int RY, int NW, int NS, int MODE, int MINB = 1>
 bcgs_status launch_tb4_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
 {
     using S = Tb4Shape<K, RY, NW, NS>;
-    auto kern = k_cheb_tb4<K, RY, NW, NS, MODE>;
+    auto kern = k_cheb_tb4<K, RY, NW, NS, MODE, MINB>;
     static bool attr = false;
     if (!attr) {
         CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -159,6 +159,8 @@ bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz)
             if (c->tb_variant == 7 && tma_ok(c)) return launch_tb4_k<K, 2, 24, 3, MODE>(c, a, nz);
             if (c->tb_variant == 8 && tma_ok(c)) return launch_tb4_k<K, 1, 32, 4, MODE>(c, a, nz);
             if (c->tb_variant == 9 && tma_ok(c)) return launch_tb6_k<K, 2, 12, 3, MODE>(c, a, nz);
+            if (c->tb_variant == 10 && tma_ok(c))
+                return launch_tb4_k<K, 2, 12, 3, MODE, 2>(c, a, nz);   // 2 CTAs / SM
         }
         if (c->tb_variant == 3) return launch_tb3_k<K, 2, 16, MODE>(c, a, nz);
     }
