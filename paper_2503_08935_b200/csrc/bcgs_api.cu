@@ -140,6 +140,7 @@ __global__ void k_init_state(DevState* st, double tol, int max_iter, int fixed)
     st->fixed_iters = fixed;
     st->done = DONE_RUNNING;
     st->iter = 0;
+    st->x_applied = 0;
 }
 
 // ------------------------------------------------------------------ communication
@@ -747,6 +748,7 @@ bcgs_status bcgs_finish(bcgs_ctx c, bcgs_report* out)
 {
     if (!c) return BCGS_E_INVALID;
     if (!c->begun) return fail(c, BCGS_E_STATE, "bcgs_finish before bcgs_begin");
+    TRY(fused::flush_x(c));
     int32_t done = 0, iter = 0;
     TRY(poll_state(c, &done, &iter));
     // true residual (R22): ||b - A x|| / ||b||, once
@@ -833,6 +835,7 @@ bcgs_status bcgs_get_solution(bcgs_ctx c, double* x, int32_t mem)
 {
     if (!c || !x) return BCGS_E_INVALID;
     TRY(enter(c));
+    TRY(fused::flush_x(c));
     const size_t bytes = sizeof(double) * (size_t)npts(c);
     CUDA_OK(c, cudaMemcpyAsync(x, F(c, V_X), bytes,
                                mem == BCGS_MEM_HOST ? cudaMemcpyDeviceToHost

@@ -74,7 +74,7 @@ bcgs_status launch_tb(bcgs_ctx c, TbArgs& a)
     // SMs (one CTA per SM) more evenly.  Pick the chunk count minimising
     // waves * (planes per chunk + 2k).
     int tx, ty;
-    variant_tile(c->tb_variant, k, &tx, &ty);
+    variant_tile((MODE == MODE_P && c->defer_x) ? 5 : c->tb_variant, k, &tx, &ty);
     const int64_t tiles = ((a.nx + tx - 1) / tx) * (int64_t)((a.ny + ty - 1) / ty) * c->bpr;
     int64_t best_n = 1;
     double best = 1e300;
@@ -119,7 +119,22 @@ bcgs_status precond_apply(bcgs_ctx c, const double* q, double* out)
     return launch_tb<MODE_PLAIN>(c, a);
 }
 
-void on_begin(bcgs_ctx) {}
+void on_begin(bcgs_ctx c)
+{
+    c->defer_x = (c->kernels == 1 && c->pc != BCGS_PC_NONE && (c->lay.nx % 2) == 0 &&
+                  defer_x_ok(c)) ? 1 : 0;
+}
+
+// deferred-x mode: bring x up to date (idempotent; stream-ordered)
+bcgs_status flush_x(bcgs_ctx c)
+{
+    if (!c->defer_x || !c->begun) return BCGS_OK;
+    stream::k_xflush<<<kEwBlocks, 256, 0, c->s>>>(F(c, V_X), F(c, V_PH), F(c, V_RH), npts(c),
+                                                 c->st);
+    stream::k_xmark<<<1, 1, 0, c->s>>>(c->st);
+    CUDA_OK(c, cudaGetLastError());
+    return BCGS_OK;
+}
 
 // a3 + a4 (a8 + a9): halo exchange of v overlapped with the stencil+dot of the interior
 // planes 1..L-2 (side stream + events), then the two boundary planes once the ghost planes
@@ -171,8 +186,10 @@ bcgs_status iteration(bcgs_ctx c)
         a.side_a = F(c, V_P);
         a.side_b = F(c, V_P2);
         a.out = F(c, V_PH);
+        a.x = F(c, V_X);
+        a.rh = F(c, V_RH);
         a.st = st;
-        Prof pf(c, KC_FUSED_P1, 40.0 * n);
+        Prof pf(c, KC_FUSED_P1, (c->defer_x ? 72.0 : 40.0) * n);
         TRY(launch_tb<MODE_P>(c, a));
     }
     const bool vec = (c->lay.nx % 2) == 0;   // 16-byte rows: vectorised streaming kernels
@@ -205,7 +222,12 @@ bcgs_status iteration(bcgs_ctx c)
                                                   c->part, st);
     }
     TRY(reduce<2>(c, np2, STAGE_OMEGA));
-    {
+    if (vec && c->defer_x) {   // a12 only: x was (or will be) updated by the p-kernel
+        Prof pf(c, KC_FUSED_XR, 32.0 * n);
+        stream::k_update_r2<<<kEwBlocks, 256, 0, c->s>>>(
+            (const double2*)F(c, V_S), (double2*)F(c, V_R), (const double2*)F(c, V_T),
+            (const double2*)F(c, V_RT), n / 2, c->part, st);
+    } else {
         Prof pf(c, KC_FUSED_XR, 64.0 * n);
         if (vec)
             stream::k_update_xr2<<<kEwBlocks, 256, 0, c->s>>>(

@@ -33,6 +33,8 @@ struct TbArgs {
     double* side_a;       // MODE_P: output p_i = parity ? side_a : side_b (the other buffer)
     double* side_b;       // MODE_S: side_a = s
     double* out;          // level-K output: M^-1 q
+    double* x;            // MODE_P + XUPD: x_{i-1} += α p̂_{i-1} + ω r̂_{i-1} (deferred a11)
+    const double* rh;     //   r̂ of the previous iteration
     int nx, ny, Lb, zch, nchunk;
     double h2inv, cz, g1, A2, B2;
     double rho[KMAX_TB + 1];

@@ -136,4 +136,65 @@ __global__ void __launch_bounds__(256) k_update_xr2(double2* __restrict__ x,
     block_reduce_dd<2>(p, q, part + (int64_t)blockIdx.x * 2);
 }
 
+// a12 alone (deferred-x mode, x is updated inside the next p-kernel): r = fma(-ω, t, s);
+// partials r~·r and r·r.
+__global__ void __launch_bounds__(256) k_update_r2(const double2* __restrict__ s,
+                                                   double2* __restrict__ r,
+                                                   const double2* __restrict__ t,
+                                                   const double2* __restrict__ rt, int64_t n2,
+                                                   dd* __restrict__ part,
+                                                   const DevState* __restrict__ st)
+{
+    if (st->done) return;
+    const double omega = st->omega;
+    double p[2] = {0.0, 0.0}, q[2] = {0.0, 0.0};
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; c + 3 * stride < n2; c += 4 * stride) {
+        double2 vs[4], vt[4], vrt[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            vs[u] = __ldg(s + c + u * stride);
+            vt[u] = __ldg(t + c + u * stride);
+            vrt[u] = __ldg(rt + c + u * stride);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            double2 rn;
+            rn.x = upd_r(vs[u].x, vt[u].x, omega);
+            rn.y = upd_r(vs[u].y, vt[u].y, omega);
+            r[c + u * stride] = rn;
+            dot2_acc(p[0], q[0], vrt[u].x, rn.x);
+            dot2_acc(p[0], q[0], vrt[u].y, rn.y);
+            dot2_acc(p[1], q[1], rn.x, rn.x);
+            dot2_acc(p[1], q[1], rn.y, rn.y);
+        }
+    }
+    for (; c < n2; c += stride) {
+        const double2 vs = s[c], vt = t[c], vrt = rt[c];
+        double2 rn;
+        rn.x = upd_r(vs.x, vt.x, omega);
+        rn.y = upd_r(vs.y, vt.y, omega);
+        r[c] = rn;
+        dot2_acc(p[0], q[0], vrt.x, rn.x);
+        dot2_acc(p[0], q[0], vrt.y, rn.y);
+        dot2_acc(p[1], q[1], rn.x, rn.x);
+        dot2_acc(p[1], q[1], rn.y, rn.y);
+    }
+    block_reduce_dd<2>(p, q, part + (int64_t)blockIdx.x * 2);
+}
+
+// deferred-x mode: apply the last completed iteration's x update if no p-kernel did.
+__global__ void k_xflush(double* __restrict__ x, const double* __restrict__ ph,
+                         const double* __restrict__ rh, int64_t n, const DevState* __restrict__ st)
+{
+    if (st->iter < 1 || st->x_applied == st->iter) return;
+    const double alpha = st->alpha, omega = st->omega;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
+         c += (int64_t)gridDim.x * blockDim.x)
+        x[c] = upd_x(x[c], ph[c], rh[c], alpha, omega);
+}
+
+__global__ void k_xmark(DevState* st) { st->x_applied = st->iter; }
+
 }  // namespace stream

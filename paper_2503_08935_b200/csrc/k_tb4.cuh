@@ -72,7 +72,7 @@ struct Tb4Shape {
     static constexpr size_t smem = level_bytes + stage_bytes + 128;
 };
 
-template <int K, int RY, int NW, int NS, int MODE>
+template <int K, int RY, int NW, int NS, int MODE, bool XUPD = false>
 struct Tb4Thread {
     using S = Tb4Shape<K, RY, NW, NS>;
     static constexpr int EX = S::EX, TX = S::TX, TY = S::TY, PLANE = S::PLANE, QW = S::QW,
@@ -92,6 +92,7 @@ struct Tb4Thread {
     double alpha, beta, omega;
     const CUtensorMap* pmap;
     double* side;
+    bool xdo;          // XUPD: this launch applies the previous iteration's x update
 
     static constexpr int ninputs() { return MODE == MODE_PLAIN ? 1 : (MODE == MODE_P ? 3 : 2); }
 
@@ -122,6 +123,22 @@ struct Tb4Thread {
     template <int PH, bool MASK>
     __device__ __forceinline__ void step(int t)
     {
+        // ---- deferred a11 of the previous iteration on plane t - K (read p̂_{i-1} before
+        //      this step's level K overwrites it with p̂_i; same thread, same point)
+        double xv[RY], phv[RY], rhv[RY];
+        const int mx = t - K;
+        const bool xs = XUPD && xdo && mx >= c0 && mx < c1;
+        if (XUPD && xs) {
+#pragma unroll
+            for (int r = 0; r < RY; ++r) {
+                if (in_tile[r]) {
+                    const int64_t e = col[r] + plane * mx;
+                    xv[r] = a->x[e];
+                    phv[r] = a->out[e];
+                    rhv[r] = __ldg(a->rh + e);
+                }
+            }
+        }
         // ---- level 0 from the TMA stage of plane t
         double q0[RY];
         if (t < b1) {
@@ -197,6 +214,11 @@ struct Tb4Thread {
                 }
             }
         }
+        if (XUPD && xs) {
+#pragma unroll
+            for (int r = 0; r < RY; ++r)
+                if (in_tile[r]) a->x[col[r] + plane * mx] = upd_x(xv[r], phv[r], rhv[r], alpha, omega);
+        }
         double* cur = sm + S::PAD + (t & 1) * (K * PLANE) + ey0 * EX + lane;
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
@@ -253,11 +275,11 @@ struct Tb4Thread {
     }
 };
 
-template <int K, int RY, int NW, int NS, int MODE, int MINB = 1>
+template <int K, int RY, int NW, int NS, int MODE, int MINB = 1, bool XUPD = false>
 __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constant__ TbArgs a,
                                                        const __grid_constant__ TbMaps maps)
 {
-    using T = Tb4Thread<K, RY, NW, NS, MODE>;
+    using T = Tb4Thread<K, RY, NW, NS, MODE, XUPD>;
     using S = Tb4Shape<K, RY, NW, NS>;
     constexpr int TX = S::TX, TY = S::TY, U = S::QW;
     extern __shared__ __align__(128) double smraw[];

@@ -17,6 +17,7 @@ struct DevState {
     int32_t done;         // DONE_*
     int32_t fixed_iters;  // > 0: run exactly this many
     int32_t max_iter;
+    int32_t x_applied;    // deferred-x mode: last iteration whose x update is in x
     double scratch[8];    // results of stand-alone dot calls
 };
 
@@ -50,6 +51,7 @@ __device__ __forceinline__ void stage_update(DevState* st, int stage, const doub
         break;
     }
     case STAGE_ALPHA: {
+        st->x_applied = st->iter;   // the fused p-kernel of this iteration applied x_{iter}
         const int i = st->iter + 1;
         double* sc = scal + 8 * (i - 1);
         const double rw = v[0];

@@ -93,6 +93,9 @@ inline bool make_map(CUtensorMap* m, const double* base, int64_t nx, int64_t ny,
 
 inline bool tma_ok(bcgs_ctx c) { return encode_fn() != nullptr && c->lay.nx % 2 == 0; }
 
+// deferred x update needs the TMA warp-row kernel (K <= 5)
+inline bool defer_x_possible(bcgs_ctx c) { return tma_ok(c) && c->degree >= 1 && c->degree <= 5; }
+
 inline bool make_maps(bcgs_ctx c, TbMaps* maps, const TbArgs& a, int mode, int box_y,
                       int box_x = 32)
 {
@@ -129,11 +132,11 @@ bcgs_status launch_tb6_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
     return BCGS_OK;
 }
 
-template <int K, int RY, int NW, int NS, int MODE, int MINB = 1>
+template <int K, int RY, int NW, int NS, int MODE, int MINB = 1, bool XUPD = false>
 bcgs_status launch_tb4_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
 {
     using S = Tb4Shape<K, RY, NW, NS>;
-    auto kern = k_cheb_tb4<K, RY, NW, NS, MODE, MINB>;
+    auto kern = k_cheb_tb4<K, RY, NW, NS, MODE, MINB, XUPD>;
     static bool attr = false;
     if (!attr) {
         CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -154,6 +157,8 @@ template <int K, int MODE>
 bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz)
 {
     if constexpr (K <= 5) {   // register budget: warp-row layouts up to K = 5
+        if (MODE == MODE_P && c->defer_x)   // deferred a11 fused into the p-kernel (16 warps)
+            return launch_tb4_k<K, 2, 16, 4, MODE, 1, true>(c, a, nz);
         if (c->tb_variant == 5 && tma_ok(c)) return launch_tb4_k<K, 2, 16, 4, MODE>(c, a, nz);
         if constexpr (K <= 4) {
             if (c->tb_variant == 7 && tma_ok(c)) return launch_tb4_k<K, 2, 24, 3, MODE>(c, a, nz);
