@@ -93,6 +93,7 @@ struct Tb4Thread {
     const CUtensorMap* pmap;
     double* side;
     bool xdo;          // XUPD: this launch applies the previous iteration's x update
+    double xv[RY], phv[RY], rhv[RY];   // XUPD operands of the plane due next step
 
     static constexpr int ninputs() { return MODE == MODE_PLAIN ? 1 : (MODE == MODE_P ? 3 : 2); }
 
@@ -123,20 +124,16 @@ struct Tb4Thread {
     template <int PH, bool MASK>
     __device__ __forceinline__ void step(int t)
     {
-        // ---- deferred a11 of the previous iteration on plane t - K (read p̂_{i-1} before
-        //      this step's level K overwrites it with p̂_i; same thread, same point)
-        double xv[RY], phv[RY], rhv[RY];
-        const int mx = t - K;
-        const bool xs = XUPD && xdo && mx >= c0 && mx < c1;
-        if (XUPD && xs) {
+        // ---- deferred a11 of the previous iteration on plane t - K: the operands were loaded
+        //      at the end of step t-1 (registers live only across the barrier); p̂_{i-1} of
+        //      plane t - K is read before this step's level K overwrites it with p̂_i.
+        if (XUPD && xdo) {
+            const int mx = t - K;
+            if (mx >= c0 && mx < c1) {
 #pragma unroll
-            for (int r = 0; r < RY; ++r) {
-                if (in_tile[r]) {
-                    const int64_t e = col[r] + plane * mx;
-                    xv[r] = a->x[e];
-                    phv[r] = a->out[e];
-                    rhv[r] = __ldg(a->rh + e);
-                }
+                for (int r = 0; r < RY; ++r)
+                    if (in_tile[r])
+                        a->x[col[r] + plane * mx] = upd_x(xv[r], phv[r], rhv[r], alpha, omega);
             }
         }
         // ---- level 0 from the TMA stage of plane t
@@ -214,11 +211,6 @@ struct Tb4Thread {
                 }
             }
         }
-        if (XUPD && xs) {
-#pragma unroll
-            for (int r = 0; r < RY; ++r)
-                if (in_tile[r]) a->x[col[r] + plane * mx] = upd_x(xv[r], phv[r], rhv[r], alpha, omega);
-        }
         double* cur = sm + S::PAD + (t & 1) * (K * PLANE) + ey0 * EX + lane;
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
@@ -231,6 +223,31 @@ struct Tb4Thread {
         if (threadIdx.x == 0 && t + NS < b1 && t + NS <= t1) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue(t + NS);
+        }
+        if (XUPD && xdo) xload(t + 1);
+    }
+
+    // XUPD: load the a11 operands of plane tt - K into registers (consumed at the top of
+    // step tt) and prefetch plane tt + XPF - K into L2.
+    static constexpr int XPF = 4;
+    __device__ __forceinline__ void xload(int tt)
+    {
+        const int mx = tt - K, mp = mx + XPF;
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+            if (!in_tile[r]) continue;
+            if (mx >= c0 && mx < c1) {
+                const int64_t e = col[r] + plane * mx;
+                xv[r] = a->x[e];
+                phv[r] = a->out[e];
+                rhv[r] = __ldg(a->rh + e);
+            }
+            if (mp >= c0 && mp < c1) {
+                const int64_t e = col[r] + plane * mp;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(a->x + e));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(a->out + e));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(a->rh + e));
+            }
         }
     }
 
@@ -296,6 +313,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constan
     th.first = false;
     th.pmap = nullptr;
     th.side = nullptr;
+    th.xdo = false;
     if (MODE == MODE_P) {
         const int par = st->iter & 1;
         th.first = (st->iter == 0);
@@ -303,6 +321,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constan
         th.omega = st->omega;
         th.pmap = par ? &maps.pb : &maps.pa;
         th.side = par ? a.side_a : a.side_b;
+        if (XUPD) {
+            th.alpha = st->alpha;            // α_{i-1}, ω_{i-1} of the pending x update
+            th.xdo = !th.first && st->x_applied != st->iter;
+        }
     } else if (MODE == MODE_S) {
         th.alpha = st->alpha;
         th.side = a.side_a;
@@ -358,6 +380,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constan
     __syncthreads();
     if (threadIdx.x == 0)
         for (int tt = th.t0; tt < th.t0 + NS && tt < th.b1 && tt <= th.t1; ++tt) th.issue(tt);
+    if (XUPD && th.xdo) th.xload(th.t0);
 
     // interior tile: the extended tile lies inside the grid -> masks only near block ends
     const bool interior = th.tx0 >= 0 && th.tx0 + 32 <= a.nx && th.ty0 >= 0 &&
