@@ -70,6 +70,7 @@ struct Tb4Shape {
     static constexpr size_t level_bytes = sizeof(double) * 2 * K * PLANE;
     static constexpr size_t stage_bytes = sizeof(double) * (size_t)NS * 3 * BOX;
     static constexpr size_t smem = level_bytes + stage_bytes + 128;
+    static constexpr size_t xupd_bytes = sizeof(double) * 2 * 3 * NW * 32 * RY;
 };
 
 template <int K, int RY, int NW, int NS, int MODE, bool XUPD = false>
@@ -93,7 +94,7 @@ struct Tb4Thread {
     const CUtensorMap* pmap;
     double* side;
     bool xdo;          // XUPD: this launch applies the previous iteration's x update
-    double xv[RY], phv[RY], rhv[RY];   // XUPD operands of the plane due next step
+    double* xsm;       // XUPD: [2][3][XN] cp.async landing buffers
 
     static constexpr int ninputs() { return MODE == MODE_PLAIN ? 1 : (MODE == MODE_P ? 3 : 2); }
 
@@ -124,17 +125,22 @@ struct Tb4Thread {
     template <int PH, bool MASK>
     __device__ __forceinline__ void step(int t)
     {
-        // ---- deferred a11 of the previous iteration on plane t - K: the operands were loaded
-        //      at the end of step t-1 (registers live only across the barrier); p̂_{i-1} of
-        //      plane t - K is read before this step's level K overwrites it with p̂_i.
+        // ---- deferred a11 of the previous iteration on plane t - K.  Its operands were
+        //      copied to shared memory by cp.async issued one step earlier (no registers held
+        //      across the sweeps); p̂_{i-1}(t-K) is read here, before this step's level K
+        //      overwrites it with p̂_i.  Then the copies for plane t+1-K are issued.
         if (XUPD && xdo) {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
             const int mx = t - K;
             if (mx >= c0 && mx < c1) {
+                const double* xb = xsm + (size_t)(t & 1) * 3 * XN + threadIdx.x * RY;
 #pragma unroll
                 for (int r = 0; r < RY; ++r)
                     if (in_tile[r])
-                        a->x[col[r] + plane * mx] = upd_x(xv[r], phv[r], rhv[r], alpha, omega);
+                        a->x[col[r] + plane * mx] =
+                            upd_x(xb[r], xb[XN + r], xb[2 * XN + r], alpha, omega);
             }
+            xissue(t + 1);
         }
         // ---- level 0 from the TMA stage of plane t
         double q0[RY];
@@ -224,34 +230,30 @@ struct Tb4Thread {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue(t + NS);
         }
-        if (XUPD && xdo) xload(t + 1);
     }
 
-    // XUPD: load the a11 operands of plane tt - K into registers (consumed at the top of
-    // step tt) and prefetch plane tt + XPF - K into L2.
-    static constexpr int XPF = 4;
-    __device__ __forceinline__ void xload(int tt)
+    // XUPD: cp.async the a11 operands (x, p̂, r̂) of plane tt - K into slot tt & 1
+    static constexpr int XN = NW * 32 * RY;
+    __device__ __forceinline__ void xissue(int tt)
     {
-        const int mx = tt - K, mp = mx + XPF;
+        const int mx = tt - K;
+        if (mx >= c0 && mx < c1) {
+            double* xb = xsm + (size_t)(tt & 1) * 3 * XN + threadIdx.x * RY;
 #pragma unroll
-        for (int r = 0; r < RY; ++r) {
-            if (!in_tile[r]) continue;
-            if (mx >= c0 && mx < c1) {
+            for (int r = 0; r < RY; ++r) {
+                if (!in_tile[r]) continue;
                 const int64_t e = col[r] + plane * mx;
-                xv[r] = a->x[e];
-                phv[r] = a->out[e];
-                rhv[r] = __ldg(a->rh + e);
-            }
-            if (mp >= c0 && mp < c1) {
-                const int64_t e = col[r] + plane * mp;
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(a->x + e));
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(a->out + e));
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(a->rh + e));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(xb + r)),
+                             "l"(a->x + e));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(xb + XN + r)),
+                             "l"(a->out + e));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(xb + 2 * XN + r)),
+                             "l"(a->rh + e));
             }
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
     }
 
-    // steps [tb, te) (te - tb a multiple of U unless FULL == false)
     template <bool MASK>
     __device__ __forceinline__ void run_blocks(int tb, int nblk)
     {
@@ -309,6 +311,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constan
     th.stg = smraw;                                              // 128-B aligned TMA boxes
     th.sm = smraw + (size_t)NS * 3 * S::BOX;
     th.bar = reinterpret_cast<uint64_t*>(th.sm + 2 * K * S::PLANE);
+    th.xsm = reinterpret_cast<double*>(reinterpret_cast<char*>(smraw) + S::smem);
     th.alpha = th.beta = th.omega = 0.0;
     th.first = false;
     th.pmap = nullptr;
@@ -380,7 +383,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constan
     __syncthreads();
     if (threadIdx.x == 0)
         for (int tt = th.t0; tt < th.t0 + NS && tt < th.b1 && tt <= th.t1; ++tt) th.issue(tt);
-    if (XUPD && th.xdo) th.xload(th.t0);
+    if (XUPD && th.xdo) th.xissue(th.t0);
 
     // interior tile: the extended tile lies inside the grid -> masks only near block ends
     const bool interior = th.tx0 >= 0 && th.tx0 + 32 <= a.nx && th.ty0 >= 0 &&

@@ -136,11 +136,13 @@ template <int K, int RY, int NW, int NS, int MODE, int MINB = 1, bool XUPD = fal
 bcgs_status launch_tb4_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
 {
     using S = Tb4Shape<K, RY, NW, NS>;
+    constexpr size_t smem = S::smem + (XUPD ? S::xupd_bytes : 0);
+    static_assert(smem <= 227 * 1024, "tb4 shared memory budget");
     auto kern = k_cheb_tb4<K, RY, NW, NS, MODE, MINB, XUPD>;
     static bool attr = false;
     if (!attr) {
         CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)S::smem));
+                                        (int)smem));
         attr = true;
     }
     TbMaps maps;
@@ -148,7 +150,7 @@ bcgs_status launch_tb4_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
         return fail(c, BCGS_E_CUDA, "cuTensorMapEncodeTiled failed");
     dim3 grid((unsigned)((a.nx + S::TX - 1) / S::TX), (unsigned)((a.ny + S::TY - 1) / S::TY),
               (unsigned)nchunk_total);
-    kern<<<grid, NW * 32, S::smem, c->s>>>(a, maps);
+    kern<<<grid, NW * 32, smem, c->s>>>(a, maps);
     CUDA_OK(c, cudaGetLastError());
     return BCGS_OK;
 }
@@ -158,7 +160,7 @@ bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz)
 {
     if constexpr (K <= 5) {   // register budget: warp-row layouts up to K = 5
         if (MODE == MODE_P && c->defer_x)   // deferred a11 fused into the p-kernel (16 warps)
-            return launch_tb4_k<K, 2, 16, 4, MODE, 1, true>(c, a, nz);
+            return launch_tb4_k<K, 2, 16, (K <= 4 ? 4 : 3), MODE, 1, true>(c, a, nz);
         if (c->tb_variant == 5 && tma_ok(c)) return launch_tb4_k<K, 2, 16, 4, MODE>(c, a, nz);
         if constexpr (K <= 4) {
             if (c->tb_variant == 7 && tma_ok(c)) return launch_tb4_k<K, 2, 24, 3, MODE>(c, a, nz);
