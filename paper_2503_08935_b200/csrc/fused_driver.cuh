@@ -121,7 +121,8 @@ bcgs_status precond_apply(bcgs_ctx c, const double* q, double* out)
 
 void on_begin(bcgs_ctx c)
 {
-    c->defer_x = (c->kernels == 1 && c->pc != BCGS_PC_NONE && (c->lay.nx % 2) == 0 &&
+    c->defer_x = (c->defer_x_opt && c->kernels == 1 && c->pc != BCGS_PC_NONE &&
+                  (c->lay.nx % 2) == 0 &&
                   defer_x_ok(c)) ? 1 : 0;
 }
 

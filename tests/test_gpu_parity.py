@@ -251,3 +251,21 @@ def test_c5_1024_properties(bc):
     s.close()
     del s
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("n,pc,k,bpr", [(64, "gnocomm", 4, 1), (48, "bj", 3, 2), ((40, 36, 48), "gnocomm", 5, 3)])
+def test_deferred_x_update_parity(bc, orc, n, pc, k, bpr):
+    """BCGS_OPT_DEFER_X: a11 applied inside the next p-kernel (and flushed at the end) gives
+    the same x as the oracle, bitwise."""
+    n3 = (n,) * 3 if np.isscalar(n) else n
+    h = si.unit_cube_h(n3[0])
+    s = bc.Solver(n3, h)
+    s.set_option(bc.OPT_DEFER_X, 1)
+    s.set_preconditioner(pc, k, blocks_per_rank=bpr)
+    s.set_rhs_random(si.SEED)
+    rep = s.solve(tol=1e-8)
+    b = orc.rhs_random(n3[::-1], si.SEED)
+    o = orc.bicgstab(b, h, pc=pc, k=k, nslab=bpr, tol=1e-8)
+    assert rep["iterations"] == o.iterations
+    assert np.array_equal(s.residual_history(), o.history)
+    assert np.array_equal(host(s.solution()), o.x)
