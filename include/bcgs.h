@@ -167,6 +167,8 @@ bcgs_status bcgs_solve(bcgs_ctx ctx, double rel_tol, int32_t max_iter, int32_t f
 bcgs_status bcgs_begin(bcgs_ctx ctx, double rel_tol, int32_t max_iter, int32_t fixed_iters);
 bcgs_status bcgs_iterate(bcgs_ctx ctx, int32_t n);
 bcgs_status bcgs_finish(bcgs_ctx ctx, bcgs_report* out);
+/* Order the caller's stream after all work enqueued so far (no host synchronisation). */
+bcgs_status bcgs_join(bcgs_ctx ctx);
 
 /* Residual history rel_0..rel_iters (rel_0 = 1); returns the count copied. */
 int32_t bcgs_residual_history(bcgs_ctx ctx, double* host_out, int32_t cap);

@@ -33,6 +33,7 @@ EXPORTS = [
     "bcgs_last_error", "bcgs_set_option", "bcgs_set_rhs_random", "bcgs_set_rhs",
     "bcgs_set_boundary_value", "bcgs_set_initial_guess", "bcgs_set_preconditioner",
     "bcgs_set_eigen_bounds", "bcgs_solve", "bcgs_begin", "bcgs_iterate", "bcgs_finish",
+    "bcgs_join",
     "bcgs_residual_history", "bcgs_scalar_history", "bcgs_get_solution",
     "bcgs_apply_operator", "bcgs_apply_preconditioner", "bcgs_dot", "bcgs_kernel_times",
     "bcgs_kernel_times_reset",
@@ -97,6 +98,7 @@ def load() -> ctypes.CDLL:
         "bcgs_begin": (i32, [P, f64, i32, i32]),
         "bcgs_iterate": (i32, [P, i32]),
         "bcgs_finish": (i32, [P, ctypes.POINTER(Report)]),
+        "bcgs_join": (i32, [P]),
         "bcgs_residual_history": (i32, [P, P, i32]),
         "bcgs_scalar_history": (i32, [P, P, i32]),
         "bcgs_get_solution": (i32, [P, P, i32]),
@@ -252,6 +254,10 @@ class Solver:
 
     def iterate(self, n: int):
         self._check(self.lib.bcgs_iterate(self.ctx, n), "bcgs_iterate")
+
+    def join_stream(self):
+        """Make the caller's stream wait for the library stream (stream-ordered, no host sync)."""
+        self._check(self.lib.bcgs_join(self.ctx), "bcgs_join")
 
     def finish(self) -> dict:
         rep = Report()

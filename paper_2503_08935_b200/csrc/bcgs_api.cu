@@ -730,9 +730,16 @@ bcgs_status bcgs_iterate(bcgs_ctx c, int32_t n)
 {
     if (!c || n < 0) return BCGS_E_INVALID;
     if (!c->begun) return fail(c, BCGS_E_STATE, "bcgs_iterate before bcgs_begin");
+    TRY(enter(c));   // ordered after prior work on the caller's stream
     TRY(enqueue_iterations(c, n));
     c->launched += n;
     return BCGS_OK;
+}
+
+bcgs_status bcgs_join(bcgs_ctx c)
+{
+    if (!c) return BCGS_E_INVALID;
+    return leave(c);
 }
 
 static bcgs_status poll_state(bcgs_ctx c, int32_t* done, int32_t* iter)
