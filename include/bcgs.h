@@ -84,8 +84,8 @@ typedef enum {
     BCGS_OPT_PROFILE = 2,      /* 1 = CUDA events around every kernel (bcgs_kernel_times) */
     BCGS_OPT_POLL = 3,         /* iterations launched between done-flag polls (tol mode)  */
     BCGS_OPT_TB_VARIANT = 4,   /* temporally blocked kernel layout (tuning): 2 = square   */
-                               /* tile, 3 = warp-row, 5 = TMA 16 warps, 7 = TMA 24 warps */
-                               /* (default), 8 = RY=1, 9 = 2x2 register tiles, 10 = 2/SM */
+                               /* tile (any k, odd nx), 5 = TMA warp-row 16 warps,       */
+                               /* 7 = TMA warp-row 24 warps (default; k <= 4)            */
     BCGS_OPT_DEFER_X = 5       /* 1 = apply x += αp̂ + ωr̂ inside the next p-kernel (off)    */
 } bcgs_option;
 

@@ -37,23 +37,14 @@ __global__ void k_update_xr_s(double* __restrict__ x, const double* __restrict__
 // tile (TX, TY) of a kernel variant for degree k
 void variant_tile(int variant, int k, int* tx, int* ty)
 {
+    const int hx = (k + 1) / 2 * 2;                        // TMA: even x-halo
     if (variant == 2 || k > 5) {
         *tx = 32; *ty = 16;
         if (k >= 7) { *tx = 16; *ty = 8; } else if (k >= 5) { *tx = 32; *ty = 8; }
-    } else if (variant == 5 || variant == 6) {
-        *tx = 32 - 2 * ((k + 1) / 2 * 2); *ty = 32 - 2 * k;   // TMA: even x-halo
-    } else if (variant == 10 && k <= 4) {
-        *tx = 32 - 2 * ((k + 1) / 2 * 2); *ty = 24 - 2 * k;   // 12 warps, 2 CTAs per SM
-    } else if (variant == 9 && k <= 4) {
-        *tx = 64 - 2 * ((k + 1) / 2 * 2); *ty = 24 - 2 * k;   // 2x2 register tiles, 12 warps
-    } else if (variant == 8 && k <= 4) {
-        *tx = 32 - 2 * ((k + 1) / 2 * 2); *ty = 32 - 2 * k;   // 32 warps, RY = 1
     } else if (variant == 7 && k <= 4) {
-        *tx = 32 - 2 * ((k + 1) / 2 * 2); *ty = 48 - 2 * k;   // 24 warps
-    } else if (variant == 4) {
-        *tx = 32 - 2 * k; *ty = 32 - 2 * k;      // RY = 4, NW = 8
+        *tx = 32 - 2 * hx; *ty = 48 - 2 * k;               // 24 warps x RY = 2
     } else {
-        *tx = 32 - 2 * k; *ty = 32 - 2 * k;      // RY = 2, NW = 16
+        *tx = 32 - 2 * hx; *ty = 32 - 2 * k;               // 16 warps x RY = 2 (variant 5)
     }
 }
 
@@ -80,8 +71,7 @@ bcgs_status launch_tb(bcgs_ctx c, TbArgs& a)
     double best = 1e300;
     for (int64_t nch = 1; nch <= std::max<int64_t>(1, a.Lb / 8); ++nch) {
         const int64_t zc = (a.Lb + nch - 1) / nch;
-        const int64_t conc = kNumSMs * (c->tb_variant == 10 ? 2 : 1);
-        const int64_t waves = (tiles * nch + conc - 1) / conc;
+            const int64_t waves = (tiles * nch + kNumSMs - 1) / kNumSMs;
         const double cost = (double)waves * (double)(zc + 2 * k);
         if (cost < best * 0.999) {
             best = cost;

@@ -239,247 +239,8 @@ __global__ void __launch_bounds__(TbShape<K, TX, TY>::NT, 1) k_cheb_tb(TbArgs a)
     }
 }
 
-// ------------------------------------------------------------------------------------
-// k_cheb_tb3: warp-row layout.  The extended tile is 32 columns wide (one warp lane per
-// column, TX = 32 - 2K output columns) and EY = NW*RY rows; each thread owns RY vertically
-// adjacent points of its column, so y-neighbours inside the segment come from registers
-// (RY independent dependency chains per thread = ILP) and only the segment ends read
-// shared memory.  A warp skips level j entirely (warp-uniform branch) when none of its
-// rows lies within the level-j halo, so the recomputed halo costs ~(1 + K/TY) instead of
-// the full extended tile.
-template <int K, int RY, int NW>
-struct Tb3Shape {
-    static constexpr int EX = 32, EY = NW * RY, TX = EX - 2 * K, TY = EY - 2 * K;
-    static constexpr int PAD = EX;                 // one guard row above and below
-    static constexpr int PLANE = EX * EY + 2 * PAD;
-    static constexpr size_t smem = sizeof(double) * 2 * K * PLANE;
-    static constexpr int QW = ((K + 1 + 2) / 3) * 3 < 3 ? 3 : ((K + 1 + 2) / 3) * 3;
-};
-
-template <int K, int RY, int NW, int MODE>
-struct Tb3Thread {
-    using S = Tb3Shape<K, RY, NW>;
-    static constexpr int EX = S::EX, TX = S::TX, TY = S::TY, PLANE = S::PLANE, QW = S::QW;
-
-    double qw[QW][RY];
-    double win[K > 1 ? K : 2][3][RY];
-    double nr[RY], np[RY], nw[RY];
-    const TbArgs* a;
-    double* sm;
-    int lane, ey0, b0, b1, c0, c1, wdy;   // wdy: min y-distance of this warp's rows
-    int64_t col[RY], plane;
-    unsigned actmask[RY];
-    bool in_dom[RY], in_tile[RY], first;
-    double alpha, beta, omega;
-    const double* pin;
-    double* side;
-
-    __device__ __forceinline__ void load(int t)
-    {
-#pragma unroll
-        for (int r = 0; r < RY; ++r) {
-            if (in_dom[r] && t < b1) {
-                const int64_t c = col[r] + plane * t;
-                if (MODE == MODE_PLAIN) {
-                    nr[r] = __ldg(a->q + c);
-                } else if (MODE == MODE_P) {
-                    np[r] = __ldg(pin + c);
-                    if (!first) {
-                        nr[r] = __ldg(a->r + c);
-                        nw[r] = __ldg(a->w + c);
-                    }
-                } else {
-                    nr[r] = __ldg(a->r + c);
-                    nw[r] = __ldg(a->w + c);
-                }
-            }
-        }
-    }
-
-    template <int PH>
-    __device__ __forceinline__ void step(int t)
-    {
-        double q0[RY];
-#pragma unroll
-        for (int r = 0; r < RY; ++r) {
-            q0[r] = 0.0;
-            if (in_dom[r] && t < b1) {
-                if (MODE == MODE_PLAIN) q0[r] = nr[r];
-                else if (MODE == MODE_P) q0[r] = first ? np[r] : upd_p(nr[r], np[r], nw[r], beta, omega);
-                else q0[r] = upd_s(nr[r], nw[r], alpha);
-                if (MODE != MODE_PLAIN && in_tile[r] && t >= c0 && t < c1)
-                    side[col[r] + plane * t] = q0[r];
-            }
-        }
-        load(t + 1);
-#pragma unroll
-        for (int r = 0; r < RY; ++r) qw[PH % QW][r] = q0[r];
-        const double* prev = sm + S::PAD + ((t - 1) & 1) * (K * PLANE);
-#pragma unroll
-        for (int j = 1; j <= K; ++j) {
-            const int m = t - j;
-            const bool mok = (unsigned)(m - b0) < (unsigned)(b1 - b0);
-            if (wdy <= K - j) {                       // warp-uniform level skip
-                const double* pl = prev + (j - 1) * PLANE + ey0 * EX + lane;
-                double v[RY];
-#pragma unroll
-                for (int r = 0; r < RY; ++r) {
-                    // x_{j-1} at plane m: this row (zc), rows r-1 / r+1, planes m-1 / m+1
-                    double zm, zc, zp, yc_m, yc_p;
-                    if (j == 1) {
-                        zp = qw[PH % QW][r];
-                        zc = qw[(PH + QW - 1) % QW][r];
-                        zm = qw[(PH + QW - 2) % QW][r];
-                        yc_m = r > 0 ? qw[(PH + QW - 1) % QW][r > 0 ? r - 1 : 0] : pl[(r - 1) * EX];
-                        yc_p = r < RY - 1 ? qw[(PH + QW - 1) % QW][r < RY - 1 ? r + 1 : 0]
-                                          : pl[(r + 1) * EX];
-                    } else {
-                        zp = win[j - 1][PH % 3][r];
-                        zc = win[j - 1][(PH + 2) % 3][r];
-                        zm = win[j - 1][(PH + 1) % 3][r];
-                        yc_m = r > 0 ? win[j - 1][(PH + 2) % 3][r > 0 ? r - 1 : 0] : pl[(r - 1) * EX];
-                        yc_p = r < RY - 1 ? win[j - 1][(PH + 2) % 3][r < RY - 1 ? r + 1 : 0]
-                                          : pl[(r + 1) * EX];
-                    }
-                    const double xm = pl[r * EX - 1], xp = pl[r * EX + 1];
-                    const double Sv = stencil_row(zc, xm, xp, yc_m, yc_p, zm, zp, a->h2inv);
-                    const double qc = qw[(PH + QW - j) % QW][r];
-                    double vv;
-                    if (j == 1) {
-                        vv = cheb_first(qc, Sv, a->g1, a->cz);
-                    } else {
-                        const double z2 = (j == 2) ? qc * a->cz : win[j - 2][(PH + 1) % 3][r];
-                        vv = cheb_step(qc, Sv, zc, z2, a->rho[j], a->rho[j - 1], a->A2, a->B2);
-                    }
-                    const bool act = ((actmask[r] >> j) & 1u) && mok;
-                    v[r] = act ? vv : 0.0;
-                }
-#pragma unroll
-                for (int r = 0; r < RY; ++r) {
-                    if (j < K) win[j][PH % 3][r] = v[r];
-                    else if (in_tile[r] && m >= c0 && m < c1) a->out[col[r] + plane * m] = v[r];
-                }
-            } else if (j < K) {
-#pragma unroll
-                for (int r = 0; r < RY; ++r) win[j][PH % 3][r] = 0.0;
-            }
-        }
-        double* cur = sm + S::PAD + (t & 1) * (K * PLANE) + ey0 * EX + lane;
-#pragma unroll
-        for (int r = 0; r < RY; ++r) {
-            cur[r * EX] = q0[r];
-#pragma unroll
-            for (int j = 1; j < K; ++j) cur[j * PLANE + r * EX] = win[j][PH % 3][r];
-        }
-        __syncthreads();
-    }
-};
-
-template <int K, int RY, int NW, int MODE>
-__global__ void __launch_bounds__(NW * 32, 1) k_cheb_tb3(TbArgs a)
-{
-    using T = Tb3Thread<K, RY, NW, MODE>;
-    using S = Tb3Shape<K, RY, NW>;
-    constexpr int TX = S::TX, TY = S::TY, U = S::QW;
-    extern __shared__ double sm[];
-
-    const DevState* st = a.st;
-    if (st && st->done) return;
-    T th;
-    th.a = &a;
-    th.sm = sm;
-    th.alpha = th.beta = th.omega = 0.0;
-    th.first = false;
-    th.pin = nullptr;
-    th.side = nullptr;
-    if (MODE == MODE_P) {
-        const int par = st->iter & 1;
-        th.first = (st->iter == 0);
-        th.beta = st->beta;
-        th.omega = st->omega;
-        th.pin = par ? a.p_b : a.p_a;
-        th.side = par ? a.side_a : a.side_b;
-    } else if (MODE == MODE_S) {
-        th.alpha = st->alpha;
-        th.side = a.side_a;
-    }
-    const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
-    th.lane = lane;
-    th.ey0 = wy * RY;
-    const int gx = blockIdx.x * TX + lane - K;
-    const int dx = max(K - lane, lane - (K + TX - 1));
-    int wdy = 1 << 20;
-#pragma unroll
-    for (int r = 0; r < RY; ++r) {
-        const int ey = th.ey0 + r;
-        const int gy = blockIdx.y * TY + ey - K;
-        const int dy = max(K - ey, ey - (K + TY - 1));
-        wdy = min(wdy, dy);
-        const int dist = max(dx, dy);
-        th.in_dom[r] = gx >= 0 && gx < a.nx && gy >= 0 && gy < a.ny;
-        th.in_tile[r] = th.in_dom[r] && dist <= 0;
-        th.col[r] = th.in_dom[r] ? gx + (int64_t)a.nx * gy : 0;
-        unsigned msk = 0;
-#pragma unroll
-        for (int j = 1; j <= K; ++j)
-            if (th.in_dom[r] && dist <= K - j) msk |= 1u << j;
-        th.actmask[r] = msk;
-        th.nr[r] = th.np[r] = th.nw[r] = 0.0;
-    }
-    th.wdy = wdy;
-    const int blk = blockIdx.z / a.nchunk, ch = blockIdx.z % a.nchunk;
-    th.b0 = blk * a.Lb;
-    th.b1 = th.b0 + a.Lb;
-    th.c0 = th.b0 + ch * a.zch;
-    th.c1 = min(th.b1, th.c0 + a.zch);
-    if (th.c0 >= th.b1) return;
-    const int t0 = max(th.b0, th.c0 - K), t1 = th.c1 - 1 + K;
-    th.plane = (int64_t)a.nx * a.ny;
-#pragma unroll
-    for (int d = 0; d < S::QW; ++d)
-#pragma unroll
-        for (int r = 0; r < RY; ++r) th.qw[d][r] = 0.0;
-#pragma unroll
-    for (int j = 0; j < (K > 1 ? K : 2); ++j)
-#pragma unroll
-        for (int r = 0; r < RY; ++r) th.win[j][0][r] = th.win[j][1][r] = th.win[j][2][r] = 0.0;
-    for (int i = threadIdx.x; i < 2 * K * S::PLANE; i += blockDim.x) sm[i] = 0.0;
-    __syncthreads();
-
-    th.load(t0);
-    int t = t0;
-    for (; t + U - 1 <= t1; t += U) {
-        th.template step<0>(t);
-        th.template step<1 % U>(t + 1);
-        th.template step<2 % U>(t + 2);
-        if (U > 3) {
-            th.template step<3 % U>(t + 3);
-            th.template step<4 % U>(t + 4);
-            th.template step<5 % U>(t + 5);
-        }
-        if (U > 6) {
-            th.template step<6 % U>(t + 6);
-            th.template step<7 % U>(t + 7);
-            th.template step<8 % U>(t + 8);
-        }
-    }
-    if (t <= t1) th.template step<0>(t);
-    if (t + 1 <= t1) th.template step<1 % U>(t + 1);
-    if (U > 3) {
-        if (t + 2 <= t1) th.template step<2 % U>(t + 2);
-        if (t + 3 <= t1) th.template step<3 % U>(t + 3);
-        if (t + 4 <= t1) th.template step<4 % U>(t + 4);
-    }
-    if (U > 6) {
-        if (t + 5 <= t1) th.template step<5 % U>(t + 5);
-        if (t + 6 <= t1) th.template step<6 % U>(t + 6);
-        if (t + 7 <= t1) th.template step<7 % U>(t + 7);
-    }
-}
-
 }  // namespace fused
 #include "k_tb4.cuh"
-#include "k_tb6.cuh"
 namespace fused {
 
 // ----------------------------------------------------------------------------- host side

@@ -35,24 +35,6 @@ bcgs_status launch_tb_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
     return BCGS_OK;
 }
 
-template <int K, int RY, int NW, int MODE>
-bcgs_status launch_tb3_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
-{
-    using S = Tb3Shape<K, RY, NW>;
-    auto kern = k_cheb_tb3<K, RY, NW, MODE>;
-    static bool attr = false;
-    if (!attr) {
-        CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)S::smem));
-        attr = true;
-    }
-    dim3 grid((unsigned)((a.nx + S::TX - 1) / S::TX), (unsigned)((a.ny + S::TY - 1) / S::TY),
-              (unsigned)nchunk_total);
-    kern<<<grid, NW * 32, S::smem, c->s>>>(a);
-    CUDA_OK(c, cudaGetLastError());
-    return BCGS_OK;
-}
-
 // ---- TMA tensor maps (cuTensorMapEncodeTiled through the runtime's driver entry point)
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -110,28 +92,6 @@ inline bool make_maps(bcgs_ctx c, TbMaps* maps, const TbArgs& a, int mode, int b
     return ok;
 }
 
-template <int K, int RY, int NW, int NS, int MODE>
-bcgs_status launch_tb6_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
-{
-    using S = Tb6Shape<K, RY, NW, NS>;
-    static_assert(S::smem <= 227 * 1024, "tb6 shared memory budget");
-    auto kern = k_cheb_tb6<K, RY, NW, NS, MODE>;
-    static bool attr = false;
-    if (!attr) {
-        CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)S::smem));
-        attr = true;
-    }
-    TbMaps maps;
-    if (!make_maps(c, &maps, a, MODE, S::EY, S::EX))
-        return fail(c, BCGS_E_CUDA, "cuTensorMapEncodeTiled failed");
-    dim3 grid((unsigned)((a.nx + S::TX - 1) / S::TX), (unsigned)((a.ny + S::TY - 1) / S::TY),
-              (unsigned)nchunk_total);
-    kern<<<grid, NW * 32, S::smem, c->s>>>(a, maps);
-    CUDA_OK(c, cudaGetLastError());
-    return BCGS_OK;
-}
-
 template <int K, int RY, int NW, int NS, int MODE, int MINB = 1, bool XUPD = false>
 bcgs_status launch_tb4_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
 {
@@ -164,12 +124,7 @@ bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz)
         if (c->tb_variant == 5 && tma_ok(c)) return launch_tb4_k<K, 2, 16, 4, MODE>(c, a, nz);
         if constexpr (K <= 4) {
             if (c->tb_variant == 7 && tma_ok(c)) return launch_tb4_k<K, 2, 24, 3, MODE>(c, a, nz);
-            if (c->tb_variant == 8 && tma_ok(c)) return launch_tb4_k<K, 1, 32, 4, MODE>(c, a, nz);
-            if (c->tb_variant == 9 && tma_ok(c)) return launch_tb6_k<K, 2, 12, 3, MODE>(c, a, nz);
-            if (c->tb_variant == 10 && tma_ok(c))
-                return launch_tb4_k<K, 2, 12, 3, MODE, 2>(c, a, nz);   // 2 CTAs / SM
         }
-        if (c->tb_variant == 3) return launch_tb3_k<K, 2, 16, MODE>(c, a, nz);
     }
     return launch_tb_k<K, MODE>(c, a, nz);
 }

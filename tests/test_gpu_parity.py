@@ -269,3 +269,19 @@ def test_deferred_x_update_parity(bc, orc, n, pc, k, bpr):
     assert rep["iterations"] == o.iterations
     assert np.array_equal(s.residual_history(), o.history)
     assert np.array_equal(host(s.solution()), o.x)
+
+
+@pytest.mark.parametrize("variant", [2, 5, 7])
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_tb_variants_bitwise(bc, orc, variant, k):
+    """Every temporally blocked layout (square tile / TMA warp-row 16 or 24 warps) gives the
+    oracle's Chebyshev application bitwise, including ragged tiles and a block cut."""
+    n3 = (70, 52, 40)
+    h = si.unit_cube_h(70)
+    s = bc.Solver(n3, h)
+    s.set_option(bc.OPT_TB_VARIANT, variant)
+    s.set_preconditioner("gnocomm", k, blocks_per_rank=2)
+    q = np.random.default_rng(7).standard_normal(n3[::-1])
+    out = host(s.apply_preconditioner(dev(q)))
+    ivl, _, _ = bc.chebyshev_constants(n3, h, 2, "gnocomm", k)
+    assert np.array_equal(out, orc.apply_cheb(q, h, 2, k, ivl[0], ivl[1]))
