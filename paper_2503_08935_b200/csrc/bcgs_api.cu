@@ -610,6 +610,7 @@ bcgs_status bcgs_set_option(bcgs_ctx c, int32_t option, int64_t value)
     case BCGS_OPT_POLL: c->poll = std::max<int>(1, (int)value); break;
     case BCGS_OPT_TB_VARIANT: c->tb_variant = (int)value; break;
     case BCGS_OPT_DEFER_X: c->defer_x_opt = (int)value; break;
+    case BCGS_OPT_STENCIL_CFG: c->stencil_cfg = (int)value; break;
     default: return fail(c, BCGS_E_INVALID, "unknown option %d", option);
     }
     drop_graph(c);

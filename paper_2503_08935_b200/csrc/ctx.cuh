@@ -130,7 +130,8 @@ struct bcgs_ctx_s {
     double* h_pinned = nullptr;    // small pinned buffer for flag polls
     // options
     int defer_x = 0;                  // fused path: a11 applied inside the next p-kernel
-    int defer_x_opt = 0;              // BCGS_OPT_DEFER_X (measured slower at 512^3: off)
+    int defer_x_opt = 0;
+    int stencil_cfg = 0;              // BCGS_OPT_STENCIL_CFG (k_stream.cuh launch configs)              // BCGS_OPT_DEFER_X (measured slower at 512^3: off)
     int kernels = 1, use_graph = 1, profile = 0, poll = 8, tb_variant = 7;
     // preconditioner
     bcgs_pc pc = BCGS_PC_NONE;

@@ -135,12 +135,19 @@ bcgs_status halo_stencil(bcgs_ctx c, double* v, const double* a, double* out, in
                          int* nparts)
 {
     const int nx = (int)c->lay.nx, ny = (int)c->lay.ny, L = (int)c->lay.L;
-    const dim3 sb(stream::SBX, stream::SBY);
+    const int cfg = std::min(std::max(c->stencil_cfg, 0), stream::NCFG - 1);
+    const dim3 sb(stream::CFG_BX[cfg], stream::CFG_BY[cfg]);
     int nb = 0;
     auto launch = [&](int kb, int ke) {
-        const dim3 g = stream::stencil2_grid(nx, ny, ke - kb);
-        stream::k_stencil2_dot<ND><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv,
-                                                       c->part + (int64_t)nb * ND, c->st);
+        const dim3 g = stream::stencil2_grid(nx, ny, ke - kb, cfg);
+        dd* pp = c->part + (int64_t)nb * ND;
+        switch (cfg) {
+        case 1: stream::k_stencil2_dot<ND, 32, 8, 16><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv, pp, c->st); break;
+        case 2: stream::k_stencil2_dot<ND, 32, 4, 16><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv, pp, c->st); break;
+        case 3: stream::k_stencil2_dot<ND, 64, 4, 8><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv, pp, c->st); break;
+        case 4: stream::k_stencil2_dot<ND, 32, 16, 4><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv, pp, c->st); break;
+        default: stream::k_stencil2_dot<ND, 32, 8, 8><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv, pp, c->st); break;
+        }
         nb += (int)(g.x * g.y * g.z);
     };
     Prof pf(c, kc, 24.0 * npts(c));

@@ -246,7 +246,8 @@ namespace fused {
 // ----------------------------------------------------------------------------- host side
 inline int64_t max_blocks(int64_t nx, int64_t ny, int64_t L)
 {   // partial-sum slots of the stream::k_stencil2_dot grid (k_stream.cuh)
-    return ((nx / 2 + 31) / 32) * ((ny + 7) / 8) * ((L + 7) / 8 + 2);   // + 2 boundary launches
+    // worst case over the stencil launch configurations (x pairs / 32, rows / 4, planes / 4)
+    return ((nx / 2 + 31) / 32) * ((ny + 3) / 4) * ((L + 3) / 4 + 2);   // + 2 boundary launches
 }
 inline bool supported(int64_t, int64_t, int64_t, int, int degree, bool has_pc)
 {

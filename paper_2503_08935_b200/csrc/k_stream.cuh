@@ -12,12 +12,16 @@
 
 namespace stream {
 
-constexpr int SBX = 32, SBY = 8, SZC = 8;   // threads (x pairs) x rows, planes per thread
+constexpr int SBX = 32, SBY = 8, SZC = 8;   // default: threads (x pairs) x rows, planes/thread
+// launch configurations selectable with BCGS_OPT_STENCIL_CFG (tuning)
+constexpr int NCFG = 5;
+constexpr int CFG_BX[NCFG] = {32, 32, 32, 64, 32}, CFG_BY[NCFG] = {8, 8, 4, 4, 16},
+              CFG_ZC[NCFG] = {8, 16, 16, 8, 4};
 
 // w = A v (global operator; ghost planes hold halo data or zeros) and Dot2 partials of
 // a·w (ND >= 1) and w·w (ND == 2).  Each thread owns 2 adjacent x points of one row and
 // marches SZC planes; requires nx even (16-byte aligned rows).
-template <int ND>
+template <int ND, int SBX, int SBY, int SZC>
 __global__ void __launch_bounds__(SBX * SBY) k_stencil2_dot(const double* __restrict__ v,
                                                             const double* __restrict__ a,
                                                             double* __restrict__ out, int nx,
@@ -67,10 +71,11 @@ __global__ void __launch_bounds__(SBX * SBY) k_stencil2_dot(const double* __rest
     }
 }
 
-inline dim3 stencil2_grid(int64_t nx, int64_t ny, int64_t nplanes)
+inline dim3 stencil2_grid(int64_t nx, int64_t ny, int64_t nplanes, int cfg = 0)
 {
-    return dim3((unsigned)((nx / 2 + SBX - 1) / SBX), (unsigned)((ny + SBY - 1) / SBY),
-                (unsigned)((nplanes + SZC - 1) / SZC));
+    return dim3((unsigned)((nx / 2 + CFG_BX[cfg] - 1) / CFG_BX[cfg]),
+                (unsigned)((ny + CFG_BY[cfg] - 1) / CFG_BY[cfg]),
+                (unsigned)((nplanes + CFG_ZC[cfg] - 1) / CFG_ZC[cfg]));
 }
 
 // a11 + a12: x = fma(ω, r̂, fma(α, p̂, x)); r = fma(-ω, t, s); partials r~·r, r·r.
