@@ -141,6 +141,7 @@ __global__ void k_init_state(DevState* st, double tol, int max_iter, int fixed)
     st->done = DONE_RUNNING;
     st->iter = 0;
     st->x_applied = 0;
+    st->omega_iter = 0;
 }
 
 // ------------------------------------------------------------------ communication
@@ -352,7 +353,7 @@ bcgs_status enqueue_iterations(bcgs_ctx c, int n)
 {
     // graphs: single rank only (multi-rank runs launch directly; NCCL inside captured graphs
     // is supported but not exercised in round 1)
-    if (c->use_graph && !c->profile && !c->lg && c->nranks == 1) {
+    if (c->use_graph && !c->profile && !c->lg && c->nranks == 1 && !c->xconc) {
         if (!c->gexec) {
             cudaGraph_t graph;
             CUDA_OK(c, cudaStreamBeginCapture(c->s, cudaStreamCaptureModeThreadLocal));
@@ -512,7 +513,12 @@ static bcgs_status create_ctx(const bcgs_grid_desc* grid, int32_t rank, int32_t 
     c->lg = lg;
     *out = c;
     CUDA_OK(c, cudaSetDevice(cuda_device));
-    CUDA_OK(c, cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+    int prio_lo = 0, prio_hi = 0;
+    CUDA_OK(c, cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    CUDA_OK(c, cudaStreamCreateWithPriority(&c->s, cudaStreamNonBlocking, prio_hi));
+    CUDA_OK(c, cudaStreamCreateWithPriority(&c->s_x, cudaStreamNonBlocking, prio_lo));
+    CUDA_OK(c, cudaEventCreateWithFlags(&c->ev_omega, cudaEventDisableTiming));
+    CUDA_OK(c, cudaEventCreateWithFlags(&c->ev_xdone, cudaEventDisableTiming));
     CUDA_OK(c, cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
     CUDA_OK(c, cudaMallocHost(&c->h_pinned, 64));
     if (nranks > 1) {
@@ -583,6 +589,9 @@ void bcgs_destroy(bcgs_ctx c)
     if (c->ev_pre) cudaEventDestroy(c->ev_pre);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
     if (c->s_comm) cudaStreamDestroy(c->s_comm);
+    if (c->s_x) cudaStreamSynchronize(c->s_x), cudaStreamDestroy(c->s_x);
+    if (c->ev_omega) cudaEventDestroy(c->ev_omega);
+    if (c->ev_xdone) cudaEventDestroy(c->ev_xdone);
     if (c->ev_done) cudaEventDestroy(c->ev_done);
     if (c->lg) {
         bool last = true;
@@ -611,6 +620,7 @@ bcgs_status bcgs_set_option(bcgs_ctx c, int32_t option, int64_t value)
     case BCGS_OPT_TB_VARIANT: c->tb_variant = (int)value; break;
     case BCGS_OPT_DEFER_X: c->defer_x_opt = (int)value; break;
     case BCGS_OPT_STENCIL_CFG: c->stencil_cfg = (int)value; break;
+    case BCGS_OPT_XCONC: c->xconc_opt = (int)value; break;
     default: return fail(c, BCGS_E_INVALID, "unknown option %d", option);
     }
     drop_graph(c);

@@ -29,24 +29,25 @@ constexpr size_t kAlign = 256;
 enum KClass {
     KC_PRECOND = 0, KC_STENCIL1, KC_AXPY, KC_STENCIL2, KC_UPDATE_XR, KC_UPDATE_P,
     KC_FINALIZE, KC_HALO, KC_ALLGATHER, KC_SCALARS, KC_FUSED_P1, KC_FUSED_P2, KC_FUSED_XR,
-    KC_COUNT
+    KC_XCONC, KC_COUNT
 };
 inline const char* kClassName[KC_COUNT] = {
     "precond_sweep", "stencil_dot1", "axpy_s", "stencil_dot2", "update_xr", "update_p",
-    "finalize", "halo", "allgather", "scalars", "fused_p_cheb", "fused_s_cheb", "fused_xr"};
+    "finalize", "halo", "allgather", "scalars", "fused_p_cheb", "fused_s_cheb", "fused_xr",
+    "x_update_concurrent"};
 
 inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {
     int64_t nx, ny, nz, L, plane, vec_elems;   // vec_elems = (L + 2) * plane
     int64_t n_part;
-    size_t off_vec[16];
+    size_t off_vec[17];
     size_t off_state, off_hist, off_scal, off_part, off_rank, off_gath, total;
 };
 
 constexpr int V_X = 0, V_R = 1, V_RT = 2, V_P = 3, V_PH = 4, V_RH = 5, V_W = 6, V_T = 7,
               V_B = 8, V_C1 = 9, V_C2 = 10, V_IO = 11, V_W2 = 12, V_P2 = 13,
-              V_S = 14, V_COUNT = 15;
+              V_S = 14, V_PH2 = 15, V_COUNT = 16;
 
 inline int64_t stencil_blocks(int64_t nx, int64_t ny, int64_t L)
 {
@@ -131,7 +132,12 @@ struct bcgs_ctx_s {
     // options
     int defer_x = 0;                  // fused path: a11 applied inside the next p-kernel
     int defer_x_opt = 0;
-    int stencil_cfg = 0;              // BCGS_OPT_STENCIL_CFG (k_stream.cuh launch configs)              // BCGS_OPT_DEFER_X (measured slower at 512^3: off)
+    int stencil_cfg = 0;              // BCGS_OPT_STENCIL_CFG (k_stream.cuh launch configs)
+    int xconc_opt = 1;                // BCGS_OPT_XCONC: x update on a concurrent stream
+    int xconc = 0;                    // active for the current solve
+    int it_host = 0;                  // iterations enqueued since begin (host parity)
+    cudaStream_t s_x = nullptr;       // low-priority stream of the concurrent x update
+    cudaEvent_t ev_omega = nullptr, ev_xdone = nullptr;              // BCGS_OPT_DEFER_X (measured slower at 512^3: off)
     int kernels = 1, use_graph = 1, profile = 0, poll = 8, tb_variant = 7;
     // preconditioner
     bcgs_pc pc = BCGS_PC_NONE;

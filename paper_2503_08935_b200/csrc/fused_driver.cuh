@@ -111,6 +111,15 @@ bcgs_status precond_apply(bcgs_ctx c, const double* q, double* out)
 
 void on_begin(bcgs_ctx c)
 {
+    c->it_host = 0;
+    c->xconc = (c->xconc_opt && c->kernels == 1 && c->pc != BCGS_PC_NONE &&
+                (c->lay.nx % 2) == 0 && !c->defer_x_opt &&
+                supported(c->lay.nx, c->lay.ny, c->lay.L, c->bpr, c->degree, true)) ? 1 : 0;
+    if (c->xconc) {   // s_x starts after the setup (x = x0 written on s)
+        cudaEventRecord(c->ev_omega, c->s);
+        cudaStreamWaitEvent(c->s_x, c->ev_omega, 0);
+        cudaEventRecord(c->ev_xdone, c->s_x);
+    }
     c->defer_x = (c->defer_x_opt && c->kernels == 1 && c->pc != BCGS_PC_NONE &&
                   (c->lay.nx % 2) == 0 &&
                   defer_x_ok(c)) ? 1 : 0;
@@ -119,6 +128,11 @@ void on_begin(bcgs_ctx c)
 // deferred-x mode: bring x up to date (idempotent; stream-ordered)
 bcgs_status flush_x(bcgs_ctx c)
 {
+    if (c->xconc && c->begun) {   // join the concurrent x updates into the main stream
+        CUDA_OK(c, cudaEventRecord(c->ev_xdone, c->s_x));
+        CUDA_OK(c, cudaStreamWaitEvent(c->s, c->ev_xdone, 0));
+        return BCGS_OK;
+    }
     if (!c->defer_x || !c->begun) return BCGS_OK;
     stream::k_xflush<<<kEwBlocks, 256, 0, c->s>>>(F(c, V_X), F(c, V_PH), F(c, V_RH), npts(c),
                                                  c->st);
@@ -172,6 +186,11 @@ bcgs_status iteration(bcgs_ctx c)
 {
     const int64_t n = npts(c);
     DevState* st = c->st;
+    // concurrent-x mode: p̂ alternates between two buffers by iteration parity so that the
+    // x update of iteration i (reading p̂_i on s_x) overlaps the p-kernel of iteration i+1
+    const int par = c->xconc ? (c->it_host & 1) : 0;
+    double* ph = F(c, par ? V_PH2 : V_PH);
+    c->it_host += 1;
     ref::Grid g = ref_grid(c, (int)c->lay.L);
     dim3 sg = stencil_grid(c), sb(ref::BX, ref::BY);
     const int nsb = (int)(sg.x * sg.y * sg.z);
@@ -183,7 +202,7 @@ bcgs_status iteration(bcgs_ctx c)
         a.p_b = F(c, V_P2);
         a.side_a = F(c, V_P);
         a.side_b = F(c, V_P2);
-        a.out = F(c, V_PH);
+        a.out = ph;
         a.x = F(c, V_X);
         a.rh = F(c, V_RH);
         a.st = st;
@@ -193,14 +212,16 @@ bcgs_status iteration(bcgs_ctx c)
     const bool vec = (c->lay.nx % 2) == 0;   // 16-byte rows: vectorised streaming kernels
     int np1 = nsb, np2 = nsb;
     if (vec) {
-        TRY(halo_stencil<1>(c, F(c, V_PH), F(c, V_RT), F(c, V_W), KC_STENCIL1, &np1));
+        TRY(halo_stencil<1>(c, ph, F(c, V_RT), F(c, V_W), KC_STENCIL1, &np1));
     } else {
-        TRY(halo(c, F(c, V_PH)));
+        TRY(halo(c, ph));
         Prof pf(c, KC_STENCIL1, 24.0 * n);
-        ref::k_stencil_dot<1><<<sg, sb, 0, c->s>>>(F(c, V_PH), F(c, V_RT), F(c, V_W), g, 0,
+        ref::k_stencil_dot<1><<<sg, sb, 0, c->s>>>(ph, F(c, V_RT), F(c, V_W), g, 0,
                                                   c->part, st);
     }
     TRY(reduce<1>(c, np1, STAGE_ALPHA));
+    // r̂ is overwritten by K2: the previous iteration's concurrent x update must be done
+    if (c->xconc) CUDA_OK(c, cudaStreamWaitEvent(c->s, c->ev_xdone, 0));
     {   // K2: a6 + a7
         TbArgs a{};
         a.r = F(c, V_R);
@@ -220,7 +241,19 @@ bcgs_status iteration(bcgs_ctx c)
                                                   c->part, st);
     }
     TRY(reduce<2>(c, np2, STAGE_OMEGA));
-    if (vec && c->defer_x) {   // a12 only: x was (or will be) updated by the p-kernel
+    if (c->xconc) {   // a11 on the low-priority stream, overlapping a12 and the next p-kernel
+        CUDA_OK(c, cudaEventRecord(c->ev_omega, c->s));
+        CUDA_OK(c, cudaStreamWaitEvent(c->s_x, c->ev_omega, 0));
+        {
+            Prof pf(c, KC_XCONC, 32.0 * n, c->s_x);
+            stream::k_xupd_conc<<<kNumSMs, 256, 0, c->s_x>>>(
+                (double2*)F(c, V_X), (const double2*)F(c, V_PH), (const double2*)F(c, V_PH2),
+                (const double2*)F(c, V_RH), n / 2, st);
+            stream::k_xmark_conc<<<1, 1, 0, c->s_x>>>(st);
+        }
+        CUDA_OK(c, cudaEventRecord(c->ev_xdone, c->s_x));
+    }
+    if (vec && (c->defer_x || c->xconc)) {   // a12 only: x updated elsewhere
         Prof pf(c, KC_FUSED_XR, 32.0 * n);
         stream::k_update_r2<<<kEwBlocks, 256, 0, c->s>>>(
             (const double2*)F(c, V_S), (double2*)F(c, V_R), (const double2*)F(c, V_T),

@@ -202,4 +202,46 @@ __global__ void k_xflush(double* __restrict__ x, const double* __restrict__ ph,
 
 __global__ void k_xmark(DevState* st) { st->x_applied = st->iter; }
 
+// concurrent-x mode (a11 on its own low-priority stream, overlapping the ALU-bound
+// Chebyshev kernel of the next iteration): x = fma(ω, r̂, fma(α, p̂, x)) for iteration
+// omega_iter, with p̂ from the buffer of that iteration's parity and the (α, ω) snapshot.
+__global__ void __launch_bounds__(256) k_xupd_conc(double2* __restrict__ x,
+                                                   const double2* __restrict__ ph_a,
+                                                   const double2* __restrict__ ph_b,
+                                                   const double2* __restrict__ rh, int64_t n2,
+                                                   const DevState* __restrict__ st)
+{
+    const int it = st->omega_iter;
+    if (it < 1 || it == st->x_applied) return;
+    const double alpha = st->xa, omega = st->xw;
+    const double2* __restrict__ ph = ((it - 1) & 1) ? ph_b : ph_a;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; c + 3 * stride < n2; c += 4 * stride) {
+        double2 vx[4], vp[4], vr[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            vx[u] = x[c + u * stride];
+            vp[u] = __ldg(ph + c + u * stride);
+            vr[u] = __ldg(rh + c + u * stride);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            double2 o;
+            o.x = upd_x(vx[u].x, vp[u].x, vr[u].x, alpha, omega);
+            o.y = upd_x(vx[u].y, vp[u].y, vr[u].y, alpha, omega);
+            x[c + u * stride] = o;
+        }
+    }
+    for (; c < n2; c += stride) {
+        const double2 vx = x[c], vp = ph[c], vr = rh[c];
+        double2 o;
+        o.x = upd_x(vx.x, vp.x, vr.x, alpha, omega);
+        o.y = upd_x(vx.y, vp.y, vr.y, alpha, omega);
+        x[c] = o;
+    }
+}
+
+__global__ void k_xmark_conc(DevState* st) { st->x_applied = st->omega_iter; }
+
 }  // namespace stream

@@ -17,7 +17,9 @@ struct DevState {
     int32_t done;         // DONE_*
     int32_t fixed_iters;  // > 0: run exactly this many
     int32_t max_iter;
-    int32_t x_applied;    // deferred-x mode: last iteration whose x update is in x
+    int32_t x_applied;    // deferred-x modes: last iteration whose x update is in x
+    int32_t omega_iter;   // last iteration that reached its ω (x update due)
+    double xa, xw;        // α, ω of iteration omega_iter (for the concurrent x update)
     double scratch[8];    // results of stand-alone dot calls
 };
 
@@ -74,6 +76,9 @@ __device__ __forceinline__ void stage_update(DevState* st, int stage, const doub
         sc[2] = v[0];
         sc[3] = v[1];
         sc[4] = st->omega;
+        st->xa = st->alpha;
+        st->xw = st->omega;
+        st->omega_iter = i;
         break;
     }
     case STAGE_RHO: {
