@@ -88,7 +88,7 @@ typedef enum {
                                /* 7 = TMA warp-row 24 warps (default; k <= 4)            */
     BCGS_OPT_DEFER_X = 5,      /* 1 = apply x += αp̂ + ωr̂ inside the next p-kernel (off)    */
     BCGS_OPT_STENCIL_CFG = 6,  /* stencil+dot launch configuration 0..4 (tuning)          */
-    BCGS_OPT_XCONC = 7         /* 1 = x update on a concurrent low-priority stream (default)*/
+    BCGS_OPT_XCONC = 7         /* 1 = x update on a concurrent low-priority stream (off)  */
 } bcgs_option;
 
 typedef struct {

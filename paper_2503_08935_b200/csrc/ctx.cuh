@@ -133,7 +133,7 @@ struct bcgs_ctx_s {
     int defer_x = 0;                  // fused path: a11 applied inside the next p-kernel
     int defer_x_opt = 0;
     int stencil_cfg = 0;              // BCGS_OPT_STENCIL_CFG (k_stream.cuh launch configs)
-    int xconc_opt = 1;                // BCGS_OPT_XCONC: x update on a concurrent stream
+    int xconc_opt = 0;                // BCGS_OPT_XCONC: x update on a concurrent stream (off)
     int xconc = 0;                    // active for the current solve
     int it_host = 0;                  // iterations enqueued since begin (host parity)
     cudaStream_t s_x = nullptr;       // low-priority stream of the concurrent x update

@@ -285,3 +285,19 @@ def test_tb_variants_bitwise(bc, orc, variant, k):
     out = host(s.apply_preconditioner(dev(q)))
     ivl, _, _ = bc.chebyshev_constants(n3, h, 2, "gnocomm", k)
     assert np.array_equal(out, orc.apply_cheb(q, h, 2, k, ivl[0], ivl[1]))
+
+
+@pytest.mark.parametrize("n,pc,k,bpr", [(64, "gnocomm", 4, 1), (48, "bj", 3, 2)])
+def test_concurrent_x_update_parity(bc, orc, n, pc, k, bpr):
+    """BCGS_OPT_XCONC: a11 on a concurrent stream (p̂ double-buffered) -- bitwise oracle x."""
+    n3 = (n,) * 3
+    h = si.unit_cube_h(n)
+    s = bc.Solver(n3, h)
+    s.set_option(bc.OPT_XCONC, 1)
+    s.set_preconditioner(pc, k, blocks_per_rank=bpr)
+    s.set_rhs_random(si.SEED)
+    rep = s.solve(tol=1e-8)
+    b = orc.rhs_random(n3[::-1], si.SEED)
+    o = orc.bicgstab(b, h, pc=pc, k=k, nslab=bpr, tol=1e-8)
+    assert rep["iterations"] == o.iterations
+    assert np.array_equal(host(s.solution()), o.x)
