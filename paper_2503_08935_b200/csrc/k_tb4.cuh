@@ -73,7 +73,7 @@ struct Tb4Shape {
     static constexpr size_t xupd_bytes = sizeof(double) * 2 * 3 * NW * 32 * RY;
 };
 
-template <int K, int RY, int NW, int NS, int MODE, bool XUPD = false>
+template <int K, int RY, int NW, int NS, int MODE, bool XUPD = false, bool XSH = false>
 struct Tb4Thread {
     using S = Tb4Shape<K, RY, NW, NS>;
     static constexpr int EX = S::EX, TX = S::TX, TY = S::TY, PLANE = S::PLANE, QW = S::QW,
@@ -197,7 +197,10 @@ struct Tb4Thread {
                         yc_p = r < RY - 1 ? win[j - 1][(PH + 2) % 3][r < RY - 1 ? r + 1 : 0]
                                           : pl[(r + 1) * EX];
                     }
-                    const double xm = pl[r * EX - 1], xp = pl[r * EX + 1];
+                    // x-neighbours: from the neighbouring lanes' registers (XSH; the warp is one
+                    // extended row segment and the x-halo lanes are never active) or smem
+                    const double xm = XSH ? __shfl_up_sync(0xffffffffu, zc, 1) : pl[r * EX - 1];
+                    const double xp = XSH ? __shfl_down_sync(0xffffffffu, zc, 1) : pl[r * EX + 1];
                     const double Sv = stencil_row(zc, xm, xp, yc_m, yc_p, zm, zp, a->h2inv);
                     const double qc = qw[(PH + QW - j) % QW][r];
                     double vv;
@@ -294,11 +297,12 @@ struct Tb4Thread {
     }
 };
 
-template <int K, int RY, int NW, int NS, int MODE, int MINB = 1, bool XUPD = false>
+template <int K, int RY, int NW, int NS, int MODE, int MINB = 1, bool XUPD = false,
+          bool XSH = false>
 __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constant__ TbArgs a,
                                                        const __grid_constant__ TbMaps maps)
 {
-    using T = Tb4Thread<K, RY, NW, NS, MODE, XUPD>;
+    using T = Tb4Thread<K, RY, NW, NS, MODE, XUPD, XSH>;
     using S = Tb4Shape<K, RY, NW, NS>;
     constexpr int TX = S::TX, TY = S::TY, U = S::QW;
     extern __shared__ __align__(128) double smraw[];

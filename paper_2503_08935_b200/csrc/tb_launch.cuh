@@ -92,13 +92,14 @@ inline bool make_maps(bcgs_ctx c, TbMaps* maps, const TbArgs& a, int mode, int b
     return ok;
 }
 
-template <int K, int RY, int NW, int NS, int MODE, int MINB = 1, bool XUPD = false>
+template <int K, int RY, int NW, int NS, int MODE, int MINB = 1, bool XUPD = false,
+          bool XSH = false>
 bcgs_status launch_tb4_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
 {
     using S = Tb4Shape<K, RY, NW, NS>;
     constexpr size_t smem = S::smem + (XUPD ? S::xupd_bytes : 0);
     static_assert(smem <= 227 * 1024, "tb4 shared memory budget");
-    auto kern = k_cheb_tb4<K, RY, NW, NS, MODE, MINB, XUPD>;
+    auto kern = k_cheb_tb4<K, RY, NW, NS, MODE, MINB, XUPD, XSH>;
     static bool attr = false;
     if (!attr) {
         CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -124,6 +125,8 @@ bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz)
         if (c->tb_variant == 5 && tma_ok(c)) return launch_tb4_k<K, 2, 16, 4, MODE>(c, a, nz);
         if constexpr (K <= 4) {
             if (c->tb_variant == 7 && tma_ok(c)) return launch_tb4_k<K, 2, 24, 3, MODE>(c, a, nz);
+            if (c->tb_variant == 6 && tma_ok(c))   // x-neighbours by warp shuffle
+                return launch_tb4_k<K, 2, 24, 3, MODE, 1, false, true>(c, a, nz);
         }
     }
     return launch_tb_k<K, MODE>(c, a, nz);
