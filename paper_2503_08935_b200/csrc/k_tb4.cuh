@@ -223,6 +223,7 @@ struct Tb4Thread {
         double* cur = sm + S::PAD + (t & 1) * (K * PLANE) + ey0 * EX + lane;
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
+            if (XSH && r > 0 && r < RY - 1) continue;   // shuffles: only segment ends are read
             cur[r * EX] = q0[r];
 #pragma unroll
             for (int j = 1; j < K; ++j) cur[j * PLANE + r * EX] = win[j][PH % 3][r];

@@ -123,12 +123,12 @@ bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz)
         if (MODE == MODE_P && c->defer_x)   // deferred a11 fused into the p-kernel (16 warps)
             return launch_tb4_k<K, 2, 16, (K <= 4 ? 4 : 3), MODE, 1, true>(c, a, nz);
         if (c->tb_variant == 5 && tma_ok(c)) return launch_tb4_k<K, 2, 16, 4, MODE>(c, a, nz);
-        if (c->tb_variant == 4 && tma_ok(c))   // 16 warps, x-neighbours by warp shuffle
-            return launch_tb4_k<K, 2, 16, 4, MODE, 1, false, true>(c, a, nz);
+        if constexpr (K <= 4) {
+            if (c->tb_variant == 4 && tma_ok(c))   // 12 warps x RY = 4, shuffle x-neighbours
+                return launch_tb4_k<K, 4, 12, 3, MODE, 1, false, true>(c, a, nz);
+        }
         if constexpr (K <= 4) {
             if (c->tb_variant == 7 && tma_ok(c)) return launch_tb4_k<K, 2, 24, 3, MODE>(c, a, nz);
-            if (c->tb_variant == 6 && tma_ok(c))   // x-neighbours by warp shuffle
-                return launch_tb4_k<K, 2, 24, 3, MODE, 1, false, true>(c, a, nz);
         }
     }
     return launch_tb_k<K, MODE>(c, a, nz);
