@@ -41,7 +41,7 @@ void variant_tile(int variant, int k, int* tx, int* ty)
     if (variant == 2 || k > 5) {
         *tx = 32; *ty = 16;
         if (k >= 7) { *tx = 16; *ty = 8; } else if (k >= 5) { *tx = 32; *ty = 8; }
-    } else if ((variant == 7 || variant == 4) && k <= 4) {
+    } else if (variant == 7 && k <= 4) {
         *tx = 32 - 2 * hx; *ty = 48 - 2 * k;               // 24 warps x RY = 2
     } else {
         *tx = 32 - 2 * hx; *ty = 32 - 2 * k;               // 16 warps x RY = 2 (variant 5)

@@ -124,10 +124,6 @@ bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz)
             return launch_tb4_k<K, 2, 16, (K <= 4 ? 4 : 3), MODE, 1, true>(c, a, nz);
         if (c->tb_variant == 5 && tma_ok(c)) return launch_tb4_k<K, 2, 16, 4, MODE>(c, a, nz);
         if constexpr (K <= 4) {
-            if (c->tb_variant == 4 && tma_ok(c))   // 12 warps x RY = 4, shuffle x-neighbours
-                return launch_tb4_k<K, 4, 12, 3, MODE, 1, false, true>(c, a, nz);
-        }
-        if constexpr (K <= 4) {
             if (c->tb_variant == 7 && tma_ok(c)) return launch_tb4_k<K, 2, 24, 3, MODE>(c, a, nz);
         }
     }
