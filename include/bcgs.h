@@ -69,8 +69,12 @@ typedef enum {
     BCGS_PC_NONE = 0,          /* M = I: plain Bi-CGSTAB (Alg. 1)               */
     BCGS_PC_CHEB_GNOCOMM = 1,  /* GNoComm(CI): Chebyshev on each slab block with   */
                                /* the global Eq. 9-11 bounds rescaled by (c_min, c_max)    */
-    BCGS_PC_CHEB_BJ = 2        /* BJ(CI): Chebyshev on each slab block with the    */
+    BCGS_PC_CHEB_BJ = 2,       /* BJ(CI): Chebyshev on each slab block with the    */
                                /* exact local-block bounds (R10)                           */
+    BCGS_PC_CHEB_G = 3         /* G(CI): Chebyshev on the GLOBAL operator with */
+                               /* the rescaled global bounds; multi-rank: one k-deep halo  */
+                               /* exchange per application instead of Alg. 4's per-sweep   */
+                               /* MPI2 (requires k <= L); blocks_per_rank is ignored       */
 } bcgs_pc;
 
 typedef enum { BCGS_MEM_DEVICE = 0, BCGS_MEM_HOST = 1 } bcgs_mem;

@@ -163,7 +163,7 @@ def apply_cheb(q: np.ndarray, h: float, nslab: int, k: int, a: float, b: float) 
     return out
 
 
-PC = {"none": 0, "gnocomm": 1, "bj": 2}
+PC = {"none": 0, "gnocomm": 1, "bj": 2, "g": 3}
 STATUS = {0: "ok", 1: "config", 6: "not_converged", 7: "breakdown"}
 
 

@@ -295,7 +295,7 @@ int orc_apply_cheb(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, 
 /* ------------------------------------------------------------------------------------------
  * Preconditioned Bi-CGSTAB, Alg. 3, Alg. 1 for the scalar forms.
  *
- * pc: 0 = none (M = I), 1 = GNoComm(CI), 2 = BJ(CI).
+ * pc: 0 = none (M = I), 1 = GNoComm(CI), 2 = BJ(CI), 3 = G(CI).
  * nslab = number of z-slabs of the decomposition (ranks x blocks per rank): the
  * preconditioner acts on each slab separately (Eq. 13); the global stencils of
  * KernelBiCGS1/3 ignore the cuts (halo exchange MPI1/MPI3).
@@ -322,10 +322,13 @@ int orc_bicgstab(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, in
     int64_t n = nx * ny * nz, pl = nx * ny;
     if (nslab < 1 || nz % nslab != 0) return 1;
     double a_iv = 0.0, b_iv = 0.0;
-    if (pc == 1 || pc == 2) {
+    /* pc 3 = G(CI): Chebyshev on the global operator (no slab cuts) with the
+     * global rescaled bounds -- the preconditioner is independent of the decomposition. */
+    const int64_t nslab_pc = (pc == 3) ? 1 : nslab;
+    if (pc == 1 || pc == 2 || pc == 3) {
         if (lmin_ov > 0.0 && lmax_ov > 0.0) {
             a_iv = lmin_ov; b_iv = lmax_ov;
-        } else if (pc == 1) {
+        } else if (pc == 1 || pc == 3) {
             double lmn, lmx;
             orc_bounds(nx, ny, nz, h, &lmn, &lmx);
             a_iv = c_min * lmn;
@@ -380,7 +383,7 @@ int orc_bicgstab(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, in
         double* sc = scal ? scal + 8 * (i - 1) : NULL;
         /* line 6: solve M p̂ = p */
         if (pc == 0) memcpy(ph, p, sizeof(double) * (size_t)n);
-        else orc_apply_cheb(nx, ny, nz, h, nslab, k, a_iv, b_iv, p, ph);
+        else orc_apply_cheb(nx, ny, nz, h, nslab_pc, k, a_iv, b_iv, p, ph);
         /* MPI1 + KernelBiCGS1: w = A p̂ (global), local r~ᵀw; MPI2 */
         orc_apply_A(nx, ny, nz, h, 1, ph, w);
         double rw = orc_dot(pl, nz, rt, w);
@@ -393,7 +396,7 @@ int orc_bicgstab(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, in
         for (int64_t c = 0; c < n; ++c) r[c] = fma(-alpha, w[c], r[c]);
         /* solve M r̂ = r */
         if (pc == 0) memcpy(rh, r, sizeof(double) * (size_t)n);
-        else orc_apply_cheb(nx, ny, nz, h, nslab, k, a_iv, b_iv, r, rh);
+        else orc_apply_cheb(nx, ny, nz, h, nslab_pc, k, a_iv, b_iv, r, rh);
         /* MPI3 + KernelBiCGS3: t = A r̂, tᵀr, tᵀt; MPI4 */
         orc_apply_A(nx, ny, nz, h, 1, rh, t);
         double ts = orc_dot(pl, nz, t, r);

@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_PKG, "lib", "libbcgs.so")
 OK, E_INVALID, E_CONFIG, E_SPECTRUM, E_CUDA, E_NCCL, NOT_CONVERGED, BREAKDOWN, E_STATE = range(9)
 STATUS_NAMES = {0: "ok", 1: "invalid", 2: "config", 3: "spectrum", 4: "cuda", 5: "nccl",
                 6: "not_converged", 7: "breakdown", 8: "state"}
-PC = {"none": 0, "gnocomm": 1, "bj": 2}
+PC = {"none": 0, "gnocomm": 1, "bj": 2, "g": 3}
 MEM_DEVICE, MEM_HOST = 0, 1
 OPT_KERNELS, OPT_GRAPH, OPT_PROFILE, OPT_POLL, OPT_TB_VARIANT, OPT_DEFER_X = 0, 1, 2, 3, 4, 5
 OPT_STENCIL_CFG, OPT_XCONC = 6, 7

@@ -106,7 +106,7 @@ bcgs_status cheb_constants(const bcgs_grid_desc* g, int32_t nslab, bcgs_pc pc, i
     if (ov_a > 0.0 || ov_b > 0.0) {
         a = ov_a;
         b = ov_b;
-    } else if (pc == BCGS_PC_CHEB_GNOCOMM) {
+    } else if (pc == BCGS_PC_CHEB_GNOCOMM || pc == BCGS_PC_CHEB_G) {
         double lo, hi;
         bounds_box(g->n[0], g->n[1], g->n[2], g->h, &lo, &hi);
         a = c_min * lo;
@@ -241,10 +241,93 @@ bcgs_status reduce(bcgs_ctx c, int nparts, int stage)
 
 // ------------------------------------------------------------------ preconditioner (ref)
 // Alg. 4 with one sweep per launch; out = M^-1 q on every block.
+// G(CI) on P > 1 ranks: exact global Chebyshev polynomial.  Instead of Alg. 4's
+// halo exchange before every sweep (MPI2), exchange k planes of the input once
+// (communication-avoiding); sweep j is then exact on the extended slab minus
+// j planes per side, so after k sweeps the rank's own L planes are exact.
+bcgs_status halo_deep(bcgs_ctx c, const double* q, double* E, int k)
+{
+    const size_t pl = (size_t)c->lay.plane;
+    const int64_t L = c->lay.L, KG = BCGS_MAX_DEGREE;
+    Prof pf(c, KC_HALO, 0.0);
+    if (c->lg) {
+        const ptrdiff_t off = (const char*)q - c->ws;
+        TRY(local_exchange_begin(c, c->s));
+        for (int d = -1; d <= 1; d += 2) {
+            const int nb = c->rank + d;
+            if (nb < 0 || nb >= c->nranks) continue;
+            bcgs_ctx p = c->lg->ctxs[nb];
+            const double* pq = (const double*)(p->ws + off);
+            CUDA_OK(c, cudaStreamWaitEvent(c->s, p->ev_ready, 0));
+            const double* src = d < 0 ? pq + (L - k) * pl : pq;
+            double* dst = d < 0 ? E + (KG - k) * pl : E + (KG + L) * pl;
+            CUDA_OK(c, cudaMemcpyAsync(dst, src, k * pl * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, c->s));
+        }
+        return local_exchange_end(c, false, c->s);
+    }
+    NCCL_OK(c, ncclGroupStart());
+    if (c->rank > 0) {
+        NCCL_OK(c, ncclSend(q, k * pl, ncclDouble, c->rank - 1, c->comm, c->s));
+        NCCL_OK(c, ncclRecv(E + (KG - k) * pl, k * pl, ncclDouble, c->rank - 1, c->comm, c->s));
+    }
+    if (c->rank < c->nranks - 1) {
+        NCCL_OK(c, ncclSend(q + (L - k) * pl, k * pl, ncclDouble, c->rank + 1, c->comm, c->s));
+        NCCL_OK(c, ncclRecv(E + (KG + L) * pl, k * pl, ncclDouble, c->rank + 1, c->comm, c->s));
+    }
+    NCCL_OK(c, ncclGroupEnd());
+    return BCGS_OK;
+}
+
+bcgs_status precond_g(bcgs_ctx c, const double* q, double* out, const DevState* st)
+{
+    const int k = c->degree;
+    const int64_t pl = c->lay.plane, L = c->lay.L, KG = BCGS_MAX_DEGREE;
+    ref::ChebConst cc{c->cst[3], c->cst[4], c->cst[5], c->cst[6]};
+    if (k == 0) {
+        Prof pf(c, KC_PRECOND, 16.0 * npts(c));
+        ref::k_scale<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(q, out, npts(c), cc.cz, st);
+        CUDA_OK(c, cudaGetLastError());
+        return BCGS_OK;
+    }
+    double* E = c->ext[0];
+    double* A = c->ext[1];
+    double* B = c->ext[2];
+    CUDA_OK(c, cudaMemcpyAsync(E + KG * pl, q, sizeof(double) * L * pl, cudaMemcpyDeviceToDevice,
+                               c->s));
+    TRY(halo_deep(c, q, E, k));
+    const int v0 = (int)(c->rank == 0 ? KG : KG - k);
+    const int v1 = (int)(c->rank == c->nranks - 1 ? KG + L : KG + L + k);
+    const int nx = (int)c->lay.nx, ny = (int)c->lay.ny;
+    const dim3 blk(ref::BX, ref::BY);
+    auto grid = [&](int kb, int ke) {
+        return dim3((unsigned)((nx + ref::BX - 1) / ref::BX), (unsigned)((ny + ref::BY - 1) / ref::BY),
+                    (unsigned)((ke - kb + ref::ZC - 1) / ref::ZC));
+    };
+    Prof pf(c, KC_PRECOND, 16.0 * npts(c));
+    ref::k_cheb_sweep_rng<<<grid(v0, v1), blk, 0, c->s>>>(E, nullptr, nullptr, A, nx, ny, v0, v1,
+                                                          v0, v1, c->h2inv, cc, 0.0, 0.0, 1, st);
+    double* xm1 = A;
+    double* xm2 = nullptr;
+    for (int j = 2; j <= k; ++j) {
+        double* dst = xm2 ? xm2 : B;
+        ref::k_cheb_sweep_rng<<<grid(v0, v1), blk, 0, c->s>>>(E, xm1, xm2, dst, nx, ny, v0, v1, v0,
+                                                              v1, c->h2inv, cc, c->rho[j],
+                                                              c->rho[j - 1], 0, st);
+        xm2 = xm1;
+        xm1 = dst;
+    }
+    CUDA_OK(c, cudaMemcpyAsync(out, xm1 + KG * pl, sizeof(double) * L * pl,
+                               cudaMemcpyDeviceToDevice, c->s));
+    CUDA_OK(c, cudaGetLastError());
+    return BCGS_OK;
+}
+
 bcgs_status precond_ref(bcgs_ctx c, const double* q, double* out, const DevState* st)
 {
     const int64_t n = npts(c);
     const int k = c->degree;
+    if (c->pc == BCGS_PC_CHEB_G && c->nranks > 1) return precond_g(c, q, out, st);
     if (c->pc == BCGS_PC_NONE) {
         Prof pf(c, KC_PRECOND, 16.0 * n);
         ref::k_copy<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(q, out, n, st);
@@ -343,6 +426,7 @@ bcgs_status iteration_ref(bcgs_ctx c)
 
 bcgs_status iteration(bcgs_ctx c)
 {
+    if (c->pc == BCGS_PC_CHEB_G && c->nranks > 1) return iteration_ref(c);   // k-deep halos
     if (c->kernels == 1 && fused::supported(c->lay.nx, c->lay.ny, c->lay.L, c->bpr, c->degree,
                                             c->pc != BCGS_PC_NONE))
         return fused::iteration(c);
@@ -474,7 +558,8 @@ bcgs_status bcgs_chebyshev_constants(const bcgs_grid_desc* grid, int32_t nslab, 
 {
     if (!grid || nslab < 1 || grid->n[2] % nslab || !interval2 || !out7 || !rho)
         return BCGS_E_INVALID;
-    if (pc != BCGS_PC_CHEB_GNOCOMM && pc != BCGS_PC_CHEB_BJ) return BCGS_E_INVALID;
+    if (pc != BCGS_PC_CHEB_GNOCOMM && pc != BCGS_PC_CHEB_BJ && pc != BCGS_PC_CHEB_G)
+        return BCGS_E_INVALID;
     return cheb_constants(grid, nslab, pc, degree, c_min, c_max, 0.0, 0.0, interval2, out7, rho);
 }
 
@@ -532,6 +617,8 @@ static bcgs_status create_ctx(const bcgs_grid_desc* grid, int32_t rank, int32_t 
     }
     for (int v = 0; v < V_COUNT; ++v)
         c->vec[v] = (double*)(c->ws + lay.off_vec[v]) + lay.plane;
+    for (int e = 0; e < 3; ++e)
+        c->ext[e] = lay.ext_elems ? (double*)(c->ws + lay.off_ext[e]) + lay.plane : nullptr;
     c->st = (DevState*)(c->ws + lay.off_state);
     c->hist = (double*)(c->ws + lay.off_hist);
     c->scal = (double*)(c->ws + lay.off_scal);
@@ -674,13 +761,20 @@ bcgs_status bcgs_set_preconditioner(bcgs_ctx c, bcgs_pc pc, int32_t degree, doub
                                     double c_max, int32_t blocks_per_rank)
 {
     if (!c) return BCGS_E_INVALID;
-    if (pc != BCGS_PC_NONE && pc != BCGS_PC_CHEB_GNOCOMM && pc != BCGS_PC_CHEB_BJ)
+    if (pc != BCGS_PC_NONE && pc != BCGS_PC_CHEB_GNOCOMM && pc != BCGS_PC_CHEB_BJ &&
+        pc != BCGS_PC_CHEB_G)
         return fail(c, BCGS_E_INVALID, "unknown preconditioner %d", (int)pc);
     if (degree < 0 || degree > BCGS_MAX_DEGREE)
         return fail(c, BCGS_E_INVALID, "degree %d outside [0, %d]", degree, BCGS_MAX_DEGREE);
     if (blocks_per_rank < 1 || c->lay.L % blocks_per_rank)
         return fail(c, BCGS_E_CONFIG, "slab of %lld planes not divisible into %d blocks (axis z)",
                     (long long)c->lay.L, blocks_per_rank);
+    if (pc == BCGS_PC_CHEB_G) {
+        blocks_per_rank = 1;   // the global operator has no block cuts
+        if (c->nranks > 1 && degree > c->lay.L)
+            return fail(c, BCGS_E_CONFIG, "G(CI) needs degree %d <= slab thickness %lld",
+                        degree, (long long)c->lay.L);
+    }
     c->pc = pc;
     c->degree = degree;
     c->c_min = c_min;
@@ -895,7 +989,8 @@ bcgs_status bcgs_apply_preconditioner(bcgs_ctx c, const double* d_in, double* d_
     double* io = F(c, V_IO);
     CUDA_OK(c, cudaMemcpyAsync(io, d_in, bytes, cudaMemcpyDeviceToDevice, c->s));
     double* o = F(c, V_W2);
-    if (c->kernels == 1 && fused::precond_supported(c))
+    if (c->kernels == 1 && fused::precond_supported(c) &&
+        !(c->pc == BCGS_PC_CHEB_G && c->nranks > 1))
         TRY(fused::precond_apply(c, io, o));
     else
         TRY(precond_ref(c, io, o, nullptr));

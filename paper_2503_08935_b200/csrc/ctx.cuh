@@ -42,6 +42,8 @@ struct Layout {
     int64_t nx, ny, nz, L, plane, vec_elems;   // vec_elems = (L + 2) * plane
     int64_t n_part;
     size_t off_vec[17];
+    int64_t ext_elems;
+    size_t off_ext[3];
     size_t off_state, off_hist, off_scal, off_part, off_rank, off_gath, total;
 };
 
@@ -71,6 +73,12 @@ inline bool make_layout(const bcgs_grid_desc* g, int32_t nranks, Layout* lay)
     for (int v = 0; v < V_COUNT; ++v) {
         lay->off_vec[v] = off;
         off = align_up(off + sizeof(double) * (size_t)lay->vec_elems);
+    }
+    // G(CI) with nranks > 1: three extended fields of L + 2*KG planes (k-deep halos)
+    lay->ext_elems = nranks > 1 ? (lay->L + 2 * (int64_t)BCGS_MAX_DEGREE + 2) * lay->plane : 0;
+    for (int e = 0; e < 3; ++e) {
+        lay->off_ext[e] = off;
+        off = align_up(off + sizeof(double) * (size_t)lay->ext_elems);
     }
     lay->off_state = off; off = align_up(off + sizeof(DevState));
     lay->off_hist = off;  off = align_up(off + sizeof(double) * (BCGS_HIST_CAP + 1));
@@ -125,6 +133,7 @@ struct bcgs_ctx_s {
     ncclComm_t comm = nullptr;
     char* ws = nullptr;
     double* vec[V_COUNT] = {};     // interior plane 0 of each field
+    double* ext[3] = {};           // G(CI) extended fields: extended plane 0 (= global z0 - KG)
     DevState* st = nullptr;
     double *hist = nullptr, *scal = nullptr;
     dd *part = nullptr, *rank_out = nullptr, *gath = nullptr;

@@ -112,7 +112,8 @@ bcgs_status precond_apply(bcgs_ctx c, const double* q, double* out)
 void on_begin(bcgs_ctx c)
 {
     c->it_host = 0;
-    c->xconc = (c->xconc_opt && c->kernels == 1 && c->pc != BCGS_PC_NONE &&
+    const bool g_multi = c->pc == BCGS_PC_CHEB_G && c->nranks > 1;   // ref path (k-deep halos)
+    c->xconc = (c->xconc_opt && !g_multi && c->kernels == 1 && c->pc != BCGS_PC_NONE &&
                 (c->lay.nx % 2) == 0 && !c->defer_x_opt &&
                 supported(c->lay.nx, c->lay.ny, c->lay.L, c->bpr, c->degree, true)) ? 1 : 0;
     if (c->xconc) {   // s_x starts after the setup (x = x0 written on s)
@@ -120,7 +121,7 @@ void on_begin(bcgs_ctx c)
         cudaStreamWaitEvent(c->s_x, c->ev_omega, 0);
         cudaEventRecord(c->ev_xdone, c->s_x);
     }
-    c->defer_x = (c->defer_x_opt && c->kernels == 1 && c->pc != BCGS_PC_NONE &&
+    c->defer_x = (c->defer_x_opt && !g_multi && c->kernels == 1 && c->pc != BCGS_PC_NONE &&
                   (c->lay.nx % 2) == 0 &&
                   defer_x_ok(c)) ? 1 : 0;
 }

@@ -141,6 +141,41 @@ __global__ void __launch_bounds__(BX * BY) k_cheb_sweep(const double* __restrict
     }
 }
 
+// G(CI) on an extended slab (k-deep halo planes present): one Chebyshev sweep over planes
+// [kb, ke) of the GLOBAL operator; planes outside [v0, v1) are the physical Dirichlet
+// ghosts (zero).  Same per-point expressions as k_cheb_sweep.
+__global__ void __launch_bounds__(BX * BY) k_cheb_sweep_rng(const double* __restrict__ q,
+                                                            const double* __restrict__ x1,
+                                                            const double* x2, double* out, int nx,
+                                                            int ny, int kb, int ke, int v0, int v1,
+                                                            double h2inv, ChebConst cc,
+                                                            double rho_j, double rho_jm1,
+                                                            int first,
+                                                            const DevState* __restrict__ st)
+{
+    if (st && st->done) return;
+    const int i = blockIdx.x * BX + threadIdx.x, j = blockIdx.y * BY + threadIdx.y;
+    const int k0 = kb + blockIdx.z * ZC, k1 = min(ke, k0 + ZC);
+    if (i >= nx || j >= ny) return;
+    const int64_t plane = (int64_t)nx * ny;
+    const double* v = first ? q : x1;
+    int64_t c = i + (int64_t)nx * j + plane * k0;
+    for (int k = k0; k < k1; ++k, c += plane) {
+        const double zm = (k - 1 < v0) ? 0.0 : v[c - plane];
+        const double zp = (k + 1 >= v1) ? 0.0 : v[c + plane];
+        const double S = stencil_at(v, c, i, j, nx, ny, zm, zp, h2inv);
+        const double qc = q[c];
+        double o;
+        if (first) {
+            o = cheb_first(qc, S, cc.g1, cc.cz);
+        } else {
+            const double zc = x2 ? x2[c] : qc * cc.cz;
+            o = cheb_step(qc, S, v[c], zc, rho_j, rho_jm1, cc.A2, cc.B2);
+        }
+        out[c] = o;
+    }
+}
+
 // ------------------------------------------------------------------- element-wise ops
 #define EW_LOOP(n) \
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < (n); \

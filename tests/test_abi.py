@@ -45,13 +45,14 @@ def test_workspace_bytes_and_config_errors():
 
 @pytest.mark.parametrize("n,nslab,pc,k", [(32, 1, "gnocomm", 4), (64, 4, "gnocomm", 4),
                                           (64, 4, "bj", 4), (128, 8, "bj", 7),
-                                          (512, 8, "gnocomm", 24), ((48, 40, 36), 3, "bj", 2)])
+                                          (512, 8, "gnocomm", 24), ((48, 40, 36), 3, "bj", 2),
+                                          (64, 4, "g", 4)])
 def test_chebyshev_constants_equal_oracle(orc, n, nslab, pc, k):
     """Host-side constants of the library (R9, R10, R18) are bit-identical to the oracle's."""
     n3 = (n,) * 3 if np.isscalar(n) else n
     h = 1.0 / (n3[0] + 1)
     ivl, cst, rho = bcgs.chebyshev_constants(n3, h, nslab, pc, k)
-    if pc == "gnocomm":
+    if pc in ("gnocomm", "g"):
         lo, hi = orc.bounds(n3[0], n3[1], n3[2], h)
         a, b = 10.0 * lo, (1.0 - 1e-4) * hi
     else:
