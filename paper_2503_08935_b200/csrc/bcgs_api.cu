@@ -298,6 +298,10 @@ bcgs_status precond_g(bcgs_ctx c, const double* q, double* out, const DevState* 
     TRY(halo_deep(c, q, E, k));
     const int v0 = (int)(c->rank == 0 ? KG : KG - k);
     const int v1 = (int)(c->rank == c->nranks - 1 ? KG + L : KG + L + k);
+    if (c->kernels == 1 && k <= fused::KMAX_TB) {   // all k sweeps in one HBM pass
+        Prof pf(c, KC_PRECOND, 16.0 * npts(c));
+        return fused::precond_g_tb(c, E, out, v0, v1);
+    }
     const int nx = (int)c->lay.nx, ny = (int)c->lay.ny;
     const dim3 blk(ref::BX, ref::BY);
     auto grid = [&](int kb, int ke) {

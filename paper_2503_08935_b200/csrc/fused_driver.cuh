@@ -66,7 +66,9 @@ bcgs_status launch_tb(bcgs_ctx c, TbArgs& a)
     // waves * (planes per chunk + 2k).
     int tx, ty;
     variant_tile((MODE == MODE_P && c->defer_x) ? 5 : c->tb_variant, k, &tx, &ty);
-    const int64_t tiles = ((a.nx + tx - 1) / tx) * (int64_t)((a.ny + ty - 1) / ty) * c->bpr;
+    if (a.ext) a.Lb = a.zo1 - a.zo0;   // chunks over the output planes, one "block"
+    const int nblk = a.ext ? 1 : c->bpr;
+    const int64_t tiles = ((a.nx + tx - 1) / tx) * (int64_t)((a.ny + ty - 1) / ty) * nblk;
     int64_t best_n = 1;
     double best = 1e300;
     for (int64_t nch = 1; nch <= std::max<int64_t>(1, a.Lb / 8); ++nch) {
@@ -80,7 +82,7 @@ bcgs_status launch_tb(bcgs_ctx c, TbArgs& a)
     }
     a.zch = (int)((a.Lb + best_n - 1) / best_n);
     a.nchunk = (a.Lb + a.zch - 1) / a.zch;
-    const int nz = a.nchunk * c->bpr;
+    const int nz = a.nchunk * nblk;
     switch (k) {
     case 1: return launch_variant<1, MODE>(c, a, nz);
     case 2: return launch_variant<2, MODE>(c, a, nz);
@@ -92,6 +94,23 @@ bcgs_status launch_tb(bcgs_ctx c, TbArgs& a)
     case 8: return launch_variant<8, MODE>(c, a, nz);
     }
     return fail(c, BCGS_E_INVALID, "temporal blocking supports degree 1..%d", KMAX_TB);
+}
+
+// G(CI) on P > 1 ranks through the temporally blocked kernel: input = the extended slab
+// (k-deep halos already exchanged), zero ghosts outside [v0, v1), outputs planes [KG, KG+L).
+bcgs_status precond_g_tb(bcgs_ctx c, const double* E, double* out, int v0, int v1)
+{
+    TbArgs a{};
+    const int64_t KG = BCGS_MAX_DEGREE;
+    a.q = E;
+    a.out = out - KG * c->lay.plane;
+    a.st = nullptr;
+    a.ext = 1;
+    a.zv0 = v0;
+    a.zv1 = v1;
+    a.zo0 = (int)KG;
+    a.zo1 = (int)(KG + c->lay.L);
+    return launch_tb<MODE_PLAIN>(c, a);
 }
 
 bool precond_supported(bcgs_ctx c)

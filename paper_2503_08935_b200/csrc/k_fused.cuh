@@ -36,6 +36,9 @@ struct TbArgs {
     double* x;            // MODE_P + XUPD: x_{i-1} += α p̂_{i-1} + ω r̂_{i-1} (deferred a11)
     const double* rh;     //   r̂ of the previous iteration
     int nx, ny, Lb, zch, nchunk;
+    // extended-slab mode (G(CI), ext = 1): zero ghosts outside planes [zv0, zv1), outputs
+    // for planes [zo0, zo1) only, one block; plane indices are extended-slab indices.
+    int ext, zv0, zv1, zo0, zo1;
     double h2inv, cz, g1, A2, B2;
     double rho[KMAX_TB + 1];
     const DevState* st;
@@ -191,11 +194,11 @@ __global__ void __launch_bounds__(TbShape<K, TX, TY>::NT, 1) k_cheb_tb(TbArgs a)
         if (th.in_dom && dist <= K - j) th.actmask |= 1u << j;
 
     const int blk = blockIdx.z / a.nchunk, ch = blockIdx.z % a.nchunk;
-    th.b0 = blk * a.Lb;
-    th.b1 = th.b0 + a.Lb;
-    th.c0 = th.b0 + ch * a.zch;
-    th.c1 = min(th.b1, th.c0 + a.zch);
-    if (th.c0 >= th.b1) return;
+    th.b0 = a.ext ? a.zv0 : blk * a.Lb;
+    th.b1 = a.ext ? a.zv1 : th.b0 + a.Lb;
+    th.c0 = (a.ext ? a.zo0 : th.b0) + ch * a.zch;
+    th.c1 = min(a.ext ? a.zo1 : th.b1, th.c0 + a.zch);
+    if (th.c0 >= (a.ext ? a.zo1 : th.b1)) return;
     const int t0 = max(th.b0, th.c0 - K), t1 = th.c1 - 1 + K;
     th.plane = (int64_t)a.nx * a.ny;
     th.col = th.in_dom ? gx + (int64_t)a.nx * gy : 0;
@@ -257,5 +260,6 @@ bcgs_status iteration(bcgs_ctx c);
 void on_begin(bcgs_ctx c);
 bool precond_supported(bcgs_ctx c);
 bcgs_status precond_apply(bcgs_ctx c, const double* q, double* out);
+bcgs_status precond_g_tb(bcgs_ctx c, const double* E, double* out, int v0, int v1);
 
 }  // namespace fused

@@ -364,11 +364,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constan
     }
     th.wdy = wdy;
     const int blk = blockIdx.z / a.nchunk, ch = blockIdx.z % a.nchunk;
-    th.b0 = blk * a.Lb;
-    th.b1 = th.b0 + a.Lb;
-    th.c0 = th.b0 + ch * a.zch;
-    th.c1 = min(th.b1, th.c0 + a.zch);
-    if (th.c0 >= th.b1) return;
+    th.b0 = a.ext ? a.zv0 : blk * a.Lb;
+    th.b1 = a.ext ? a.zv1 : th.b0 + a.Lb;
+    th.c0 = (a.ext ? a.zo0 : th.b0) + ch * a.zch;
+    th.c1 = min(a.ext ? a.zo1 : th.b1, th.c0 + a.zch);
+    if (th.c0 >= (a.ext ? a.zo1 : th.b1)) return;
     th.t0 = max(th.b0, th.c0 - K);
     th.t1 = th.c1 - 1 + K;
     th.plane = (int64_t)a.nx * a.ny;

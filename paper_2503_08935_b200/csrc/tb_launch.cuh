@@ -82,7 +82,8 @@ inline bool make_maps(bcgs_ctx c, TbMaps* maps, const TbArgs& a, int mode, int b
                       int box_x = 32)
 {
     memset(maps, 0, sizeof *maps);
-    const int64_t nx = c->lay.nx, ny = c->lay.ny, L = c->lay.L;
+    const int64_t nx = c->lay.nx, ny = c->lay.ny;
+    const int64_t L = a.ext ? c->lay.L + 2 * (int64_t)BCGS_MAX_DEGREE : c->lay.L;
     if (mode == MODE_PLAIN) return make_map(&maps->q, a.q, nx, ny, L, box_y, box_x);
     bool ok = make_map(&maps->r, a.r, nx, ny, L, box_y, box_x) &&
               make_map(&maps->w, a.w, nx, ny, L, box_y, box_x);
