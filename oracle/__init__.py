@@ -61,6 +61,21 @@ def lib() -> ctypes.CDLL:
         _lib.orc_cheb_setup.argtypes = [f64, f64, ctypes.c_int, P, P]
         _lib.orc_apply_cheb.restype = ctypes.c_int
         _lib.orc_apply_cheb.argtypes = [i64, i64, i64, f64, i64, ctypes.c_int, f64, f64, P, P]
+        _lib.orc_fold_boundary_bc.argtypes = [i64, i64, i64, f64, ctypes.c_int, P, P]
+        _lib.orc_apply_A_bc.argtypes = [i64, i64, i64, f64, i64, ctypes.c_int, P, P]
+        _lib.orc_mu_bc.restype = f64
+        _lib.orc_mu_bc.argtypes = [i64, i64, ctypes.c_int]
+        _lib.orc_bounds_bc.argtypes = [i64, i64, i64, f64, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int, P, P]
+        _lib.orc_apply_cheb_bc.restype = ctypes.c_int
+        _lib.orc_apply_cheb_bc.argtypes = [i64, i64, i64, f64, i64, ctypes.c_int, ctypes.c_int,
+                                           f64, f64, P, P]
+        _lib.orc_pc_interval.argtypes = [i64, i64, i64, f64, i64, ctypes.c_int, ctypes.c_int,
+                                         f64, f64, P]
+        _lib.orc_bicgstab_bc.restype = ctypes.c_int
+        _lib.orc_bicgstab_bc.argtypes = [i64, i64, i64, f64, i64, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_int, f64, f64, f64, f64, P, P, f64,
+                                         ctypes.c_int, ctypes.c_int, P, P, P, P, P]
         _lib.orc_bicgstab.restype = ctypes.c_int
         _lib.orc_bicgstab.argtypes = [i64, i64, i64, f64, i64, ctypes.c_int, ctypes.c_int,
                                       f64, f64, f64, f64, P, P, f64, ctypes.c_int,
@@ -95,20 +110,30 @@ def rhs_random(shape, seed: int) -> np.ndarray:
     return b
 
 
-def fold_boundary(b: np.ndarray, h: float, g6) -> np.ndarray:
+def bc_mask(bc6) -> int:
+    """Face kinds (0 Dirichlet / 1 Neumann, faces x-,x+,y-,y+,z-,z+) -> bit mask."""
+    if bc6 is None:
+        return 0
+    if isinstance(bc6, int):
+        return bc6
+    return sum((1 << f) for f, kind in enumerate(bc6) if kind)
+
+
+def fold_boundary(b: np.ndarray, h: float, g6, bc=None) -> np.ndarray:
     nx, ny, nz = _shape(b.shape)
     out = np.ascontiguousarray(b, dtype=np.float64).copy()
     g = np.ascontiguousarray(np.asarray(g6, np.float64))
-    lib().orc_fold_boundary(nx, ny, nz, h, _ptr(g), _ptr(out))
+    lib().orc_fold_boundary_bc(nx, ny, nz, h, bc_mask(bc), _ptr(g), _ptr(out))
     return out
 
 
-def apply_A(v: np.ndarray, h: float, nslab: int = 1) -> np.ndarray:
-    """Global operator (nslab=1) or block-diagonal slab operator (Eq. 6 / Eq. 12-14)."""
+def apply_A(v: np.ndarray, h: float, nslab: int = 1, bc=None) -> np.ndarray:
+    """Global operator (nslab=1) or block-diagonal slab operator (Eq. 6 / Eq. 12-14);
+    bc: Neumann faces (Eq. 5 mirror ghosts)."""
     v = np.ascontiguousarray(v, np.float64)
     nx, ny, nz = _shape(v.shape)
     out = np.empty_like(v)
-    lib().orc_apply_A(nx, ny, nz, h, nslab, _ptr(v), _ptr(out))
+    lib().orc_apply_A_bc(nx, ny, nz, h, nslab, bc_mask(bc), _ptr(v), _ptr(out))
     return out
 
 
@@ -141,6 +166,27 @@ def bounds(nx: int, ny: int, nzb: int, h: float):
     return float(lo[0]), float(hi[0])
 
 
+def mu_bc(n: int, i: int, kind: int) -> float:
+    """Eigenvalue i of the 1-D factor with `kind` Neumann ends (0: Eq. 9; 1, 2: R27)."""
+    return float(lib().orc_mu_bc(n, i, kind))
+
+
+def bounds_bc(nx: int, ny: int, nzb: int, h: float, kinds):
+    lo, hi = np.zeros(1), np.zeros(1)
+    lib().orc_bounds_bc(nx, ny, nzb, h, int(kinds[0]), int(kinds[1]), int(kinds[2]),
+                        _ptr(lo), _ptr(hi))
+    return float(lo[0]), float(hi[0])
+
+
+def pc_interval(shape, h: float, nslab: int, pc: str, c_min: float = 10.0,
+                c_max: float = 1.0 - 1e-4, bc=None):
+    """Chebyshev interval [a', b'] the oracle's Alg. 3 uses for preconditioner `pc`."""
+    nx, ny, nz = _shape(shape)
+    out = np.zeros(2)
+    lib().orc_pc_interval(nx, ny, nz, h, nslab, bc_mask(bc), PC[pc], c_min, c_max, _ptr(out))
+    return float(out[0]), float(out[1])
+
+
 def cheb_setup(a: float, b: float, k: int):
     cst = np.zeros(7)
     rho = np.zeros(max(k, 1) + 1)
@@ -153,11 +199,13 @@ def cheb_setup(a: float, b: float, k: int):
     return d
 
 
-def apply_cheb(q: np.ndarray, h: float, nslab: int, k: int, a: float, b: float) -> np.ndarray:
+def apply_cheb(q: np.ndarray, h: float, nslab: int, k: int, a: float, b: float,
+               bc=None) -> np.ndarray:
     q = np.ascontiguousarray(q, np.float64)
     nx, ny, nz = _shape(q.shape)
     out = np.empty_like(q)
-    rc = lib().orc_apply_cheb(nx, ny, nz, h, nslab, k, a, b, _ptr(q), _ptr(out))
+    rc = lib().orc_apply_cheb_bc(nx, ny, nz, h, nslab, bc_mask(bc), k, a, b, _ptr(q),
+                                 _ptr(out))
     if rc:
         raise ValueError(f"apply_cheb rc={rc}")
     return out
@@ -181,7 +229,7 @@ class Result:
 def bicgstab(b: np.ndarray, h: float, *, pc: str = "none", k: int = 4, nslab: int = 1,
              c_min: float = 10.0, c_max: float = 1.0 - 1e-4, bounds_override=None,
              x0: np.ndarray | None = None, tol: float = 1e-8, max_it: int = 5000,
-             fixed_it: int = 0) -> Result:
+             fixed_it: int = 0, bc=None) -> Result:
     """Alg. 3 (P:264-308) with M = I, GNoComm(CI) or BJ(CI) on `nslab` z-slabs."""
     b = np.ascontiguousarray(b, np.float64)
     nx, ny, nz = _shape(b.shape)
@@ -196,7 +244,8 @@ def bicgstab(b: np.ndarray, h: float, *, pc: str = "none", k: int = 4, nslab: in
     if x0 is not None:
         x0 = np.ascontiguousarray(x0, np.float64)
         x0p = _ptr(x0)
-    st = lib().orc_bicgstab(nx, ny, nz, h, nslab, PC[pc], k, c_min, c_max, lmin, lmax,
+    st = lib().orc_bicgstab_bc(nx, ny, nz, h, nslab, bc_mask(bc), PC[pc], k, c_min, c_max,
+                               lmin, lmax,
                             _ptr(b), x0p, tol, max_it, fixed_it, _ptr(x), _ptr(hist),
                             _ptr(scal), ctypes.byref(it), ctypes.byref(tr))
     n = it.value

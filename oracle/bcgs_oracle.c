@@ -17,9 +17,11 @@
  * algorithm numbers are given next to every citation.
  *
  * Layout (DESIGN.md §3 R14): unknown (i,j,k), 0-based, i fastest:  idx = i + nx*(j + ny*k).
- * The grid has nx*ny*nz unknowns strictly inside the domain; all physical boundary ghosts
- * are homogeneous Dirichlet zeros (Eq. 4); non-zero boundary data are folded into
- * the right-hand side once (orc_fold_boundary).
+ * The grid has nx*ny*nz unknowns; physical boundary ghosts are homogeneous Dirichlet zeros
+ * (Eq. 4) or, on faces flagged Neumann in the bit mask bcm (bit f = face f,
+ * 0..5 = x-,x+,y-,y+,z-,z+), mirrors of the first interior neighbour (Eq. 5;
+ * "_bc" entry points); non-zero boundary data are folded into the right-hand side once
+ * (orc_fold_boundary_bc).
  *
  * Parity status: every function below is pinned by tests/test_oracle_pins.py against values
  * that do not come from this file (dense Kronecker assembly, closed-form spectra, closed-form
@@ -69,11 +71,15 @@ void orc_rhs_random(int64_t nx, int64_t ny, int64_t nz, uint64_t seed, double* b
  * next to face f the stencil row (Eq. 3) references one ghost whose value is g_f;
  * moving it to the right-hand side adds g_f/h^2.  Faces: 0=x-,1=x+,2=y-,3=y+,4=z-,5=z+.
  * Faces are folded in face order 0..5, each as b += g*h2inv. */
-void orc_fold_boundary(int64_t nx, int64_t ny, int64_t nz, double h, const double* g6, double* b)
+void orc_fold_boundary_bc(int64_t nx, int64_t ny, int64_t nz, double h, int bcm,
+                          const double* g6, double* b)
 {
     double h2inv = 1.0 / (h * h);
     for (int f = 0; f < 6; ++f) {
-        double add = g6[f] * h2inv;
+        /* Dirichlet value g: the ghost g moves to the RHS as g/h^2.  Neumann (bit f of bcm)
+         * outward normal derivative g: the centred ghost rule ghost = mirror + 2 h g
+         * ("Set Neumann BCs") leaves 2 h g / h^2 = 2 g / h on the RHS (R28). */
+        double add = ((bcm >> f) & 1) ? (2.0 * g6[f]) / h : g6[f] * h2inv;
         if (g6[f] == 0.0) continue;
         for (int64_t k = 0; k < nz; ++k)
             for (int64_t j = 0; j < ny; ++j)
@@ -86,6 +92,11 @@ void orc_fold_boundary(int64_t nx, int64_t ny, int64_t nz, double h, const doubl
     }
 }
 
+void orc_fold_boundary(int64_t nx, int64_t ny, int64_t nz, double h, const double* g6, double* b)
+{
+    orc_fold_boundary_bc(nx, ny, nz, h, 0, g6, b);
+}
+
 /* ------------------------------------------------------------------------------------------
  * The operator.  P:95-100 (Eq. 6): P = I⊗I⊗D_x/Δx² + I⊗D_y/Δy²⊗I + D_z/Δz²⊗I⊗I with D from
  * Eq. 4.  With uniform spacing h the row for unknown c reads
@@ -95,8 +106,8 @@ void orc_fold_boundary(int64_t nx, int64_t ny, int64_t nz, double h, const doubl
  * (P:185-205): z is cut into nslab equal slabs and neighbours across a cut are also +0.0.
  * nslab == 1 is the global operator (used by KernelBiCGS1/3).
  * ---------------------------------------------------------------------------------------- */
-void orc_apply_A(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab,
-                 const double* v, double* out)
+void orc_apply_A_bc(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, int bcm,
+                    const double* v, double* out)
 {
     double h2inv = 1.0 / (h * h);
     int64_t L = nz / nslab;
@@ -108,16 +119,24 @@ void orc_apply_A(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab,
         for (int64_t j = 0; j < ny; ++j)
             for (int64_t i = 0; i < nx; ++i) {
                 int64_t c = IDX(i, j, k);
-                double xm = (i > 0) ? v[c - 1] : 0.0;
-                double xp = (i < nx - 1) ? v[c + 1] : 0.0;
-                double ym = (j > 0) ? v[c - nx] : 0.0;
-                double yp = (j < ny - 1) ? v[c + nx] : 0.0;
-                double zm = cut_lo ? 0.0 : v[c - pl];
-                double zp = cut_hi ? 0.0 : v[c + pl];
+                /* Neumann face (bit of bcm): the ghost is the mirror of the first interior
+                 * neighbour (ghost_{-1} = v_1), which gives Eq. 5's rows (2, -2) (R27). */
+                double xm = (i > 0) ? v[c - 1] : ((bcm & 1) ? v[c + 1] : 0.0);
+                double xp = (i < nx - 1) ? v[c + 1] : ((bcm & 2) ? v[c - 1] : 0.0);
+                double ym = (j > 0) ? v[c - nx] : ((bcm & 4) ? v[c + nx] : 0.0);
+                double yp = (j < ny - 1) ? v[c + nx] : ((bcm & 8) ? v[c - nx] : 0.0);
+                double zm = (k == 0 && (bcm & 16)) ? v[c + pl] : (cut_lo ? 0.0 : v[c - pl]);
+                double zp = (k == nz - 1 && (bcm & 32)) ? v[c - pl] : (cut_hi ? 0.0 : v[c + pl]);
                 double nb = ((((xm + xp) + ym) + yp) + zm) + zp;
                 out[c] = fma(6.0, v[c], -nb) * h2inv;      /* (6 v_c - nb) / h^2, R17 */
             }
     }
+}
+
+void orc_apply_A(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab,
+                 const double* v, double* out)
+{
+    orc_apply_A_bc(nx, ny, nz, h, nslab, 0, v, out);
 }
 
 /* ------------------------------------------------------------------------------------------
@@ -212,6 +231,44 @@ void orc_bounds(int64_t nx, int64_t ny, int64_t nzb, double h, double* lmin, dou
     *lmax = ((orc_mu(nx, nx) * h2inv) + (orc_mu(ny, ny) * h2inv)) + (orc_mu(nzb, nzb) * h2inv);
 }
 
+/* Mixed boundary conditions (Eq. 5; DESIGN.md §3 R27).  The paper gives no closed
+ * form for the eigenvalues of N and falls back on Gerschgorin's [0, 4], whose lower
+ * end 0 cannot be rescaled by c_min (R9).  The 1-D factor with the mirror rule on one end
+ * has the closed form 4 sin²((2i-1)π/(4n)), i = 1..n (eigenvectors cos((2i-1)π j/(2n)));
+ * with Neumann on both ends 4 sin²(iπ/(2(n-1))), i = 0..n-1 (cos(iπ j/(n-1))).  Both are
+ * pinned against dense eigen-solves of Eq. 5's matrices.  kind = number of Neumann ends. */
+double orc_mu_bc(int64_t n, int64_t i, int kind)
+{
+    double s;
+    if (kind == 0) return orc_mu(n, i);
+    if (kind == 1) s = sin(((double)(2 * i - 1) * M_PI) / (4.0 * (double)n));
+    else s = sin(((double)i * M_PI) / (2.0 * (double)(n - 1)));
+    return 4.0 * (s * s);
+}
+
+static void axis_range(int64_t n, int kind, double* mn, double* mx)
+{
+    if (kind == 2) {
+        *mn = orc_mu_bc(n, 0, 2);
+        *mx = orc_mu_bc(n, n - 1, 2);
+    } else {
+        *mn = orc_mu_bc(n, 1, kind);
+        *mx = orc_mu_bc(n, n, kind);
+    }
+}
+
+/* Eqs. 10-11 with per-axis kinds (kx, ky, kz = Neumann ends of that axis' factor). */
+void orc_bounds_bc(int64_t nx, int64_t ny, int64_t nzb, double h, int kx, int ky, int kz,
+                   double* lmin, double* lmax)
+{
+    double h2inv = 1.0 / (h * h), ax, bx, ay, by, az, bz;
+    axis_range(nx, kx, &ax, &bx);
+    axis_range(ny, ky, &ay, &by);
+    axis_range(nzb, kz, &az, &bz);
+    *lmin = ((ax * h2inv) + (ay * h2inv)) + (az * h2inv);
+    *lmax = ((bx * h2inv) + (by * h2inv)) + (bz * h2inv);
+}
+
 /* ------------------------------------------------------------------------------------------
  * Chebyshev iteration, Alg. 2 as implemented in Alg. 4.
  * Interval [a, b] (Eq. 15): θ = (b+a)/2, δ = (b-a)/2, σ = θ/δ.
@@ -252,8 +309,8 @@ int orc_cheb_setup(double a, double b, int k, double* out7, double* rho_out)
     return 0;
 }
 
-int orc_apply_cheb(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, int k,
-                   double a, double b, const double* q, double* out)
+int orc_apply_cheb_bc(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, int bcm,
+                      int k, double a, double b, const double* q, double* out)
 {
     double cst[7], rho[ORC_KMAX + 2];
     int rc = orc_cheb_setup(a, b, k, cst, rho);
@@ -271,7 +328,7 @@ int orc_apply_cheb(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, 
     double* w = (double*)malloc(sizeof(double) * (size_t)n);
 
     /* KernelCI1: z = b/θ ; y = 2(ρ_cur/δ)(2b - A b/θ) */
-    orc_apply_A(nx, ny, nz, h, nslab, q, S);
+    orc_apply_A_bc(nx, ny, nz, h, nslab, bcm, q, S);
 #pragma omp parallel for schedule(static)
     for (int64_t c = 0; c < n; ++c) {
         z[c] = q[c] * cz;
@@ -279,7 +336,7 @@ int orc_apply_cheb(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, 
     }
     /* KernelCI2 for i = 2..iterMax, with the pointer swaps of P:361-362 */
     for (int j = 2; j <= k; ++j) {
-        orc_apply_A(nx, ny, nz, h, nslab, y, S);
+        orc_apply_A_bc(nx, ny, nz, h, nslab, bcm, y, S);
         double rc_ = rho[j], ro_ = rho[j - 1];
 #pragma omp parallel for schedule(static)
         for (int64_t c = 0; c < n; ++c)
@@ -290,6 +347,43 @@ int orc_apply_cheb(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, 
     memcpy(out, y, sizeof(double) * (size_t)n);
     free(S); free(y); free(z); free(w);
     return 0;
+}
+
+int orc_apply_cheb(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, int k,
+                   double a, double b, const double* q, double* out)
+{
+    return orc_apply_cheb_bc(nx, ny, nz, h, nslab, 0, k, a, b, q, out);
+}
+
+/* Chebyshev interval [a', b'] of a preconditioner (pc 1 GNoComm, 3 G(CI): global bounds
+ * rescaled by (c_min, c_max), R9; pc 2 BJ: exact bounds of the local blocks, R10).  The BJ
+ * blocks differ only in their z factor (first block: kind of face z-, last: kind of face
+ * z+, middle: Dirichlet at both cuts); one interval covers every block's spectrum (R27). */
+void orc_pc_interval(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, int bcm,
+                     int pc, double c_min, double c_max, double* out2)
+{
+    const int kx = (bcm & 1) + ((bcm >> 1) & 1), ky = ((bcm >> 2) & 1) + ((bcm >> 3) & 1),
+              kz = ((bcm >> 4) & 1) + ((bcm >> 5) & 1);
+    double a_iv = 0.0, b_iv = 0.0;
+    if (pc == 1 || pc == 3) {
+        double lmn, lmx;
+        orc_bounds_bc(nx, ny, nz, h, kx, ky, kz, &lmn, &lmx);
+        a_iv = c_min * lmn;
+        b_iv = c_max * lmx;
+    } else if (nslab == 1) {
+        orc_bounds_bc(nx, ny, nz, h, kx, ky, kz, &a_iv, &b_iv);
+    } else {
+        int kinds[3] = {(bcm >> 4) & 1, (bcm >> 5) & 1, 0};
+        int nk = nslab > 2 ? 3 : 2;
+        for (int q = 0; q < nk; ++q) {
+            double lmn, lmx;
+            orc_bounds_bc(nx, ny, nz / nslab, h, kx, ky, kinds[q], &lmn, &lmx);
+            if (q == 0 || lmn < a_iv) a_iv = lmn;
+            if (q == 0 || lmx > b_iv) b_iv = lmx;
+        }
+    }
+    out2[0] = a_iv;
+    out2[1] = b_iv;
 }
 
 /* ------------------------------------------------------------------------------------------
@@ -314,13 +408,16 @@ int orc_apply_cheb(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, 
  * *iters_out = number of completed iterations (each appended one entry to hist); a
  * breakdown at r~ᵀw ends the run before iteration i appends anything (iters = i-1).
  * ---------------------------------------------------------------------------------------- */
-int orc_bicgstab(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, int pc, int k,
-                 double c_min, double c_max, double lmin_ov, double lmax_ov,
-                 const double* b, const double* x0, double tol, int max_it, int fixed_it,
-                 double* x, double* hist, double* scal, int* iters_out, double* true_rel)
+int orc_bicgstab_bc(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, int bcm,
+                    int pc, int k, double c_min, double c_max, double lmin_ov, double lmax_ov,
+                    const double* b, const double* x0, double tol, int max_it, int fixed_it,
+                    double* x, double* hist, double* scal, int* iters_out, double* true_rel)
 {
     int64_t n = nx * ny * nz, pl = nx * ny;
     if (nslab < 1 || nz % nslab != 0) return 1;
+    /* mirror ghosts need a second point on a Neumann axis, and (z) inside every block */
+    if (((bcm & 3) && nx < 2) || ((bcm & 12) && ny < 2) || ((bcm & 48) && nz / nslab < 2))
+        return 1;
     double a_iv = 0.0, b_iv = 0.0;
     /* pc 3 = G(CI): Chebyshev on the global operator (no slab cuts) with the
      * global rescaled bounds -- the preconditioner is independent of the decomposition. */
@@ -328,13 +425,10 @@ int orc_bicgstab(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, in
     if (pc == 1 || pc == 2 || pc == 3) {
         if (lmin_ov > 0.0 && lmax_ov > 0.0) {
             a_iv = lmin_ov; b_iv = lmax_ov;
-        } else if (pc == 1 || pc == 3) {
-            double lmn, lmx;
-            orc_bounds(nx, ny, nz, h, &lmn, &lmx);
-            a_iv = c_min * lmn;
-            b_iv = c_max * lmx;
         } else {
-            orc_bounds(nx, ny, nz / nslab, h, &a_iv, &b_iv);
+            double iv[2];
+            orc_pc_interval(nx, ny, nz, h, nslab, bcm, pc, c_min, c_max, iv);
+            a_iv = iv[0]; b_iv = iv[1];
         }
         if (!(a_iv < b_iv) || !(a_iv > 0.0)) return 1;
     } else if (pc != 0) {
@@ -354,7 +448,7 @@ int orc_bicgstab(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, in
     /* Alg. 3 line 1: r0 = b - A x0 */
     if (x0) {
         memcpy(x, x0, sizeof(double) * (size_t)n);
-        orc_apply_A(nx, ny, nz, h, 1, x, tmp);
+        orc_apply_A_bc(nx, ny, nz, h, 1, bcm, x, tmp);
         for (int64_t c = 0; c < n; ++c) r[c] = b[c] - tmp[c];
     } else {
         memset(x, 0, sizeof(double) * (size_t)n);
@@ -383,9 +477,9 @@ int orc_bicgstab(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, in
         double* sc = scal ? scal + 8 * (i - 1) : NULL;
         /* line 6: solve M p̂ = p */
         if (pc == 0) memcpy(ph, p, sizeof(double) * (size_t)n);
-        else orc_apply_cheb(nx, ny, nz, h, nslab_pc, k, a_iv, b_iv, p, ph);
+        else orc_apply_cheb_bc(nx, ny, nz, h, nslab_pc, bcm, k, a_iv, b_iv, p, ph);
         /* MPI1 + KernelBiCGS1: w = A p̂ (global), local r~ᵀw; MPI2 */
-        orc_apply_A(nx, ny, nz, h, 1, ph, w);
+        orc_apply_A_bc(nx, ny, nz, h, 1, bcm, ph, w);
         double rw = orc_dot(pl, nz, rt, w);
         if (sc) sc[0] = rw;
         if (rw == 0.0 || !isfinite(rw)) { status = 7; it = i - 1; break; }
@@ -396,9 +490,9 @@ int orc_bicgstab(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, in
         for (int64_t c = 0; c < n; ++c) r[c] = fma(-alpha, w[c], r[c]);
         /* solve M r̂ = r */
         if (pc == 0) memcpy(rh, r, sizeof(double) * (size_t)n);
-        else orc_apply_cheb(nx, ny, nz, h, nslab_pc, k, a_iv, b_iv, r, rh);
+        else orc_apply_cheb_bc(nx, ny, nz, h, nslab_pc, bcm, k, a_iv, b_iv, r, rh);
         /* MPI3 + KernelBiCGS3: t = A r̂, tᵀr, tᵀt; MPI4 */
-        orc_apply_A(nx, ny, nz, h, 1, rh, t);
+        orc_apply_A_bc(nx, ny, nz, h, 1, bcm, rh, t);
         double ts = orc_dot(pl, nz, t, r);
         double tt = orc_dot(pl, nz, t, t);
         double omega = (tt == 0.0) ? 0.0 : ts / tt;  /* P:293, guard R6 */
@@ -437,12 +531,21 @@ int orc_bicgstab(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, in
 done:
     *iters_out = it;
     if (true_rel) {
-        orc_apply_A(nx, ny, nz, h, 1, x, tmp);
+        orc_apply_A_bc(nx, ny, nz, h, 1, bcm, x, tmp);
         for (int64_t c = 0; c < n; ++c) tmp[c] = b[c] - tmp[c];
         *true_rel = nb == 0.0 ? 0.0 : sqrt(orc_dot(pl, nz, tmp, tmp)) / nb;
     }
     free(r); free(rt); free(p); free(ph); free(rh); free(w); free(t); free(tmp);
     return status;
+}
+
+int orc_bicgstab(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, int pc, int k,
+                 double c_min, double c_max, double lmin_ov, double lmax_ov,
+                 const double* b, const double* x0, double tol, int max_it, int fixed_it,
+                 double* x, double* hist, double* scal, int* iters_out, double* true_rel)
+{
+    return orc_bicgstab_bc(nx, ny, nz, h, nslab, 0, pc, k, c_min, c_max, lmin_ov, lmax_ov, b,
+                           x0, tol, max_it, fixed_it, x, hist, scal, iters_out, true_rel);
 }
 
 /* Number of OpenMP threads the oracle's parallel loops use (reported as cpu_baseline.cores). */

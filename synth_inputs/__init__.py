@@ -107,3 +107,29 @@ def mms_polyexp(n: int):
     u = g(z) * g(y) * g(x)
     f = mg2(x) * g(y) * g(z) + g(x) * mg2(y) * g(z) + g(x) * g(y) * mg2(z)
     return f, u, h
+
+
+# --- the paper's own workload (§IV, R27) --------------------------
+
+#: Face kinds of the §IV problem, faces x-,x+,y-,y+,z-,z+ (0 Dirichlet, 1 Neumann):
+#: "Dirichlet ... on x-, y+, z+, while Neumann ... on x+, y-, z-".
+PAPER_BC = (0, 1, 1, 0, 1, 0)
+PAPER_LO = (3.0, 2.5, 10.0)          # x in [3, 28.5], y in [2.5, 28], z in [10, 35.5]
+PAPER_LEN = 25.5
+
+
+def paper_problem(n: int, z0: int = 0, nzl: int | None = None):
+    """f = sin x + cos y + 3 sin z - 2yz + 2 at the nodes of an n^3 grid over the paper's box.
+
+    Node i of an axis sits at lo + i*h with h = 25.5/(n-1) (n = 256 gives the paper's
+    Δ = 0.1 and 256 nodes per axis).  Boundary data are homogeneous (the paper does not
+    state them).  Returns (f planes z0..z0+nzl-1, h, PAPER_BC).
+    """
+    nzl = n - z0 if nzl is None else nzl
+    h = PAPER_LEN / (n - 1)
+    i = np.arange(n, dtype=np.float64)
+    x = (PAPER_LO[0] + i * h)[None, None, :]
+    y = (PAPER_LO[1] + i * h)[None, :, None]
+    z = (PAPER_LO[2] + (np.arange(z0, z0 + nzl, dtype=np.float64)) * h)[:, None, None]
+    f = np.sin(x) + np.cos(y) + 3.0 * np.sin(z) - 2.0 * y * z + 2.0
+    return np.ascontiguousarray(f), h, PAPER_BC

@@ -40,3 +40,25 @@ def cheb_T(n: int, x):
     for _ in range(n - 1):
         t0, t1 = t1, 2.0 * x * t1 - t0
     return t1
+
+
+def N(n: int, left: bool, right: bool) -> np.ndarray:
+    """Eq. 5: D with first row (2, -α) and last row (-β, 2); α = 2 for a Neumann
+    left end, β = 2 for a Neumann right end (else 1, i.e. matrix D).  Both ends Neumann is
+    the natural extension (α = β = 2)."""
+    m = D(n)
+    if left:
+        m[0, 1] = -2.0
+    if right:
+        m[n - 1, n - 2] = -2.0
+    return m
+
+
+def assemble_bc(nx: int, ny: int, nz: int, h: float, bc6) -> np.ndarray:
+    """Eq. 6 with O_d = D or N per axis; bc6 = face kinds x-,x+,y-,y+,z-,z+ (1 = Neumann)."""
+    Ox, Oy, Oz = N(nx, bc6[0], bc6[1]), N(ny, bc6[2], bc6[3]), N(nz, bc6[4], bc6[5])
+    Ix, Iy, Iz = np.eye(nx), np.eye(ny), np.eye(nz)
+    h2 = h * h
+    return (np.kron(Iz, np.kron(Iy, Ox / h2))
+            + np.kron(Iz, np.kron(Oy / h2, Ix))
+            + np.kron(Oz / h2, np.kron(Iy, Ix)))
