@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define BCGS_ABI_VERSION 1
+#define BCGS_ABI_VERSION 2
 #define BCGS_MAX_DEGREE 64       /* Chebyshev degree k (sweeps per application) cap      */
 #define BCGS_HIST_CAP 16384      /* max outer iterations recorded per solve              */
 
@@ -95,9 +95,20 @@ typedef enum {
     BCGS_OPT_XCONC = 7         /* 1 = x update on a concurrent low-priority stream (off)  */
 } bcgs_option;
 
+/* Boundary condition kind of a physical face (Eq. 4 / Eq. 5). */
+typedef enum {
+    BCGS_BC_DIRICHLET = 0,     /* ghost = boundary value, folded into b (R15)              */
+    BCGS_BC_NEUMANN = 1        /* ghost = mirror of the first interior neighbour, i.e. the */
+                               /* rows (2, -2) of Eq. 5's N ("Set Neumann BCs");    */
+                               /* a face value is the outward normal derivative (R28)      */
+} bcgs_bc;
+
 typedef struct {
-    int64_t n[3];   /* global unknowns along x, y, z (each >= 1)                          */
+    int64_t n[3];   /* global unknowns along x, y, z (each >= 1; >= 2 on a Neumann axis)  */
     double h;       /* uniform grid spacing (> 0); unit cube: h = 1/(n+1)                  */
+    int32_t bc[6];  /* bcgs_bc of faces x-, x+, y-, y+, z-, z+ (all 0 = all Dirichlet).   */
+                    /* Chebyshev bounds follow the face kinds (R27).  A Neumann z face    */
+                    /* needs >= 2 planes per preconditioner block.                        */
 } bcgs_grid_desc;
 
 typedef struct {
@@ -148,7 +159,8 @@ bcgs_status bcgs_set_option(bcgs_ctx ctx, int32_t option, int64_t value);
 /* Right-hand side b (Eq. 1; Alg. 3 l.1).  Random: R16, generated on the device from
  * the global index (identical bits for any rank count).  bcgs_set_rhs copies this rank's
  * slab.  Face values (R15): face 0..5 = x-,x+,y-,y+,z-,z+; the values set are folded
- * into b by every subsequent set_rhs* call (R15). */
+ * into b by every subsequent set_rhs* call: a Dirichlet value g adds g/h² to the first
+ * plane of unknowns (R15), a Neumann outward derivative g adds 2g/h (R28). */
 bcgs_status bcgs_set_rhs_random(bcgs_ctx ctx, uint64_t seed);
 bcgs_status bcgs_set_rhs(bcgs_ctx ctx, const double* f, int32_t mem);
 bcgs_status bcgs_set_boundary_value(bcgs_ctx ctx, int32_t face, double value);

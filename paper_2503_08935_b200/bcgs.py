@@ -48,7 +48,10 @@ class BcgsError(RuntimeError):
 
 
 class GridDesc(ctypes.Structure):
-    _fields_ = [("n", ctypes.c_int64 * 3), ("h", ctypes.c_double)]
+    _fields_ = [("n", ctypes.c_int64 * 3), ("h", ctypes.c_double), ("bc", ctypes.c_int32 * 6)]
+
+
+BC_DIRICHLET, BC_NEUMANN = 0, 1
 
 
 class Report(ctypes.Structure):
@@ -117,11 +120,14 @@ def load() -> ctypes.CDLL:
     return lib
 
 
-def grid_desc(n, h: float) -> GridDesc:
+def grid_desc(n, h: float, bc=None) -> GridDesc:
+    """bc: six face kinds (x-, x+, y-, y+, z-, z+; 0 Dirichlet, 1 Neumann), default all 0."""
     n3 = (n, n, n) if np.isscalar(n) else tuple(n)
     g = GridDesc()
     g.n[0], g.n[1], g.n[2] = (int(v) for v in n3)
     g.h = float(h)
+    for f, kind in enumerate(bc or (0,) * 6):
+        g.bc[f] = int(kind)
     return g
 
 
@@ -129,9 +135,9 @@ def workspace_bytes(n, h: float, nranks: int = 1) -> int:
     return int(load().bcgs_workspace_bytes(ctypes.byref(grid_desc(n, h)), nranks))
 
 
-def chebyshev_constants(n, h, nslab, pc, degree, c_min=10.0, c_max=1.0 - 1e-4):
+def chebyshev_constants(n, h, nslab, pc, degree, c_min=10.0, c_max=1.0 - 1e-4, bc=None):
     ivl, cst, rho = np.zeros(2), np.zeros(7), np.zeros(max(degree, 1) + 1)
-    st = load().bcgs_chebyshev_constants(ctypes.byref(grid_desc(n, h)), nslab, PC[pc], degree,
+    st = load().bcgs_chebyshev_constants(ctypes.byref(grid_desc(n, h, bc)), nslab, PC[pc], degree,
                                          c_min, c_max, ivl.ctypes.data, cst.ctypes.data,
                                          rho.ctypes.data)
     if st:
@@ -158,7 +164,7 @@ class Solver:
 
     def __init__(self, n, h: float, *, rank: int = 0, nranks: int = 1,
                  nccl_id: bytes | None = None, device: int | None = None, stream=None,
-                 _ctx=None, _workspace=None):
+                 bc=None, _ctx=None, _workspace=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("bcgs.Solver needs a CUDA device (no CPU fallback)")
@@ -169,7 +175,8 @@ class Solver:
         self.device = torch.cuda.current_device() if device is None else device
         self.L = self.n[2] // nranks
         self.shape = (self.L, self.n[1], self.n[0])
-        self.desc = grid_desc(self.n, h)
+        self.bc = tuple(bc) if bc is not None else (0,) * 6
+        self.desc = grid_desc(self.n, h, self.bc)
         if _ctx is not None:                       # member of a local group
             self.ctx, self.workspace = _ctx, _workspace
             self.stream = stream
@@ -323,13 +330,13 @@ class Solver:
         self.lib.bcgs_kernel_times_reset(self.ctx)
 
 
-def local_group(n, h: float, nranks: int, device: int | None = None) -> list:
+def local_group(n, h: float, nranks: int, device: int | None = None, bc=None) -> list:
     """nranks Solver contexts on ONE GPU exchanging halos / reductions by device copies
     (bcgs_create_local).  Drive each from its own thread."""
     import torch
     lib = load()
     device = torch.cuda.current_device() if device is None else device
-    desc = grid_desc(n, h)
+    desc = grid_desc(n, h, bc)
     nbytes = lib.bcgs_workspace_bytes(ctypes.byref(desc), nranks)
     if nbytes == 0:
         raise BcgsError(E_CONFIG, "grid not divisible into z-slabs")
@@ -341,5 +348,5 @@ def local_group(n, h: float, nranks: int, device: int | None = None) -> list:
                                stream.cuda_stream, outs)
     if st:
         raise BcgsError(st, "bcgs_create_local")
-    return [Solver(n, h, rank=r, nranks=nranks, device=device, stream=stream,
+    return [Solver(n, h, rank=r, nranks=nranks, device=device, stream=stream, bc=bc,
                    _ctx=ctypes.c_void_p(outs[r]), _workspace=wss[r]) for r in range(nranks)]

@@ -19,7 +19,18 @@ ref::Grid ref_grid(bcgs_ctx c, int Lb)
     g.L = (int)c->lay.L;
     g.Lb = Lb;
     g.h2inv = c->h2inv;
+    g.bc = c->mbc;
     return g;
+}
+
+// Mirror faces of the extended slab of G(CI) (planes [v0, v1) valid): the physical z faces
+// sit at v0 on the first rank and at v1 - 1 on the last.
+ref::MirrorBc ext_mirror(bcgs_ctx c, int v0, int v1)
+{
+    ref::MirrorBc m = c->mbc;
+    m.zlo = (c->rank == 0 && c->bc[4]) ? v0 : -1;
+    m.zhi = (c->rank == c->nranks - 1 && c->bc[5]) ? v1 - 1 : -1;
+    return m;
 }
 
 dim3 stencil_grid(bcgs_ctx c)
@@ -90,11 +101,44 @@ double mu(int64_t n, int64_t i)
     return 4.0 * (s * s);
 }
 
-void bounds_box(int64_t nx, int64_t ny, int64_t nzb, double h, double* lo, double* hi)
+// Extreme eigenvalues of one 1-D factor with `nn` Neumann ends (R27; Eq. 5's N):
+//   nn = 0: Eq. 9, i = 1 and n;   nn = 1: 4 sin²((2i-1)π/(4n)), i = 1 and n;
+//   nn = 2: 4 sin²(iπ/(2(n-1))), i = 0 and n-1.
+void factor_range(int64_t n, int nn, double* lo, double* hi)
 {
-    double h2inv = 1.0 / (h * h);
-    *lo = ((mu(nx, 1) * h2inv) + (mu(ny, 1) * h2inv)) + (mu(nzb, 1) * h2inv);
-    *hi = ((mu(nx, nx) * h2inv) + (mu(ny, ny) * h2inv)) + (mu(nzb, nzb) * h2inv);
+    auto f1 = [n](int64_t i) {
+        double s = sin(((double)(2 * i - 1) * M_PI) / (4.0 * (double)n));
+        return 4.0 * (s * s);
+    };
+    auto f2 = [n](int64_t i) {
+        double s = sin(((double)i * M_PI) / (2.0 * (double)(n - 1)));
+        return 4.0 * (s * s);
+    };
+    if (nn == 0) { *lo = mu(n, 1); *hi = mu(n, n); }
+    else if (nn == 1) { *lo = f1(1); *hi = f1(n); }
+    else { *lo = f2(0); *hi = f2(n - 1); }
+}
+
+// Eqs. 10-11: sums of the factor extremes; nn[3] = Neumann ends of the x, y, z factors.
+void bounds_box(int64_t nx, int64_t ny, int64_t nzb, double h, const int* nn, double* lo,
+                double* hi)
+{
+    double h2inv = 1.0 / (h * h), lx, hx, ly, hy, lz, hz;
+    factor_range(nx, nn[0], &lx, &hx);
+    factor_range(ny, nn[1], &ly, &hy);
+    factor_range(nzb, nn[2], &lz, &hz);
+    *lo = ((lx * h2inv) + (ly * h2inv)) + (lz * h2inv);
+    *hi = ((hx * h2inv) + (hy * h2inv)) + (hz * h2inv);
+}
+
+// Face kinds are 0 / 1 and a Neumann axis has >= 2 points (the mirror needs a neighbour).
+bool bc_ok(const bcgs_grid_desc* g)
+{
+    for (int f = 0; f < 6; ++f)
+        if (g->bc[f] != BCGS_BC_DIRICHLET && g->bc[f] != BCGS_BC_NEUMANN) return false;
+    for (int d = 0; d < 3; ++d)
+        if ((g->bc[2 * d] || g->bc[2 * d + 1]) && g->n[d] < 2) return false;
+    return true;
 }
 
 bcgs_status cheb_constants(const bcgs_grid_desc* g, int32_t nslab, bcgs_pc pc, int32_t k,
@@ -106,13 +150,27 @@ bcgs_status cheb_constants(const bcgs_grid_desc* g, int32_t nslab, bcgs_pc pc, i
     if (ov_a > 0.0 || ov_b > 0.0) {
         a = ov_a;
         b = ov_b;
-    } else if (pc == BCGS_PC_CHEB_GNOCOMM || pc == BCGS_PC_CHEB_G) {
-        double lo, hi;
-        bounds_box(g->n[0], g->n[1], g->n[2], g->h, &lo, &hi);
-        a = c_min * lo;
-        b = c_max * hi;
     } else {
-        bounds_box(g->n[0], g->n[1], g->n[2] / nslab, g->h, &a, &b);   // R10
+        int nn[3] = {g->bc[0] + g->bc[1], g->bc[2] + g->bc[3], g->bc[4] + g->bc[5]};
+        if (pc == BCGS_PC_CHEB_GNOCOMM || pc == BCGS_PC_CHEB_G) {
+            double lo, hi;
+            bounds_box(g->n[0], g->n[1], g->n[2], g->h, nn, &lo, &hi);
+            a = c_min * lo;
+            b = c_max * hi;
+        } else if (nslab == 1) {
+            bounds_box(g->n[0], g->n[1], g->n[2], g->h, nn, &a, &b);   // R10
+        } else {
+            // R10 + R27: the blocks' z factors are (z- kind, D), (D, D), (D, z+ kind); one
+            // interval spanning all of them
+            const int zk[3] = {g->bc[4], g->bc[5], 0};
+            for (int q = 0; q < (nslab > 2 ? 3 : 2); ++q) {
+                double lo, hi;
+                int nb[3] = {nn[0], nn[1], zk[q]};
+                bounds_box(g->n[0], g->n[1], g->n[2] / nslab, g->h, nb, &lo, &hi);
+                if (q == 0 || lo < a) a = lo;
+                if (q == 0 || hi > b) b = hi;
+            }
+        }
     }
     if (!(a > 0.0) || !(a < b) || !std::isfinite(b)) return BCGS_E_SPECTRUM;
     double theta = (b + a) / 2.0, delta = (b - a) / 2.0;   // Eq. 15
@@ -310,13 +368,15 @@ bcgs_status precond_g(bcgs_ctx c, const double* q, double* out, const DevState* 
     };
     Prof pf(c, KC_PRECOND, 16.0 * npts(c));
     ref::k_cheb_sweep_rng<<<grid(v0, v1), blk, 0, c->s>>>(E, nullptr, nullptr, A, nx, ny, v0, v1,
-                                                          v0, v1, c->h2inv, cc, 0.0, 0.0, 1, st);
+                                                          v0, v1, c->h2inv, ext_mirror(c, v0, v1),
+                                                          cc, 0.0, 0.0, 1, st);
     double* xm1 = A;
     double* xm2 = nullptr;
     for (int j = 2; j <= k; ++j) {
         double* dst = xm2 ? xm2 : B;
         ref::k_cheb_sweep_rng<<<grid(v0, v1), blk, 0, c->s>>>(E, xm1, xm2, dst, nx, ny, v0, v1, v0,
-                                                              v1, c->h2inv, cc, c->rho[j],
+                                                              v1, c->h2inv, ext_mirror(c, v0, v1),
+                                                              cc, c->rho[j],
                                                               c->rho[j - 1], 0, st);
         xm2 = xm1;
         xm1 = dst;
@@ -500,7 +560,8 @@ bcgs_status fold_faces(bcgs_ctx c)
     int mask = 0;
     double add[6];
     for (int f = 0; f < 6; ++f) {
-        add[f] = c->face[f] * c->h2inv;
+        // R15 Dirichlet value g -> g/h²; R28 Neumann outward derivative g -> 2g/h
+        add[f] = c->bc[f] ? (2.0 * c->face[f]) / c->h : c->face[f] * c->h2inv;
         if (c->face[f] != 0.0) mask |= 1 << f;
     }
     if (!mask) return BCGS_OK;
@@ -513,7 +574,8 @@ bcgs_status fold_faces(bcgs_ctx c)
 
 bcgs_status validate_pc(bcgs_ctx c)
 {
-    bcgs_grid_desc g{{c->lay.nx, c->lay.ny, c->lay.nz}, c->h};
+    bcgs_grid_desc g{{c->lay.nx, c->lay.ny, c->lay.nz}, c->h, {0, 0, 0, 0, 0, 0}};
+    memcpy(g.bc, c->bc, sizeof g.bc);
     if (c->pc == BCGS_PC_NONE) return BCGS_OK;
     bcgs_status s = cheb_constants(&g, c->nranks * c->bpr, c->pc, c->degree, c->c_min, c->c_max,
                                    c->ov_a, c->ov_b, c->ivl, c->cst, c->rho);
@@ -562,6 +624,9 @@ bcgs_status bcgs_chebyshev_constants(const bcgs_grid_desc* grid, int32_t nslab, 
 {
     if (!grid || nslab < 1 || grid->n[2] % nslab || !interval2 || !out7 || !rho)
         return BCGS_E_INVALID;
+    if (!bc_ok(grid)) return BCGS_E_CONFIG;
+    if ((grid->bc[4] || grid->bc[5]) && pc != BCGS_PC_CHEB_G && grid->n[2] / nslab < 2)
+        return BCGS_E_CONFIG;
     if (pc != BCGS_PC_CHEB_GNOCOMM && pc != BCGS_PC_CHEB_BJ && pc != BCGS_PC_CHEB_G)
         return BCGS_E_INVALID;
     return cheb_constants(grid, nslab, pc, degree, c_min, c_max, 0.0, 0.0, interval2, out7, rho);
@@ -585,6 +650,7 @@ static bcgs_status create_ctx(const bcgs_grid_desc* grid, int32_t rank, int32_t 
     if (!grid || !out || nranks < 1 || rank < 0 || rank >= nranks) return BCGS_E_INVALID;
     if (!(grid->h > 0.0)) return BCGS_E_INVALID;
     if (nranks > 1 && !nccl_unique_id && !lg) return BCGS_E_INVALID;
+    if (!bc_ok(grid)) return BCGS_E_CONFIG;
     Layout lay;
     if (!make_layout(grid, nranks, &lay)) return BCGS_E_CONFIG;
     if (lay.nx > (1 << 30) || lay.ny > (1 << 30)) return BCGS_E_CONFIG;
@@ -594,6 +660,11 @@ static bcgs_status create_ctx(const bcgs_grid_desc* grid, int32_t rank, int32_t 
     c->lay = lay;
     c->h = grid->h;
     c->h2inv = 1.0 / (grid->h * grid->h);
+    memcpy(c->bc, grid->bc, sizeof c->bc);
+    c->mbc.m = (grid->bc[0] ? 1 : 0) | (grid->bc[1] ? 2 : 0) | (grid->bc[2] ? 4 : 0) |
+               (grid->bc[3] ? 8 : 0);
+    c->mbc.zlo = (rank == 0 && grid->bc[4]) ? 0 : -1;
+    c->mbc.zhi = (rank == nranks - 1 && grid->bc[5]) ? (int)lay.L - 1 : -1;
     c->rank = rank;
     c->nranks = nranks;
     c->device = cuda_device;
@@ -773,6 +844,8 @@ bcgs_status bcgs_set_preconditioner(bcgs_ctx c, bcgs_pc pc, int32_t degree, doub
     if (blocks_per_rank < 1 || c->lay.L % blocks_per_rank)
         return fail(c, BCGS_E_CONFIG, "slab of %lld planes not divisible into %d blocks (axis z)",
                     (long long)c->lay.L, blocks_per_rank);
+    if ((c->bc[4] || c->bc[5]) && pc != BCGS_PC_CHEB_G && c->lay.L / blocks_per_rank < 2)
+        return fail(c, BCGS_E_CONFIG, "a Neumann z face needs >= 2 planes per block");
     if (pc == BCGS_PC_CHEB_G) {
         blocks_per_rank = 1;   // the global operator has no block cuts
         if (c->nranks > 1 && degree > c->lay.L)

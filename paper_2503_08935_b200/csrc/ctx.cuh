@@ -127,6 +127,8 @@ struct LocalGroup {
 struct bcgs_ctx_s {
     Layout lay;
     double h = 0.0, h2inv = 0.0;
+    int32_t bc[6] = {0, 0, 0, 0, 0, 0};   // face kinds (bcgs_bc)
+    ref::MirrorBc mbc{0, -1, -1};         // this rank's mirror faces, slab plane indices
     int rank = 0, nranks = 1, device = 0;
     cudaStream_t user = nullptr, s = nullptr;
     cudaEvent_t join = nullptr;

@@ -56,6 +56,7 @@ bcgs_status launch_tb(bcgs_ctx c, TbArgs& a)
     a.ny = (int)c->lay.ny;
     a.Lb = (int)(c->lay.L / c->bpr);
     a.h2inv = c->h2inv;
+    if (!a.ext) a.bc = c->mbc;
     a.cz = c->cst[3];
     a.g1 = c->cst[4];
     a.A2 = c->cst[5];
@@ -65,7 +66,10 @@ bcgs_status launch_tb(bcgs_ctx c, TbArgs& a)
     // SMs (one CTA per SM) more evenly.  Pick the chunk count minimising
     // waves * (planes per chunk + 2k).
     int tx, ty;
-    variant_tile((MODE == MODE_P && c->defer_x) ? 5 : c->tb_variant, k, &tx, &ty);
+    const bool neu = a.bc.m || a.bc.zlo >= 0 || a.bc.zhi >= 0;   // see launch_variant
+    variant_tile(neu ? ((c->tb_variant != 2 && k <= 5 && a.nx % 2 == 0) ? 5 : 2)
+                     : (MODE == MODE_P && c->defer_x) ? 5 : c->tb_variant,
+                 k, &tx, &ty);
     if (a.ext) a.Lb = a.zo1 - a.zo0;   // chunks over the output planes, one "block"
     const int nblk = a.ext ? 1 : c->bpr;
     const int64_t tiles = ((a.nx + tx - 1) / tx) * (int64_t)((a.ny + ty - 1) / ty) * nblk;
@@ -110,6 +114,7 @@ bcgs_status precond_g_tb(bcgs_ctx c, const double* E, double* out, int v0, int v
     a.zv1 = v1;
     a.zo0 = (int)KG;
     a.zo1 = (int)(KG + c->lay.L);
+    a.bc = ext_mirror(c, v0, v1);
     return launch_tb<MODE_PLAIN>(c, a);
 }
 
@@ -140,8 +145,9 @@ void on_begin(bcgs_ctx c)
         cudaStreamWaitEvent(c->s_x, c->ev_omega, 0);
         cudaEventRecord(c->ev_xdone, c->s_x);
     }
-    c->defer_x = (c->defer_x_opt && !g_multi && c->kernels == 1 && c->pc != BCGS_PC_NONE &&
-                  (c->lay.nx % 2) == 0 &&
+    const bool neu = c->mbc.m || c->mbc.zlo >= 0 || c->mbc.zhi >= 0;
+    c->defer_x = (c->defer_x_opt && !g_multi && !neu && c->kernels == 1 &&
+                  c->pc != BCGS_PC_NONE && (c->lay.nx % 2) == 0 &&
                   defer_x_ok(c)) ? 1 : 0;
 }
 
@@ -176,11 +182,11 @@ bcgs_status halo_stencil(bcgs_ctx c, double* v, const double* a, double* out, in
         const dim3 g = stream::stencil2_grid(nx, ny, ke - kb, cfg);
         dd* pp = c->part + (int64_t)nb * ND;
         switch (cfg) {
-        case 1: stream::k_stencil2_dot<ND, 32, 8, 16><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv, pp, c->st); break;
-        case 2: stream::k_stencil2_dot<ND, 32, 4, 16><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv, pp, c->st); break;
-        case 3: stream::k_stencil2_dot<ND, 64, 4, 8><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv, pp, c->st); break;
-        case 4: stream::k_stencil2_dot<ND, 32, 16, 4><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv, pp, c->st); break;
-        default: stream::k_stencil2_dot<ND, 32, 8, 8><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv, pp, c->st); break;
+        case 1: stream::k_stencil2_dot<ND, 32, 8, 16><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st); break;
+        case 2: stream::k_stencil2_dot<ND, 32, 4, 16><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st); break;
+        case 3: stream::k_stencil2_dot<ND, 64, 4, 8><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st); break;
+        case 4: stream::k_stencil2_dot<ND, 32, 16, 4><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st); break;
+        default: stream::k_stencil2_dot<ND, 32, 8, 8><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st); break;
         }
         nb += (int)(g.x * g.y * g.z);
     };

@@ -17,6 +17,7 @@
 #include <stdint.h>
 
 #include "expr.cuh"
+#include "ref_shapes.cuh"
 #include "state.cuh"
 
 namespace fused {
@@ -39,6 +40,8 @@ struct TbArgs {
     // extended-slab mode (G(CI), ext = 1): zero ghosts outside planes [zv0, zv1), outputs
     // for planes [zo0, zo1) only, one block; plane indices are extended-slab indices.
     int ext, zv0, zv1, zo0, zo1;
+    // Neumann faces (R27): x/y bits and the planes whose z-/z+ neighbour is mirrored
+    ref::MirrorBc bc;
     double h2inv, cz, g1, A2, B2;
     double rho[KMAX_TB + 1];
     const DevState* st;
@@ -56,7 +59,7 @@ struct TbShape {
 // phase PH of the (fully unrolled) z-step, so no register moves are needed:
 //   q ring (QW >= max(K+1, 3) planes, multiple of 3): q(t-d) at slot (PH-d) mod QW
 //   win[j] (levels 1..K-1, 3 planes):                x_j(newest-d) at slot (PH-d) mod 3
-template <int K, int TX, int TY, int MODE>
+template <int K, int TX, int TY, int MODE, bool NEU = false>
 struct TbThread {
     using S = TbShape<K, TX, TY>;
     static constexpr int EX = S::EX, NT = S::NT, PLANE = S::PLANE;
@@ -71,6 +74,7 @@ struct TbThread {
     int tid, b0, b1, c0, c1;
     int64_t col, plane;
     unsigned actmask;                            // bit j: level j needed at this column
+    int mir;                                     // Neumann mirror bits of this column
     bool in_dom, in_tile, first;
     double alpha, beta, omega;
     const double* pin;
@@ -114,8 +118,8 @@ struct TbThread {
         for (int j = 1; j <= K; ++j) {
             const int m = t - j;
             const double* pl = prev + (j - 1) * PLANE;
-            const double xm = pl[tid - 1], xp = pl[tid + 1];
-            const double ym = pl[tid - EX], yp = pl[tid + EX];
+            double xm = pl[tid - 1], xp = pl[tid + 1];
+            double ym = pl[tid - EX], yp = pl[tid + EX];
             double zm, zc, zp;   // x_{j-1} at planes m-1, m, m+1
             if (j == 1) {
                 zp = qw[PH % QW];
@@ -125,6 +129,16 @@ struct TbThread {
                 zp = win[j - 1][PH % 3];
                 zc = win[j - 1][(PH + 2) % 3];
                 zm = win[j - 1][(PH + 1) % 3];
+            }
+            if (NEU) {                                   // R27 mirror ghosts
+                if (mir) {
+                    if (mir & 1) xm = xp;
+                    if (mir & 2) xp = xm;
+                    if (mir & 4) ym = yp;
+                    if (mir & 8) yp = ym;
+                }
+                if (m == a->bc.zlo) zm = zp;
+                if (m == a->bc.zhi) zp = zm;
             }
             const double Sv = stencil_row(zc, xm, xp, ym, yp, zm, zp, a->h2inv);
             const double qc = qw[(PH + QW - j) % QW];
@@ -152,10 +166,10 @@ struct TbThread {
     }
 };
 
-template <int K, int TX, int TY, int MODE>
+template <int K, int TX, int TY, int MODE, bool NEU = false>
 __global__ void __launch_bounds__(TbShape<K, TX, TY>::NT, 1) k_cheb_tb(TbArgs a)
 {
-    using T = TbThread<K, TX, TY, MODE>;
+    using T = TbThread<K, TX, TY, MODE, NEU>;
     constexpr int EX = T::EX, U = T::U;
     extern __shared__ double sm[];   // [2][K][PAD + NT + PAD]
 
@@ -188,6 +202,8 @@ __global__ void __launch_bounds__(TbShape<K, TX, TY>::NT, 1) k_cheb_tb(TbArgs a)
     // Chebyshev distance of this column outside the output tile (<= 0 inside)
     const int dist = max(max(K - ex, ex - (K + TX - 1)), max(K - ey, ey - (K + TY - 1)));
     th.in_tile = th.in_dom && dist <= 0;
+    th.mir = ((gx == 0 && (a.bc.m & 1)) ? 1 : 0) | ((gx == a.nx - 1 && (a.bc.m & 2)) ? 2 : 0) |
+             ((gy == 0 && (a.bc.m & 4)) ? 4 : 0) | ((gy == a.ny - 1 && (a.bc.m & 8)) ? 8 : 0);
     th.actmask = 0;
 #pragma unroll
     for (int j = 1; j <= K; ++j)

@@ -51,14 +51,16 @@ __global__ void k_fold_boundary(double* __restrict__ b, Grid g, int64_t z0, int6
 // ------------------------------------------------------------------- stencil helpers
 // Neighbour sum of the 7-point stencil at (i, j, k); z-neighbours passed in (they may be
 // block-cut zeros or ghost-plane values).
+// Out-of-domain x / y neighbours: 0 (Dirichlet) or, on a Neumann face (bit of m), the
+// interior neighbour on the other side (R27 mirror ghost, Eq. 5).
 __device__ __forceinline__ double stencil_at(const double* __restrict__ v, int64_t c, int i,
                                              int j, int nx, int ny, double vzm, double vzp,
-                                             double h2inv)
+                                             double h2inv, int m)
 {
-    const double xm = (i > 0) ? v[c - 1] : 0.0;
-    const double xp = (i < nx - 1) ? v[c + 1] : 0.0;
-    const double ym = (j > 0) ? v[c - nx] : 0.0;
-    const double yp = (j < ny - 1) ? v[c + nx] : 0.0;
+    const double xm = (i > 0) ? v[c - 1] : ((m & 1) ? v[c + 1] : 0.0);
+    const double xp = (i < nx - 1) ? v[c + 1] : ((m & 2) ? v[c - 1] : 0.0);
+    const double ym = (j > 0) ? v[c - nx] : ((m & 4) ? v[c + nx] : 0.0);
+    const double yp = (j < ny - 1) ? v[c + nx] : ((m & 8) ? v[c - nx] : 0.0);
     return stencil_row(v[c], xm, xp, ym, yp, vzm, vzp, h2inv);
 }
 
@@ -85,9 +87,11 @@ __global__ void __launch_bounds__(BX * BY) k_stencil_dot(const double* __restric
         double vzm = in[c - plane], vc = in[c];
         for (int k = k0; k < k1; ++k, c += plane) {
             const double vzp = in[c + plane];
-            const double zm = (block_local && (k % g.Lb) == 0) ? 0.0 : vzm;
-            const double zp = (block_local && (k % g.Lb) == g.Lb - 1) ? 0.0 : vzp;
-            const double o = stencil_at(in, c, i, j, g.nx, g.ny, zm, zp, g.h2inv);
+            const double zm = (k == g.bc.zlo) ? vzp
+                              : (block_local && (k % g.Lb) == 0) ? 0.0 : vzm;
+            const double zp = (k == g.bc.zhi) ? vzm
+                              : (block_local && (k % g.Lb) == g.Lb - 1) ? 0.0 : vzp;
+            const double o = stencil_at(in, c, i, j, g.nx, g.ny, zm, zp, g.h2inv, g.bc.m);
             out[c] = o;
             if (ND >= 1) dot2_acc(p[0], s[0], a[c], o);
             if (ND >= 2) dot2_acc(p[ND - 1], s[ND - 1], o, o);
@@ -102,7 +106,8 @@ __global__ void __launch_bounds__(BX * BY) k_stencil_dot(const double* __restric
 }
 
 // ------------------------------------------------------------------- Chebyshev sweeps
-// Alg. 4 with the slab-block operator (zero ghosts at every block cut and physical face):
+// Alg. 4 with the slab-block operator (zero ghosts at every block cut and Dirichlet face,
+// mirror ghosts at Neumann faces):
 //   sweep 1 (KernelCI1): out = g1*((2q) - (S(q)*cz))
 //   sweep j (KernelCI2):     out = ρ_j*(((A2*x1) + (B2*(q - S(x1)))) - (ρ_{j-1}*x2))
 //   with x2 = q*cz for j = 2 (z = b/θ is recomputed, not stored: same bits).
@@ -126,9 +131,11 @@ __global__ void __launch_bounds__(BX * BY) k_cheb_sweep(const double* __restrict
     const double* v = first ? q : x1;
     int64_t c = i + (int64_t)g.nx * j + plane * k0;
     for (int k = k0; k < k1; ++k, c += plane) {
-        const double zm = ((k % g.Lb) == 0) ? 0.0 : v[c - plane];
-        const double zp = ((k % g.Lb) == g.Lb - 1) ? 0.0 : v[c + plane];
-        const double S = stencil_at(v, c, i, j, g.nx, g.ny, zm, zp, g.h2inv);
+        const double zm = (k == g.bc.zlo) ? v[c + plane]
+                          : ((k % g.Lb) == 0) ? 0.0 : v[c - plane];
+        const double zp = (k == g.bc.zhi) ? v[c - plane]
+                          : ((k % g.Lb) == g.Lb - 1) ? 0.0 : v[c + plane];
+        const double S = stencil_at(v, c, i, j, g.nx, g.ny, zm, zp, g.h2inv, g.bc.m);
         const double qc = q[c];
         double o;
         if (first) {
@@ -142,13 +149,13 @@ __global__ void __launch_bounds__(BX * BY) k_cheb_sweep(const double* __restrict
 }
 
 // G(CI) on an extended slab (k-deep halo planes present): one Chebyshev sweep over planes
-// [kb, ke) of the GLOBAL operator; planes outside [v0, v1) are the physical Dirichlet
+// [kb, ke) of the GLOBAL operator; planes outside [v0, v1) are the physical boundary
 // ghosts (zero).  Same per-point expressions as k_cheb_sweep.
 __global__ void __launch_bounds__(BX * BY) k_cheb_sweep_rng(const double* __restrict__ q,
                                                             const double* __restrict__ x1,
                                                             const double* x2, double* out, int nx,
                                                             int ny, int kb, int ke, int v0, int v1,
-                                                            double h2inv, ChebConst cc,
+                                                            double h2inv, MirrorBc bc, ChebConst cc,
                                                             double rho_j, double rho_jm1,
                                                             int first,
                                                             const DevState* __restrict__ st)
@@ -161,9 +168,9 @@ __global__ void __launch_bounds__(BX * BY) k_cheb_sweep_rng(const double* __rest
     const double* v = first ? q : x1;
     int64_t c = i + (int64_t)nx * j + plane * k0;
     for (int k = k0; k < k1; ++k, c += plane) {
-        const double zm = (k - 1 < v0) ? 0.0 : v[c - plane];
-        const double zp = (k + 1 >= v1) ? 0.0 : v[c + plane];
-        const double S = stencil_at(v, c, i, j, nx, ny, zm, zp, h2inv);
+        const double zm = (k == bc.zlo) ? v[c + plane] : (k - 1 < v0) ? 0.0 : v[c - plane];
+        const double zp = (k == bc.zhi) ? v[c - plane] : (k + 1 >= v1) ? 0.0 : v[c + plane];
+        const double S = stencil_at(v, c, i, j, nx, ny, zm, zp, h2inv, bc.m);
         const double qc = q[c];
         double o;
         if (first) {

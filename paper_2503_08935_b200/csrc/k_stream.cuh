@@ -8,6 +8,7 @@
 #pragma once
 #include "dd.cuh"
 #include "expr.cuh"
+#include "ref_shapes.cuh"
 #include "state.cuh"
 
 namespace stream {
@@ -26,6 +27,7 @@ __global__ void __launch_bounds__(SBX * SBY) k_stencil2_dot(const double* __rest
                                                             const double* __restrict__ a,
                                                             double* __restrict__ out, int nx,
                                                             int ny, int kb, int ke, double h2inv,
+                                                            ref::MirrorBc bc,
                                                             dd* __restrict__ part,
                                                             const DevState* __restrict__ st)
 {
@@ -43,15 +45,19 @@ __global__ void __launch_bounds__(SBX * SBY) k_stencil2_dot(const double* __rest
 #pragma unroll 2
         for (int k = k0; k < k1; ++k, c += plane) {
             const double2 zp = *reinterpret_cast<const double2*>(v + c + plane);
-            const double xm = hxm ? __ldg(v + c - 1) : 0.0;
-            const double xp = hxp ? __ldg(v + c + 2) : 0.0;
-            const double2 ym = hym ? *reinterpret_cast<const double2*>(v + c - nx) : make_double2(0, 0);
-            const double2 yp = hyp ? *reinterpret_cast<const double2*>(v + c + nx) : make_double2(0, 0);
+            // out-of-domain neighbours: 0, or the mirror on a Neumann face (R27)
+            const double xm = hxm ? __ldg(v + c - 1) : ((bc.m & 1) ? zc.y : 0.0);
+            const double xp = hxp ? __ldg(v + c + 2) : ((bc.m & 2) ? zc.x : 0.0);
+            double2 ym = hym ? *reinterpret_cast<const double2*>(v + c - nx) : make_double2(0, 0);
+            double2 yp = hyp ? *reinterpret_cast<const double2*>(v + c + nx) : make_double2(0, 0);
+            if (!hym && (bc.m & 4)) ym = yp;
+            if (!hyp && (bc.m & 8)) yp = ym;
+            const double2 zmk = (k == bc.zlo) ? zp : zm, zpk = (k == bc.zhi) ? zm : zp;
             double2 av = make_double2(0, 0);
             if (ND >= 1) av = __ldg(reinterpret_cast<const double2*>(a + c));
             double2 o;
-            o.x = stencil_row(zc.x, xm, zc.y, ym.x, yp.x, zm.x, zp.x, h2inv);
-            o.y = stencil_row(zc.y, zc.x, xp, ym.y, yp.y, zm.y, zp.y, h2inv);
+            o.x = stencil_row(zc.x, xm, zc.y, ym.x, yp.x, zmk.x, zpk.x, h2inv);
+            o.y = stencil_row(zc.y, zc.x, xp, ym.y, yp.y, zmk.y, zpk.y, h2inv);
             *reinterpret_cast<double2*>(out + c) = o;
             if (ND >= 1) {
                 dot2_acc(p[0], s[0], av.x, o.x);

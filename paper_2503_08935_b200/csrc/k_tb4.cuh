@@ -73,7 +73,8 @@ struct Tb4Shape {
     static constexpr size_t xupd_bytes = sizeof(double) * 2 * 3 * NW * 32 * RY;
 };
 
-template <int K, int RY, int NW, int NS, int MODE, bool XUPD = false, bool XSH = false>
+template <int K, int RY, int NW, int NS, int MODE, bool XUPD = false, bool XSH = false,
+          bool NEU = false>
 struct Tb4Thread {
     using S = Tb4Shape<K, RY, NW, NS>;
     static constexpr int EX = S::EX, TX = S::TX, TY = S::TY, PLANE = S::PLANE, QW = S::QW,
@@ -89,6 +90,7 @@ struct Tb4Thread {
     int lane, ey0, b0, b1, c0, c1, t0, t1, wdy, tx0, ty0;
     int64_t col[RY], plane;
     unsigned actmask[RY];
+    int mir;           // Neumann mirror bits: 1 x-, 2 x+, 4<<2r y-, 8<<2r y+ (row r)
     bool in_dom[RY], in_tile[RY], first;
     double alpha, beta, omega;
     const CUtensorMap* pmap;
@@ -199,8 +201,20 @@ struct Tb4Thread {
                     }
                     // x-neighbours: from the neighbouring lanes' registers (XSH; the warp is one
                     // extended row segment and the x-halo lanes are never active) or smem
-                    const double xm = XSH ? __shfl_up_sync(0xffffffffu, zc, 1) : pl[r * EX - 1];
-                    const double xp = XSH ? __shfl_down_sync(0xffffffffu, zc, 1) : pl[r * EX + 1];
+                    double xm = XSH ? __shfl_up_sync(0xffffffffu, zc, 1) : pl[r * EX - 1];
+                    double xp = XSH ? __shfl_down_sync(0xffffffffu, zc, 1) : pl[r * EX + 1];
+                    // R27 mirror ghosts: only next to a physical face, which only masked
+                    // steps reach (non-interior tiles; the prologue covers plane b0)
+                    if (NEU && MASK) {
+                        if (mir) {
+                            if (mir & 1) xm = xp;
+                            if (mir & 2) xp = xm;
+                            if (mir & (4 << (2 * r))) yc_m = yc_p;
+                            if (mir & (8 << (2 * r))) yc_p = yc_m;
+                        }
+                        if (m == a->bc.zlo) zm = zp;
+                        if (m == a->bc.zhi) zp = zm;
+                    }
                     const double Sv = stencil_row(zc, xm, xp, yc_m, yc_p, zm, zp, a->h2inv);
                     const double qc = qw[(PH + QW - j) % QW][r];
                     double vv;
@@ -299,11 +313,11 @@ struct Tb4Thread {
 };
 
 template <int K, int RY, int NW, int NS, int MODE, int MINB = 1, bool XUPD = false,
-          bool XSH = false>
+          bool XSH = false, bool NEU = false>
 __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constant__ TbArgs a,
                                                        const __grid_constant__ TbMaps maps)
 {
-    using T = Tb4Thread<K, RY, NW, NS, MODE, XUPD, XSH>;
+    using T = Tb4Thread<K, RY, NW, NS, MODE, XUPD, XSH, NEU>;
     using S = Tb4Shape<K, RY, NW, NS>;
     constexpr int TX = S::TX, TY = S::TY, U = S::QW;
     extern __shared__ __align__(128) double smraw[];
@@ -346,6 +360,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constan
     const int gx = th.tx0 + lane;
     const int dx = max(HX - lane, lane - (HX + TX - 1));
     int wdy = 1 << 20;
+    th.mir = ((gx == 0 && (a.bc.m & 1)) ? 1 : 0) | ((gx == a.nx - 1 && (a.bc.m & 2)) ? 2 : 0);
 #pragma unroll
     for (int r = 0; r < RY; ++r) {
         const int ey = th.ey0 + r;
@@ -355,6 +370,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constan
         const int dist = max(dx, dy);
         th.in_dom[r] = gx >= 0 && gx < a.nx && gy >= 0 && gy < a.ny;
         th.in_tile[r] = th.in_dom[r] && dist <= 0;
+        if (gy == 0 && (a.bc.m & 4)) th.mir |= 4 << (2 * r);
+        if (gy == a.ny - 1 && (a.bc.m & 8)) th.mir |= 8 << (2 * r);
         th.col[r] = th.in_dom[r] ? gx + (int64_t)a.nx * gy : 0;
         unsigned msk = 0;
 #pragma unroll
@@ -399,7 +416,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constan
     if (interior) {
         // masked prologue while a level's plane is below the block (t - K < b0), masked
         // epilogue once planes beyond the block appear (t >= b1); unmasked in between.
-        const int pro_end = max(th.t0, th.b0 + K);          // first step that may be unmasked
+        const int pro_end = max(th.t0, th.b0 + K + (NEU ? 1 : 0));   // first unmasked step
         const int epi_beg = min(th.t1 + 1, th.b1);          // first step that must be masked
         const int npro = min(NB, (pro_end - th.t0 + U - 1) / U);
         th.template run_blocks<true>(t, npro);

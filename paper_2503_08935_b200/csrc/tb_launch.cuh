@@ -16,12 +16,12 @@ template <> struct Tile<6> { static constexpr int X = 32, Y = 8; };
 template <> struct Tile<7> { static constexpr int X = 16, Y = 8; };
 template <> struct Tile<8> { static constexpr int X = 16, Y = 8; };
 
-template <int K, int MODE>
+template <int K, int MODE, bool NEU = false>
 bcgs_status launch_tb_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
 {
     constexpr int TX = Tile<K>::X, TY = Tile<K>::Y;
     using S = TbShape<K, TX, TY>;
-    auto kern = k_cheb_tb<K, TX, TY, MODE>;
+    auto kern = k_cheb_tb<K, TX, TY, MODE, NEU>;
     static bool attr = false;
     if (!attr) {
         CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -94,13 +94,13 @@ inline bool make_maps(bcgs_ctx c, TbMaps* maps, const TbArgs& a, int mode, int b
 }
 
 template <int K, int RY, int NW, int NS, int MODE, int MINB = 1, bool XUPD = false,
-          bool XSH = false>
+          bool XSH = false, bool NEU = false>
 bcgs_status launch_tb4_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
 {
     using S = Tb4Shape<K, RY, NW, NS>;
     constexpr size_t smem = S::smem + (XUPD ? S::xupd_bytes : 0);
     static_assert(smem <= 227 * 1024, "tb4 shared memory budget");
-    auto kern = k_cheb_tb4<K, RY, NW, NS, MODE, MINB, XUPD, XSH>;
+    auto kern = k_cheb_tb4<K, RY, NW, NS, MODE, MINB, XUPD, XSH, NEU>;
     static bool attr = false;
     if (!attr) {
         CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -120,6 +120,15 @@ bcgs_status launch_tb4_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
 template <int K, int MODE>
 bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz)
 {
+    // Neumann faces present (R27): the mirror-ghost instantiations (16-warp TMA kernel for
+    // k <= 5, else the square tile); the all-Dirichlet kernels carry no mirror logic
+    if (a.bc.m || a.bc.zlo >= 0 || a.bc.zhi >= 0) {
+        if constexpr (K <= 5) {
+            if (tma_ok(c) && c->tb_variant != 2)
+                return launch_tb4_k<K, 2, 16, 4, MODE, 1, false, false, true>(c, a, nz);
+        }
+        return launch_tb_k<K, MODE, true>(c, a, nz);
+    }
     if constexpr (K <= 5) {   // register budget: warp-row layouts up to K = 5
         if (MODE == MODE_P && c->defer_x)   // deferred a11 fused into the p-kernel (16 warps)
             return launch_tb4_k<K, 2, 16, (K <= 4 ? 4 : 3), MODE, 1, true>(c, a, nz);

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_status_strings():
     lib = bcgs.load()
-    assert lib.bcgs_abi_version() == 1
+    assert lib.bcgs_abi_version() == 2
     assert lib.bcgs_status_string(7) == b"breakdown"
 
 
@@ -61,6 +61,30 @@ def test_chebyshev_constants_equal_oracle(orc, n, nslab, pc, k):
     ref = orc.cheb_setup(a, b, k)
     assert list(cst) == [ref[key] for key in ("theta", "delta", "sigma", "cz", "g1", "A2", "B2")]
     assert np.array_equal(rho, ref["rho"])
+
+
+@pytest.mark.parametrize("faces", [(0, 1, 1, 0, 1, 0), (1, 1, 0, 0, 0, 1), (0, 0, 1, 1, 1, 1)])
+@pytest.mark.parametrize("pc,nslab", [("gnocomm", 1), ("gnocomm", 4), ("bj", 1), ("bj", 2),
+                                      ("bj", 4), ("g", 1)])
+def test_chebyshev_constants_mixed_bc_equal_oracle(orc, faces, pc, nslab):
+    """R27: the library's mixed-BC interval (closed-form mixed spectra, BJ union over the
+    blocks' z factors) and constants are bit-identical to the oracle's."""
+    n3, h = (40, 24, 32), 0.1
+    ivl, cst, rho = bcgs.chebyshev_constants(n3, h, nslab, pc, 6, bc=faces)
+    a, b = orc.pc_interval(n3[::-1], h, nslab, pc, bc=faces)
+    assert (ivl[0], ivl[1]) == (a, b)
+    ref = orc.cheb_setup(a, b, 6)
+    assert list(cst) == [ref[key] for key in ("theta", "delta", "sigma", "cz", "g1", "A2", "B2")]
+    assert np.array_equal(rho, ref["rho"])
+
+
+def test_chebyshev_constants_bc_config_errors():
+    with pytest.raises(bcgs.BcgsError):     # 1-plane blocks next to a Neumann z face
+        bcgs.chebyshev_constants((8, 8, 8), 0.1, 8, "bj", 2, bc=(0, 0, 0, 0, 1, 0))
+    with pytest.raises(bcgs.BcgsError):     # Neumann axis with one point
+        bcgs.chebyshev_constants((1, 8, 8), 0.1, 1, "gnocomm", 2, bc=(1, 0, 0, 0, 0, 0))
+    with pytest.raises(bcgs.BcgsError):     # unknown face kind
+        bcgs.chebyshev_constants((8, 8, 8), 0.1, 1, "gnocomm", 2, bc=(2, 0, 0, 0, 0, 0))
 
 
 def test_chebyshev_constants_reject_bad_interval():
