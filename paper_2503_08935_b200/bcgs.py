@@ -14,7 +14,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libbcgs.so")
+# BCGS_LIB: load another build of the same library (A/B timing of kernel changes)
+LIB_PATH = os.environ.get("BCGS_LIB") or os.path.join(_PKG, "lib", "libbcgs.so")
 
 OK, E_INVALID, E_CONFIG, E_SPECTRUM, E_CUDA, E_NCCL, NOT_CONVERGED, BREAKDOWN, E_STATE = range(9)
 STATUS_NAMES = {0: "ok", 1: "invalid", 2: "config", 3: "spectrum", 4: "cuda", 5: "nccl",

@@ -66,7 +66,11 @@ struct Tb4Shape {
     static constexpr int PAD = EX;
     static constexpr int PLANE = EX * EY + 2 * PAD;       // level plane incl. guard rows
     static constexpr int BOX = EX * EY;                   // staged input box (doubles)
-    static constexpr int QW = ((K + 1 + 2) / 3) * 3 < 3 ? 3 : ((K + 1 + 2) / 3) * 3;
+    // z-ring of the level-0 planes (>= K + 1, multiple of 3 for the phase-unrolled windows);
+    // at least 6 so that, with NS dividing QW / 2, the stage slot, its mbarrier parity and the
+    // level-plane double-buffer parity of a step are compile-time functions of its phase
+    static constexpr int QW = ((K + 1 + 2) / 3) * 3 < 6 ? 6 : ((K + 1 + 2) / 3) * 3;
+    static constexpr bool CT = QW % (2 * NS) == 0;
     static constexpr size_t level_bytes = sizeof(double) * 2 * K * PLANE;
     static constexpr size_t stage_bytes = sizeof(double) * (size_t)NS * 3 * BOX;
     static constexpr size_t smem = level_bytes + stage_bytes + 128;
@@ -79,6 +83,7 @@ struct Tb4Thread {
     using S = Tb4Shape<K, RY, NW, NS>;
     static constexpr int EX = S::EX, TX = S::TX, TY = S::TY, PLANE = S::PLANE, QW = S::QW,
                          BOX = S::BOX;
+    static constexpr bool CT = S::CT;
 
     double qw[QW][RY];
     double win[K > 1 ? K : 2][3][RY];
@@ -88,7 +93,7 @@ struct Tb4Thread {
     double* stg;       // [NS][3][BOX] staged inputs
     uint64_t* bar;     // [NS]
     int lane, ey0, b0, b1, c0, c1, t0, t1, wdy, tx0, ty0;
-    int64_t col[RY], plane;
+    uint32_t col[RY], plane;   // 32-bit element offsets (launcher: slab < 2^32 elements)
     unsigned actmask[RY];
     int mir;           // Neumann mirror bits: 1 x-, 2 x+, 4<<2r y-, 8<<2r y+ (row r)
     bool in_dom[RY], in_tile[RY], first;
@@ -139,16 +144,18 @@ struct Tb4Thread {
 #pragma unroll
                 for (int r = 0; r < RY; ++r)
                     if (in_tile[r])
-                        a->x[col[r] + plane * mx] =
+                        a->x[(size_t)(col[r] + plane * (uint32_t)mx)] =
                             upd_x(xb[r], xb[XN + r], xb[2 * XN + r], alpha, omega);
             }
             xissue(t + 1);
         }
         // ---- level 0 from the TMA stage of plane t
         double q0[RY];
+        // steps run in blocks of QW from t0, so (t - t0) % QW == PH: with CT the stage slot,
+        // its mbarrier phase parity and the level-plane buffer are compile-time
         if (t < b1) {
-            const int s = (t - t0) % NS;
-            mbar_wait(&bar[s], ((t - t0) / NS) & 1);
+            const int s = CT ? PH % NS : (t - t0) % NS;
+            mbar_wait(&bar[s], CT ? (PH / NS) & 1 : ((t - t0) / NS) & 1);
             const double* d = stg + (size_t)s * 3 * BOX + ey0 * EX + lane;
 #pragma unroll
             for (int r = 0; r < RY; ++r) {
@@ -164,7 +171,7 @@ struct Tb4Thread {
                 if (MASK) v = in_dom[r] ? v : 0.0;
                 q0[r] = v;
                 if (MODE != MODE_PLAIN && in_tile[r] && t >= c0 && t < c1)
-                    side[col[r] + plane * t] = v;
+                    side[(size_t)(col[r] + plane * (uint32_t)t)] = v;
             }
         } else {
 #pragma unroll
@@ -172,7 +179,7 @@ struct Tb4Thread {
         }
 #pragma unroll
         for (int r = 0; r < RY; ++r) qw[PH % QW][r] = q0[r];
-        const double* prev = sm + S::PAD + ((t - 1) & 1) * (K * PLANE);
+        const double* prev = sm + S::PAD + (CT ? ((PH + 1) & 1) : ((t - t0 + 1) & 1)) * (K * PLANE);
 #pragma unroll
         for (int j = 1; j <= K; ++j) {
             const int m = t - j;
@@ -230,11 +237,11 @@ struct Tb4Thread {
 #pragma unroll
                 for (int r = 0; r < RY; ++r) {
                     if (j < K) win[j][PH % 3][r] = v[r];
-                    else if (in_tile[r] && m >= c0 && m < c1) a->out[col[r] + plane * m] = v[r];
+                    else if (in_tile[r] && m >= c0 && m < c1) a->out[(size_t)(col[r] + plane * (uint32_t)m)] = v[r];
                 }
             }
         }
-        double* cur = sm + S::PAD + (t & 1) * (K * PLANE) + ey0 * EX + lane;
+        double* cur = sm + S::PAD + (CT ? (PH & 1) : ((t - t0) & 1)) * (K * PLANE) + ey0 * EX + lane;
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
             if (XSH && r > 0 && r < RY - 1) continue;   // shuffles: only segment ends are read
@@ -260,7 +267,7 @@ struct Tb4Thread {
 #pragma unroll
             for (int r = 0; r < RY; ++r) {
                 if (!in_tile[r]) continue;
-                const int64_t e = col[r] + plane * mx;
+                const size_t e = col[r] + plane * (uint32_t)mx;
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(xb + r)),
                              "l"(a->x + e));
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(xb + XN + r)),
@@ -372,7 +379,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constan
         th.in_tile[r] = th.in_dom[r] && dist <= 0;
         if (gy == 0 && (a.bc.m & 4)) th.mir |= 4 << (2 * r);
         if (gy == a.ny - 1 && (a.bc.m & 8)) th.mir |= 8 << (2 * r);
-        th.col[r] = th.in_dom[r] ? gx + (int64_t)a.nx * gy : 0;
+        th.col[r] = th.in_dom[r] ? (uint32_t)(gx + a.nx * gy) : 0u;
         unsigned msk = 0;
 #pragma unroll
         for (int j = 1; j <= K; ++j)
@@ -388,7 +395,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constan
     if (th.c0 >= (a.ext ? a.zo1 : th.b1)) return;
     th.t0 = max(th.b0, th.c0 - K);
     th.t1 = th.c1 - 1 + K;
-    th.plane = (int64_t)a.nx * a.ny;
+    th.plane = (uint32_t)(a.nx * a.ny);
 #pragma unroll
     for (int d = 0; d < S::QW; ++d)
 #pragma unroll

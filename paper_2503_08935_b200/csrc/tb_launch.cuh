@@ -73,7 +73,12 @@ inline bool make_map(CUtensorMap* m, const double* base, int64_t nx, int64_t ny,
            CUDA_SUCCESS;
 }
 
-inline bool tma_ok(bcgs_ctx c) { return encode_fn() != nullptr && c->lay.nx % 2 == 0; }
+// the TMA kernels index a slab field with 32-bit element offsets
+inline bool tma_ok(bcgs_ctx c)
+{
+    const uint64_t elems = (uint64_t)c->lay.nx * c->lay.ny * (c->lay.L + 2 * BCGS_MAX_DEGREE + 2);
+    return encode_fn() != nullptr && c->lay.nx % 2 == 0 && elems < (1ull << 32);
+}
 
 // deferred x update needs the TMA warp-row kernel (K <= 5)
 inline bool defer_x_possible(bcgs_ctx c) { return tma_ok(c) && c->degree >= 1 && c->degree <= 5; }
