@@ -491,8 +491,7 @@ bcgs_status iteration_ref(bcgs_ctx c)
 bcgs_status iteration(bcgs_ctx c)
 {
     if (c->pc == BCGS_PC_CHEB_G && c->nranks > 1) return iteration_ref(c);   // k-deep halos
-    if (c->kernels == 1 && fused::supported(c->lay.nx, c->lay.ny, c->lay.L, c->bpr, c->degree,
-                                            c->pc != BCGS_PC_NONE))
+    if (c->kernels == 1 && fused::supported(c, c->degree, c->pc != BCGS_PC_NONE))
         return fused::iteration(c);
     return iteration_ref(c);
 }
@@ -783,6 +782,7 @@ bcgs_status bcgs_set_option(bcgs_ctx c, int32_t option, int64_t value)
     case BCGS_OPT_DEFER_X: c->defer_x_opt = (int)value; break;
     case BCGS_OPT_STENCIL_CFG: c->stencil_cfg = (int)value; break;
     case BCGS_OPT_XCONC: c->xconc_opt = (int)value; break;
+    case BCGS_OPT_MULTIPASS: c->mp_min = std::max<int>(4, (int)value); break;
     default: return fail(c, BCGS_E_INVALID, "unknown option %d", option);
     }
     drop_graph(c);

@@ -41,7 +41,7 @@ inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 struct Layout {
     int64_t nx, ny, nz, L, plane, vec_elems;   // vec_elems = (L + 2) * plane
     int64_t n_part;
-    size_t off_vec[17];
+    size_t off_vec[18];
     int64_t ext_elems;
     size_t off_ext[3];
     size_t off_state, off_hist, off_scal, off_part, off_rank, off_gath, total;
@@ -49,7 +49,8 @@ struct Layout {
 
 constexpr int V_X = 0, V_R = 1, V_RT = 2, V_P = 3, V_PH = 4, V_RH = 5, V_W = 6, V_T = 7,
               V_B = 8, V_C1 = 9, V_C2 = 10, V_IO = 11, V_W2 = 12, V_P2 = 13,
-              V_S = 14, V_PH2 = 15, V_COUNT = 16;
+              V_S = 14, V_PH2 = 15, V_Y3 = 16, V_Y4 = 17, V_COUNT = 18;
+// V_C1, V_C2, V_Y3, V_Y4: Chebyshev iterates (reference sweeps; multi-pass buffer pairs)
 
 inline int64_t stencil_blocks(int64_t nx, int64_t ny, int64_t L)
 {
@@ -150,6 +151,7 @@ struct bcgs_ctx_s {
     cudaStream_t s_x = nullptr;       // low-priority stream of the concurrent x update
     cudaEvent_t ev_omega = nullptr, ev_xdone = nullptr;              // BCGS_OPT_DEFER_X (measured slower at 512^3: off)
     int kernels = 1, use_graph = 1, profile = 0, poll = 8, tb_variant = 7;
+    int mp_min = 4;   // multi-pass temporal blocking for degree > mp_min (BCGS_OPT_MULTIPASS)
     // preconditioner
     bcgs_pc pc = BCGS_PC_NONE;
     int degree = 0, bpr = 1;

@@ -61,6 +61,11 @@ bcgs_status launch_tb(bcgs_ctx c, TbArgs& a)
     a.g1 = c->cst[4];
     a.A2 = c->cst[5];
     a.B2 = c->cst[6];
+    // multi-pass: above the one-pass range, and by default from k = 5 on (measured faster
+    // than the one-pass square-tile kernel); variant 2 keeps the square tile
+    if (!a.ext && multipass_ok(c) &&
+        (k > KMAX_TB || (k > c->mp_min && c->tb_variant != 2)))
+        return launch_multipass(c, a, MODE);
     for (int j = 0; j <= k; ++j) a.rho[j] = c->rho[j];
     // z-chunking: each chunk re-computes ~2k warm-up/drain planes; more chunks fill the 148
     // SMs (one CTA per SM) more evenly.  Pick the chunk count minimising
@@ -120,7 +125,7 @@ bcgs_status precond_g_tb(bcgs_ctx c, const double* E, double* out, int v0, int v
 
 bool precond_supported(bcgs_ctx c)
 {
-    return c->pc != BCGS_PC_NONE && c->degree >= 1 && c->degree <= KMAX_TB;
+    return supported(c, c->degree, c->pc != BCGS_PC_NONE);
 }
 
 bcgs_status precond_apply(bcgs_ctx c, const double* q, double* out)
@@ -139,7 +144,7 @@ void on_begin(bcgs_ctx c)
     const bool g_multi = c->pc == BCGS_PC_CHEB_G && c->nranks > 1;   // ref path (k-deep halos)
     c->xconc = (c->xconc_opt && !g_multi && c->kernels == 1 && c->pc != BCGS_PC_NONE &&
                 (c->lay.nx % 2) == 0 && !c->defer_x_opt &&
-                supported(c->lay.nx, c->lay.ny, c->lay.L, c->bpr, c->degree, true)) ? 1 : 0;
+                c->degree <= KMAX_TB && supported(c, c->degree, true)) ? 1 : 0;
     if (c->xconc) {   // s_x starts after the setup (x = x0 written on s)
         cudaEventRecord(c->ev_omega, c->s);
         cudaStreamWaitEvent(c->s_x, c->ev_omega, 0);
@@ -147,7 +152,7 @@ void on_begin(bcgs_ctx c)
     }
     const bool neu = c->mbc.m || c->mbc.zlo >= 0 || c->mbc.zhi >= 0;
     c->defer_x = (c->defer_x_opt && !g_multi && !neu && c->kernels == 1 &&
-                  c->pc != BCGS_PC_NONE && (c->lay.nx % 2) == 0 &&
+                  c->pc != BCGS_PC_NONE && (c->lay.nx % 2) == 0 && c->degree <= c->mp_min &&
                   defer_x_ok(c)) ? 1 : 0;
 }
 

@@ -11,7 +11,10 @@
 //   MODE_PLAIN: q = input field                                   (apply_preconditioner)
 //   MODE_P:     q = p_i = r + β (p_{i-1} - ω w)   (KernelBiCGS6) -> also stored
 //   MODE_S:     q = s   = r - α w                 (KernelBiCGS2) -> also stored
-// so the vector update costs no extra pass.  Every point is evaluated with exactly the
+// so the vector update costs no extra pass.  Degrees above KMAX_TB run as several passes of
+// the TMA kernel (k_tb4.cuh): a pass applies sweeps j0..j0+KB-1 of the same recurrence,
+//   MODE_C:     level 0 = x_{j0-1} (stencil operand), with q and x_{j0-2} read at the centre
+// and writes the last two levels (out2 = level KB-1) for the next pass.  Every point is evaluated with exactly the
 // expression tree of the reference kernels (R17, R18, R20) -> bitwise identical results.
 #pragma once
 #include <stdint.h>
@@ -22,7 +25,7 @@
 
 namespace fused {
 
-constexpr int MODE_PLAIN = 0, MODE_P = 1, MODE_S = 2;
+constexpr int MODE_PLAIN = 0, MODE_P = 1, MODE_S = 2, MODE_C = 3;
 constexpr int KMAX_TB = 8;
 
 struct TbArgs {
@@ -33,7 +36,11 @@ struct TbArgs {
     const double* p_b;
     double* side_a;       // MODE_P: output p_i = parity ? side_a : side_b (the other buffer)
     double* side_b;       // MODE_S: side_a = s
-    double* out;          // level-K output: M^-1 q
+    double* out;          // level-K output: M^-1 q (multi-pass: x_{j0+KB-1})
+    double* out2;         // multi-pass (O2): level KB-1 output x_{j0+KB-2}
+    // MODE_C: q = input field (qsel = 0) or the p buffer the p-kernel of this iteration
+    // wrote (qsel = 1: selected by the iteration parity like side_a/side_b)
+    int qsel;
     double* x;            // MODE_P + XUPD: x_{i-1} += α p̂_{i-1} + ω r̂_{i-1} (deferred a11)
     const double* rh;     //   r̂ of the previous iteration
     int nx, ny, Lb, zch, nchunk;
@@ -43,7 +50,7 @@ struct TbArgs {
     // Neumann faces (R27): x/y bits and the planes whose z-/z+ neighbour is mirrored
     ref::MirrorBc bc;
     double h2inv, cz, g1, A2, B2;
-    double rho[KMAX_TB + 1];
+    double rho[KMAX_TB + 1];   // multi-pass: rho[i] = ρ_{j0-1+i}, i = 0..KB
     const DevState* st;
 };
 
@@ -268,9 +275,10 @@ inline int64_t max_blocks(int64_t nx, int64_t ny, int64_t L)
     // worst case over the stencil launch configurations (x pairs / 32, rows / 4, planes / 4)
     return ((nx / 2 + 31) / 32) * ((ny + 3) / 4) * ((L + 3) / 4 + 2);   // + 2 boundary launches
 }
-inline bool supported(int64_t, int64_t, int64_t, int, int degree, bool has_pc)
+bool multipass_ok(bcgs_ctx c);   // tb_multi.cu
+inline bool supported(bcgs_ctx c, int degree, bool has_pc)
 {
-    return has_pc && degree >= 1 && degree <= KMAX_TB;
+    return has_pc && degree >= 1 && (degree <= KMAX_TB || multipass_ok(c));
 }
 bcgs_status iteration(bcgs_ctx c);
 void on_begin(bcgs_ctx c);

@@ -78,15 +78,17 @@ struct Tb4Shape {
 };
 
 template <int K, int RY, int NW, int NS, int MODE, bool XUPD = false, bool XSH = false,
-          bool NEU = false>
+          bool NEU = false, bool O2 = false>
 struct Tb4Thread {
     using S = Tb4Shape<K, RY, NW, NS>;
     static constexpr int EX = S::EX, TX = S::TX, TY = S::TY, PLANE = S::PLANE, QW = S::QW,
                          BOX = S::BOX;
     static constexpr bool CT = S::CT;
 
-    double qw[QW][RY];
+    double qw[QW][RY];                   // level 0 (q; MODE_C: x_{j0-1})
     double win[K > 1 ? K : 2][3][RY];
+    double qr[MODE == MODE_C ? QW : 1][RY];   // MODE_C: q ring (centre values)
+    double y2c[RY];                      // MODE_C: x_{j0-2} at plane t-1
     const TbArgs* a;
     const TbMaps* maps;
     double* sm;        // level planes
@@ -103,7 +105,7 @@ struct Tb4Thread {
     bool xdo;          // XUPD: this launch applies the previous iteration's x update
     double* xsm;       // XUPD: [2][3][XN] cp.async landing buffers
 
-    static constexpr int ninputs() { return MODE == MODE_PLAIN ? 1 : (MODE == MODE_P ? 3 : 2); }
+    static constexpr int ninputs() { return MODE == MODE_PLAIN ? 1 : (MODE == MODE_S ? 2 : 3); }
 
     __device__ __forceinline__ void issue(int tt)
     {   // thread 0: stage the level-0 operands of plane tt
@@ -122,6 +124,11 @@ struct Tb4Thread {
                 tma_load_3d(d + BOX, &maps->r, tx0, ty0, tt, &bar[s]);
                 tma_load_3d(d + 2 * BOX, &maps->w, tx0, ty0, tt, &bar[s]);
             }
+        } else if (MODE == MODE_C) {   // x_{j0-1}, q, x_{j0-2}
+            mbar_expect_tx(&bar[s], 3 * BOX * 8);
+            tma_load_3d(d, &maps->q, tx0, ty0, tt, &bar[s]);
+            tma_load_3d(d + BOX, pmap, tx0, ty0, tt, &bar[s]);
+            tma_load_3d(d + 2 * BOX, &maps->w, tx0, ty0, tt, &bar[s]);
         } else {
             mbar_expect_tx(&bar[s], 2 * BOX * 8);
             tma_load_3d(d + BOX, &maps->r, tx0, ty0, tt, &bar[s]);
@@ -150,7 +157,7 @@ struct Tb4Thread {
             xissue(t + 1);
         }
         // ---- level 0 from the TMA stage of plane t
-        double q0[RY];
+        double q0[RY], qn[RY], y2n[RY];
         // steps run in blocks of QW from t0, so (t - t0) % QW == PH: with CT the stage slot,
         // its mbarrier phase parity and the level-plane buffer are compile-time
         if (t < b1) {
@@ -162,6 +169,14 @@ struct Tb4Thread {
                 double v;
                 if (MODE == MODE_PLAIN) {
                     v = d[r * EX];
+                } else if (MODE == MODE_C) {
+                    v = d[r * EX];
+                    qn[r] = d[BOX + r * EX];
+                    y2n[r] = d[2 * BOX + r * EX];
+                    if (MASK) {
+                        qn[r] = in_dom[r] ? qn[r] : 0.0;
+                        y2n[r] = in_dom[r] ? y2n[r] : 0.0;
+                    }
                 } else if (MODE == MODE_P) {
                     const double pv = d[r * EX];
                     v = first ? pv : upd_p(d[BOX + r * EX], pv, d[2 * BOX + r * EX], beta, omega);
@@ -170,15 +185,18 @@ struct Tb4Thread {
                 }
                 if (MASK) v = in_dom[r] ? v : 0.0;
                 q0[r] = v;
-                if (MODE != MODE_PLAIN && in_tile[r] && t >= c0 && t < c1)
+                if ((MODE == MODE_P || MODE == MODE_S) && in_tile[r] && t >= c0 && t < c1)
                     side[(size_t)(col[r] + plane * (uint32_t)t)] = v;
             }
         } else {
 #pragma unroll
-            for (int r = 0; r < RY; ++r) q0[r] = 0.0;
+            for (int r = 0; r < RY; ++r) q0[r] = qn[r] = y2n[r] = 0.0;
         }
 #pragma unroll
-        for (int r = 0; r < RY; ++r) qw[PH % QW][r] = q0[r];
+        for (int r = 0; r < RY; ++r) {
+            qw[PH % QW][r] = q0[r];
+            if (MODE == MODE_C) qr[PH % QW][r] = qn[r];
+        }
         const double* prev = sm + S::PAD + (CT ? ((PH + 1) & 1) : ((t - t0 + 1) & 1)) * (K * PLANE);
 #pragma unroll
         for (int j = 1; j <= K; ++j) {
@@ -223,12 +241,18 @@ struct Tb4Thread {
                         if (m == a->bc.zhi) zp = zm;
                     }
                     const double Sv = stencil_row(zc, xm, xp, yc_m, yc_p, zm, zp, a->h2inv);
-                    const double qc = qw[(PH + QW - j) % QW][r];
+                    const double qc = MODE == MODE_C ? qr[(PH + QW - j) % QW][r]
+                                                     : qw[(PH + QW - j) % QW][r];
                     double vv;
-                    if (j == 1) {
+                    if (j == 1 && MODE == MODE_C) {        // sweep j0: x_{j0-2} at the centre
+                        vv = cheb_step(qc, Sv, zc, y2c[r], a->rho[1], a->rho[0], a->A2, a->B2);
+                    } else if (j == 1) {
                         vv = cheb_first(qc, Sv, a->g1, a->cz);
                     } else {
-                        const double z2 = (j == 2) ? qc * a->cz : win[j - 2][(PH + 1) % 3][r];
+                        // x_{j-2} at the centre: x_0 = q/θ (first pass), level 0 (MODE_C)
+                        const double z2 = (j == 2) ? (MODE == MODE_C ? qw[(PH + QW - 2) % QW][r]
+                                                                     : qc * a->cz)
+                                                   : win[j - 2][(PH + 1) % 3][r];
                         vv = cheb_step(qc, Sv, zc, z2, a->rho[j], a->rho[j - 1], a->A2, a->B2);
                     }
                     if (MASK) vv = (((actmask[r] >> j) & 1u) && mok) ? vv : 0.0;
@@ -238,8 +262,14 @@ struct Tb4Thread {
                 for (int r = 0; r < RY; ++r) {
                     if (j < K) win[j][PH % 3][r] = v[r];
                     else if (in_tile[r] && m >= c0 && m < c1) a->out[(size_t)(col[r] + plane * (uint32_t)m)] = v[r];
+                    if (O2 && j == K - 1 && in_tile[r] && m >= c0 && m < c1)
+                        a->out2[(size_t)(col[r] + plane * (uint32_t)m)] = v[r];
                 }
             }
+        }
+        if (MODE == MODE_C) {
+#pragma unroll
+            for (int r = 0; r < RY; ++r) y2c[r] = y2n[r];
         }
         double* cur = sm + S::PAD + (CT ? (PH & 1) : ((t - t0) & 1)) * (K * PLANE) + ey0 * EX + lane;
 #pragma unroll
@@ -320,11 +350,11 @@ struct Tb4Thread {
 };
 
 template <int K, int RY, int NW, int NS, int MODE, int MINB = 1, bool XUPD = false,
-          bool XSH = false, bool NEU = false>
+          bool XSH = false, bool NEU = false, bool O2 = false>
 __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constant__ TbArgs a,
                                                        const __grid_constant__ TbMaps maps)
 {
-    using T = Tb4Thread<K, RY, NW, NS, MODE, XUPD, XSH, NEU>;
+    using T = Tb4Thread<K, RY, NW, NS, MODE, XUPD, XSH, NEU, O2>;
     using S = Tb4Shape<K, RY, NW, NS>;
     constexpr int TX = S::TX, TY = S::TY, U = S::QW;
     extern __shared__ __align__(128) double smraw[];
@@ -357,6 +387,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constan
     } else if (MODE == MODE_S) {
         th.alpha = st->alpha;
         th.side = a.side_a;
+    } else if (MODE == MODE_C) {   // q: fixed input, or this iteration's p (parity buffer)
+        const bool odd = st && (st->iter & 1);
+        th.pmap = !a.qsel ? &maps.r : odd ? &maps.pa : &maps.pb;
     }
     const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
     th.lane = lane;
@@ -399,7 +432,12 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constan
 #pragma unroll
     for (int d = 0; d < S::QW; ++d)
 #pragma unroll
-        for (int r = 0; r < RY; ++r) th.qw[d][r] = 0.0;
+        for (int r = 0; r < RY; ++r) {
+            th.qw[d][r] = 0.0;
+            if (MODE == MODE_C) th.qr[d][r] = 0.0;
+        }
+#pragma unroll
+    for (int r = 0; r < RY; ++r) th.y2c[r] = 0.0;
 #pragma unroll
     for (int j = 0; j < (K > 1 ? K : 2); ++j)
 #pragma unroll

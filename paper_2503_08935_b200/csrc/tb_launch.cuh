@@ -90,6 +90,14 @@ inline bool make_maps(bcgs_ctx c, TbMaps* maps, const TbArgs& a, int mode, int b
     const int64_t nx = c->lay.nx, ny = c->lay.ny;
     const int64_t L = a.ext ? c->lay.L + 2 * (int64_t)BCGS_MAX_DEGREE : c->lay.L;
     if (mode == MODE_PLAIN) return make_map(&maps->q, a.q, nx, ny, L, box_y, box_x);
+    if (mode == MODE_C) {   // x_{j0-1} -> q, x_{j0-2} -> w, q: r (fixed) or pa/pb (qsel)
+        bool ok = make_map(&maps->q, a.q, nx, ny, L, box_y, box_x) &&
+                  make_map(&maps->w, a.w, nx, ny, L, box_y, box_x);
+        if (a.qsel)
+            return ok && make_map(&maps->pa, a.p_a, nx, ny, L, box_y, box_x) &&
+                   make_map(&maps->pb, a.p_b, nx, ny, L, box_y, box_x);
+        return ok && make_map(&maps->r, a.r, nx, ny, L, box_y, box_x);
+    }
     bool ok = make_map(&maps->r, a.r, nx, ny, L, box_y, box_x) &&
               make_map(&maps->w, a.w, nx, ny, L, box_y, box_x);
     if (mode == MODE_P)
@@ -99,13 +107,13 @@ inline bool make_maps(bcgs_ctx c, TbMaps* maps, const TbArgs& a, int mode, int b
 }
 
 template <int K, int RY, int NW, int NS, int MODE, int MINB = 1, bool XUPD = false,
-          bool XSH = false, bool NEU = false>
+          bool XSH = false, bool NEU = false, bool O2 = false>
 bcgs_status launch_tb4_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
 {
     using S = Tb4Shape<K, RY, NW, NS>;
     constexpr size_t smem = S::smem + (XUPD ? S::xupd_bytes : 0);
     static_assert(smem <= 227 * 1024, "tb4 shared memory budget");
-    auto kern = k_cheb_tb4<K, RY, NW, NS, MODE, MINB, XUPD, XSH, NEU>;
+    auto kern = k_cheb_tb4<K, RY, NW, NS, MODE, MINB, XUPD, XSH, NEU, O2>;
     static bool attr = false;
     if (!attr) {
         CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

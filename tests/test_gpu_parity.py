@@ -261,6 +261,7 @@ def test_deferred_x_update_parity(bc, orc, n, pc, k, bpr):
     h = si.unit_cube_h(n3[0])
     s = bc.Solver(n3, h)
     s.set_option(bc.OPT_DEFER_X, 1)
+    s.set_option(bc.OPT_MULTIPASS, 8)     # k = 5: the one-pass kernel carries the deferred x
     s.set_preconditioner(pc, k, blocks_per_rank=bpr)
     s.set_rhs_random(si.SEED)
     rep = s.solve(tol=1e-8)

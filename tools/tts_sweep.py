@@ -1,0 +1,59 @@
+"""Time to solution on one GPU (SURVEY §8(d) 'Sweep' and C4 rows): iterations and seconds to a
+1e-8 relative residual at n^3 for GNoComm(CI) k x c_min, BJ(CI) vs GNoComm on P-slab block
+decompositions (blocks_per_rank = P on one GPU = the P-rank preconditioner), and G(CI).
+Prints one JSON object per solve.  python tools/tts_sweep.py --n 512"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import synth_inputs as si  # noqa: E402
+from paper_2503_08935_b200 import bcgs  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=512)
+ap.add_argument("--tol", type=float, default=1e-8)
+ap.add_argument("--degrees", default="2,4,8,16,24")
+ap.add_argument("--cmins", default="1,10,100")
+ap.add_argument("--slabs", default="1,8")
+ap.add_argument("--c4", action="store_true", help="BJ vs GNoComm at P = 1,2,4,8 (k = 4)")
+ap.add_argument("--sweep", action="store_true")
+a = ap.parse_args()
+n = a.n
+h = si.unit_cube_h(n)
+
+
+def run(pc, k, bpr, c_min=10.0):
+    s = bcgs.Solver(n, h)
+    s.set_preconditioner(pc, k, c_min=c_min, blocks_per_rank=bpr)
+    s.set_rhs_random(si.SEED)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rep = s.solve(tol=a.tol, max_iter=5000)
+    wall = time.perf_counter() - t0
+    it = rep["iterations"]
+    out = {"n": n, "pc": pc, "k": k, "c_min": c_min, "slabs": bpr, "iterations": it,
+           "status": rep["status_name"], "seconds": round(rep["seconds"], 4),
+           "wall_s": round(wall, 4), "ms_per_iter": round(1e3 * rep["seconds"] / max(it, 1), 3),
+           "stencils_per_iter": 2 * k + 2, "rel_residual": rep["rel_residual"],
+           "true_rel_residual": rep["true_rel_residual"]}
+    print(json.dumps(out), flush=True)
+    s.close()
+
+
+run("gnocomm", 4, 1)      # warm-up (graph capture, module load) -- also a data point
+if a.sweep:
+    for bpr in [int(x) for x in a.slabs.split(",")]:
+        for k in [int(x) for x in a.degrees.split(",")]:
+            for cm in [float(x) for x in a.cmins.split(",")]:
+                run("gnocomm", k, bpr, cm)
+if a.c4:
+    for bpr in (1, 2, 4, 8):
+        run("bj", 4, bpr)
+        run("gnocomm", 4, bpr)
+    run("g", 4, 1)
+    run("none", 0, 1)
