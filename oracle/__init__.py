@@ -76,6 +76,14 @@ def lib() -> ctypes.CDLL:
         _lib.orc_bicgstab_bc.argtypes = [i64, i64, i64, f64, i64, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_int, f64, f64, f64, f64, P, P, f64,
                                          ctypes.c_int, ctypes.c_int, P, P, P, P, P]
+        _lib.orc_bicgstab_ex.restype = ctypes.c_int
+        _lib.orc_bicgstab_ex.argtypes = [i64, i64, i64, f64, i64, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_int, f64, f64, f64, f64, f64, ctypes.c_int,
+                                         P, P, f64, ctypes.c_int, ctypes.c_int, P, P, P, P, P,
+                                         P]
+        _lib.orc_apply_inner.restype = ctypes.c_longlong
+        _lib.orc_apply_inner.argtypes = [i64, i64, i64, f64, i64, ctypes.c_int, f64,
+                                         ctypes.c_int, P, P]
         _lib.orc_bicgstab.restype = ctypes.c_int
         _lib.orc_bicgstab.argtypes = [i64, i64, i64, f64, i64, ctypes.c_int, ctypes.c_int,
                                       f64, f64, f64, f64, P, P, f64, ctypes.c_int,
@@ -211,7 +219,9 @@ def apply_cheb(q: np.ndarray, h: float, nslab: int, k: int, a: float, b: float,
     return out
 
 
-PC = {"none": 0, "gnocomm": 1, "bj": 2, "g": 3}
+PC = {"none": 0, "gnocomm": 1, "bj": 2, "g": 3, "bj_bicgs": 4, "g_bicgs": 5}
+# inner-Krylov preconditioners: default inner settings of the paper
+INNER_DEFAULT = {"bj_bicgs": (1e-6, 500), "g_bicgs": (1e-2, 500)}
 STATUS = {0: "ok", 1: "config", 6: "not_converged", 7: "breakdown"}
 
 
@@ -226,11 +236,30 @@ class Result:
     extra: dict = field(default_factory=dict)
 
 
+def apply_inner(q: np.ndarray, h: float, nslab: int, tol: float, max_it: int,
+                bc=None) -> tuple[np.ndarray, int]:
+    """One BJ(BiCGS) application: inner unpreconditioned Bi-CGSTAB on each of the
+    nslab z-blocks.  Returns (M^{-1} q, total inner iterations)."""
+    q = np.ascontiguousarray(q, np.float64)
+    nx, ny, nz = _shape(q.shape)
+    out = np.empty_like(q)
+    tot = lib().orc_apply_inner(nx, ny, nz, h, nslab, bc_mask(bc), tol, max_it, _ptr(q),
+                                _ptr(out))
+    return out, int(tot)
+
+
 def bicgstab(b: np.ndarray, h: float, *, pc: str = "none", k: int = 4, nslab: int = 1,
              c_min: float = 10.0, c_max: float = 1.0 - 1e-4, bounds_override=None,
              x0: np.ndarray | None = None, tol: float = 1e-8, max_it: int = 5000,
-             fixed_it: int = 0, bc=None) -> Result:
-    """Alg. 3 (P:264-308) with M = I, GNoComm(CI) or BJ(CI) on `nslab` z-slabs."""
+             fixed_it: int = 0, bc=None, inner_tol: float | None = None,
+             inner_max: int | None = None) -> Result:
+    """Alg. 3 (P:264-308) with M = I, GNoComm(CI), BJ(CI), G(CI) on `nslab` z-slabs, or the
+    inner-Krylov BJ(BiCGS) / G(BiCGS) (inner_tol / inner_max default to P:393-394's values;
+    Result.extra["inner_iterations"] = total inner iterations)."""
+    dt, dm = INNER_DEFAULT.get(pc, (0.0, 0))
+    inner_tol = dt if inner_tol is None else inner_tol
+    inner_max = dm if inner_max is None else inner_max
+    tot = ctypes.c_longlong(0)
     b = np.ascontiguousarray(b, np.float64)
     nx, ny, nz = _shape(b.shape)
     cap = (fixed_it if fixed_it > 0 else max_it)
@@ -244,10 +273,11 @@ def bicgstab(b: np.ndarray, h: float, *, pc: str = "none", k: int = 4, nslab: in
     if x0 is not None:
         x0 = np.ascontiguousarray(x0, np.float64)
         x0p = _ptr(x0)
-    st = lib().orc_bicgstab_bc(nx, ny, nz, h, nslab, bc_mask(bc), PC[pc], k, c_min, c_max,
-                               lmin, lmax,
-                            _ptr(b), x0p, tol, max_it, fixed_it, _ptr(x), _ptr(hist),
-                            _ptr(scal), ctypes.byref(it), ctypes.byref(tr))
+    st = lib().orc_bicgstab_ex(nx, ny, nz, h, nslab, bc_mask(bc), PC[pc], k, c_min, c_max,
+                               lmin, lmax, inner_tol, inner_max,
+                               _ptr(b), x0p, tol, max_it, fixed_it, _ptr(x), _ptr(hist),
+                               _ptr(scal), ctypes.byref(it), ctypes.byref(tr),
+                               ctypes.byref(tot))
     n = it.value
     return Result(STATUS.get(st, str(st)), n, x, hist[: n + 1].copy(), scal[:n].copy(),
-                  float(tr.value))
+                  float(tr.value), {"inner_iterations": int(tot.value)})

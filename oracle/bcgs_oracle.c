@@ -387,6 +387,41 @@ void orc_pc_interval(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab
 }
 
 /* ------------------------------------------------------------------------------------------
+ * Inner-Krylov preconditioners: FBiCGS-BJ(BiCGS) and FBiCGS-G(BiCGS),
+ * P:176-207.  M_i^{-1} p is computed "as a solution of the linear system
+ * (R_s A R_s^T) p̂_s = p_s" on every subdomain s (Eq. 15) by "the already available
+ * BiCGS method": the unpreconditioned Alg. 3 below (M = I) on the block, x0 = 0,
+ * relative tolerance tol_in, at most max_in iterations (1e-6 / 500 for BJ(BiCGS),
+ * 1e-2 / 500 for G(BiCGS) = one block spanning the whole domain).  The block operator has
+ * zero ghosts at the cuts (Eq. 12-14) and keeps the physical faces (a Neumann z face only in
+ * the first / last block).  Reading (paper silent): the inner result is used whatever the
+ * inner status (converged, breakdown or iteration cap).  The outer solver is flexible
+ * because Alg. 3 stores p̂ and r̂.
+ * ---------------------------------------------------------------------------------------- */
+int orc_bicgstab_ex(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, int bcm,
+                    int pc, int k, double c_min, double c_max, double lmin_ov, double lmax_ov,
+                    double tol_in, int max_in, const double* b, const double* x0, double tol,
+                    int max_it, int fixed_it, double* x, double* hist, double* scal,
+                    int* iters_out, double* true_rel, long long* inner_total);
+
+static void apply_inner_bicgs(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab,
+                              int bcm, double tol_in, int max_in, const double* q, double* out,
+                              long long* inner_total)
+{
+    int64_t Lb = nz / nslab, pl = nx * ny;
+    double* hist = (double*)malloc(sizeof(double) * (size_t)(max_in + 1));
+    for (int64_t s = 0; s < nslab; ++s) {
+        int bcm_s = (bcm & 15) | (s == 0 ? (bcm & 16) : 0) | (s == nslab - 1 ? (bcm & 32) : 0);
+        int its = 0;
+        orc_bicgstab_ex(nx, ny, Lb, h, 1, bcm_s, 0, 0, 0.0, 0.0, 0.0, 0.0, 0.0, 0,
+                        q + s * Lb * pl, NULL, tol_in, max_in, 0, out + s * Lb * pl, hist,
+                        NULL, &its, NULL, NULL);
+        if (inner_total) *inner_total += its;
+    }
+    free(hist);
+}
+
+/* ------------------------------------------------------------------------------------------
  * Preconditioned Bi-CGSTAB, Alg. 3, Alg. 1 for the scalar forms.
  *
  * pc: 0 = none (M = I), 1 = GNoComm(CI), 2 = BJ(CI), 3 = G(CI).
@@ -408,10 +443,11 @@ void orc_pc_interval(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab
  * *iters_out = number of completed iterations (each appended one entry to hist); a
  * breakdown at r~ᵀw ends the run before iteration i appends anything (iters = i-1).
  * ---------------------------------------------------------------------------------------- */
-int orc_bicgstab_bc(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, int bcm,
+int orc_bicgstab_ex(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, int bcm,
                     int pc, int k, double c_min, double c_max, double lmin_ov, double lmax_ov,
-                    const double* b, const double* x0, double tol, int max_it, int fixed_it,
-                    double* x, double* hist, double* scal, int* iters_out, double* true_rel)
+                    double tol_in, int max_in, const double* b, const double* x0, double tol,
+                    int max_it, int fixed_it, double* x, double* hist, double* scal,
+                    int* iters_out, double* true_rel, long long* inner_total)
 {
     int64_t n = nx * ny * nz, pl = nx * ny;
     if (nslab < 1 || nz % nslab != 0) return 1;
@@ -431,9 +467,13 @@ int orc_bicgstab_bc(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab,
             a_iv = iv[0]; b_iv = iv[1];
         }
         if (!(a_iv < b_iv) || !(a_iv > 0.0)) return 1;
+    } else if (pc == 4 || pc == 5) {           /* BJ(BiCGS) / G(BiCGS) */
+        if (!(tol_in > 0.0) || max_in < 1) return 1;
     } else if (pc != 0) {
         return 1;
     }
+    /* pc 5 = G(BiCGS): one inner solve over the whole domain (no block cuts) */
+    const int64_t nslab_in = (pc == 5) ? 1 : nslab;
     int max_run = fixed_it > 0 ? fixed_it : max_it;
 
     double* r = (double*)calloc((size_t)n, sizeof(double));
@@ -477,6 +517,8 @@ int orc_bicgstab_bc(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab,
         double* sc = scal ? scal + 8 * (i - 1) : NULL;
         /* line 6: solve M p̂ = p */
         if (pc == 0) memcpy(ph, p, sizeof(double) * (size_t)n);
+        else if (pc >= 4) apply_inner_bicgs(nx, ny, nz, h, nslab_in, bcm, tol_in, max_in, p, ph,
+                                            inner_total);
         else orc_apply_cheb_bc(nx, ny, nz, h, nslab_pc, bcm, k, a_iv, b_iv, p, ph);
         /* MPI1 + KernelBiCGS1: w = A p̂ (global), local r~ᵀw; MPI2 */
         orc_apply_A_bc(nx, ny, nz, h, 1, bcm, ph, w);
@@ -490,6 +532,8 @@ int orc_bicgstab_bc(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab,
         for (int64_t c = 0; c < n; ++c) r[c] = fma(-alpha, w[c], r[c]);
         /* solve M r̂ = r */
         if (pc == 0) memcpy(rh, r, sizeof(double) * (size_t)n);
+        else if (pc >= 4) apply_inner_bicgs(nx, ny, nz, h, nslab_in, bcm, tol_in, max_in, r, rh,
+                                            inner_total);
         else orc_apply_cheb_bc(nx, ny, nz, h, nslab_pc, bcm, k, a_iv, b_iv, r, rh);
         /* MPI3 + KernelBiCGS3: t = A r̂, tᵀr, tᵀt; MPI4 */
         orc_apply_A_bc(nx, ny, nz, h, 1, bcm, rh, t);
@@ -537,6 +581,26 @@ done:
     }
     free(r); free(rt); free(p); free(ph); free(rh); free(w); free(t); free(tmp);
     return status;
+}
+
+/* One application of the inner-Krylov preconditioner: out = M^{-1} q on nslab blocks.
+ * Returns the total number of inner iterations. */
+long long orc_apply_inner(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, int bcm,
+                          double tol_in, int max_in, const double* q, double* out)
+{
+    long long tot = 0;
+    apply_inner_bicgs(nx, ny, nz, h, nslab, bcm, tol_in, max_in, q, out, &tot);
+    return tot;
+}
+
+int orc_bicgstab_bc(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, int bcm,
+                    int pc, int k, double c_min, double c_max, double lmin_ov, double lmax_ov,
+                    const double* b, const double* x0, double tol, int max_it, int fixed_it,
+                    double* x, double* hist, double* scal, int* iters_out, double* true_rel)
+{
+    return orc_bicgstab_ex(nx, ny, nz, h, nslab, bcm, pc, k, c_min, c_max, lmin_ov, lmax_ov,
+                           0.0, 0, b, x0, tol, max_it, fixed_it, x, hist, scal, iters_out,
+                           true_rel, NULL);
 }
 
 int orc_bicgstab(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, int pc, int k,
