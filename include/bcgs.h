@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define BCGS_ABI_VERSION 2
+#define BCGS_ABI_VERSION 3
 #define BCGS_MAX_DEGREE 64       /* Chebyshev degree k (sweeps per application) cap      */
 #define BCGS_HIST_CAP 16384      /* max outer iterations recorded per solve              */
 
@@ -71,10 +71,16 @@ typedef enum {
                                /* the global Eq. 9-11 bounds rescaled by (c_min, c_max)    */
     BCGS_PC_CHEB_BJ = 2,       /* BJ(CI): Chebyshev on each slab block with the    */
                                /* exact local-block bounds (R10)                           */
-    BCGS_PC_CHEB_G = 3         /* G(CI): Chebyshev on the GLOBAL operator with */
+    BCGS_PC_CHEB_G = 3,        /* G(CI): Chebyshev on the GLOBAL operator with */
                                /* the rescaled global bounds; multi-rank: one k-deep halo  */
                                /* exchange per application instead of Alg. 4's per-sweep   */
                                /* MPI2 (requires k <= L); blocks_per_rank is ignored       */
+    BCGS_PC_BJ_BICGS = 4,      /* BJ(BiCGS) (Eq. 15): inner unpreconditioned    */
+                               /* Bi-CGSTAB on every slab block (zero ghosts at the cuts), */
+                               /* x0 = 0, default tol 1e-6 / 500 iterations; the   */
+                               /* outer Alg. 3 is flexible.  degree is ignored     */
+    BCGS_PC_G_BICGS = 5        /* G(BiCGS): the inner solve on the whole       */
+                               /* domain, default tol 1e-2 / 500; nranks == 1 only */
 } bcgs_pc;
 
 typedef enum { BCGS_MEM_DEVICE = 0, BCGS_MEM_HOST = 1 } bcgs_mem;
@@ -175,6 +181,14 @@ bcgs_status bcgs_set_initial_guess(bcgs_ctx ctx, const double* x0, int32_t mem);
  * GNoComm (R9), blocks_per_rank >= 1 with L % blocks_per_rank == 0. */
 bcgs_status bcgs_set_preconditioner(bcgs_ctx ctx, bcgs_pc pc, int32_t degree, double c_min,
                                     double c_max, int32_t blocks_per_rank);
+/* Inner solver of BJ(BiCGS) / G(BiCGS): relative tolerance and iteration cap of every inner
+ * solve (set after bcgs_set_preconditioner, which restores the paper's defaults).  The
+ * inner result is used whatever the inner status (R29).  Inner solves run on the library's
+ * stream through private contexts (workspaces allocated and owned by the library) and
+ * synchronise the host, so these preconditioners are not graph-captured. */
+bcgs_status bcgs_set_inner_solver(bcgs_ctx ctx, double rel_tol, int32_t max_iter);
+/* Total inner iterations since the last bcgs_begin (Table II "it. / outer it."). */
+int64_t bcgs_inner_iterations(bcgs_ctx ctx);
 /* Override the Chebyshev interval [a', b'] (0 < a' < b'); (0, 0) restores the default. */
 bcgs_status bcgs_set_eigen_bounds(bcgs_ctx ctx, double a, double b);
 

@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("BCGS_LIB") or os.path.join(_PKG, "lib", "libbcgs.so")
 OK, E_INVALID, E_CONFIG, E_SPECTRUM, E_CUDA, E_NCCL, NOT_CONVERGED, BREAKDOWN, E_STATE = range(9)
 STATUS_NAMES = {0: "ok", 1: "invalid", 2: "config", 3: "spectrum", 4: "cuda", 5: "nccl",
                 6: "not_converged", 7: "breakdown", 8: "state"}
-PC = {"none": 0, "gnocomm": 1, "bj": 2, "g": 3}
+PC = {"none": 0, "gnocomm": 1, "bj": 2, "g": 3, "bj_bicgs": 4, "g_bicgs": 5}
 MEM_DEVICE, MEM_HOST = 0, 1
 OPT_KERNELS, OPT_GRAPH, OPT_PROFILE, OPT_POLL, OPT_TB_VARIANT, OPT_DEFER_X = 0, 1, 2, 3, 4, 5
 OPT_STENCIL_CFG, OPT_XCONC, OPT_MULTIPASS = 6, 7, 8
@@ -38,7 +38,7 @@ EXPORTS = [
     "bcgs_join",
     "bcgs_residual_history", "bcgs_scalar_history", "bcgs_get_solution",
     "bcgs_apply_operator", "bcgs_apply_preconditioner", "bcgs_dot", "bcgs_kernel_times",
-    "bcgs_kernel_times_reset",
+    "bcgs_kernel_times_reset", "bcgs_set_inner_solver", "bcgs_inner_iterations",
 ]
 
 
@@ -112,6 +112,8 @@ def load() -> ctypes.CDLL:
         "bcgs_dot": (i32, [P, P, P, P]),
         "bcgs_kernel_times": (i32, [P, ctypes.c_char_p, i32, P, P, P, i32]),
         "bcgs_kernel_times_reset": (None, [P]),
+        "bcgs_set_inner_solver": (i32, [P, f64, i32]),
+        "bcgs_inner_iterations": (i64, [P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -246,6 +248,14 @@ class Solver:
         self._check(self.lib.bcgs_set_preconditioner(self.ctx, PC[pc], degree, c_min, c_max,
                                                      blocks_per_rank),
                     "bcgs_set_preconditioner")
+
+    def set_inner_solver(self, tol: float, max_iter: int = 500):
+        """BJ(BiCGS) / G(BiCGS): inner relative tolerance and iteration cap."""
+        self._check(self.lib.bcgs_set_inner_solver(self.ctx, tol, max_iter),
+                    "bcgs_set_inner_solver")
+
+    def inner_iterations(self) -> int:
+        return int(self.lib.bcgs_inner_iterations(self.ctx))
 
     def set_eigen_bounds(self, a: float, b: float):
         self._check(self.lib.bcgs_set_eigen_bounds(self.ctx, a, b), "bcgs_set_eigen_bounds")

@@ -387,10 +387,13 @@ bcgs_status precond_g(bcgs_ctx c, const double* q, double* out, const DevState* 
     return BCGS_OK;
 }
 
+bcgs_status precond_inner(bcgs_ctx c, const double* q, double* out, const DevState* st);
+
 bcgs_status precond_ref(bcgs_ctx c, const double* q, double* out, const DevState* st)
 {
     const int64_t n = npts(c);
     const int k = c->degree;
+    if (inner_pc(c)) return precond_inner(c, q, out, st);
     if (c->pc == BCGS_PC_CHEB_G && c->nranks > 1) return precond_g(c, q, out, st);
     if (c->pc == BCGS_PC_NONE) {
         Prof pf(c, KC_PRECOND, 16.0 * n);
@@ -500,7 +503,8 @@ bcgs_status enqueue_iterations(bcgs_ctx c, int n)
 {
     // graphs: single rank only (multi-rank runs launch directly; NCCL inside captured graphs
     // is supported but not exercised in round 1)
-    if (c->use_graph && !c->profile && !c->lg && c->nranks == 1 && !c->xconc) {
+    // (inner-Krylov preconditioners synchronise the host inside an iteration: no graph)
+    if (c->use_graph && !c->profile && !c->lg && c->nranks == 1 && !c->xconc && !inner_pc(c)) {
         if (!c->gexec) {
             cudaGraph_t graph;
             CUDA_OK(c, cudaStreamBeginCapture(c->s, cudaStreamCaptureModeThreadLocal));
@@ -516,6 +520,17 @@ bcgs_status enqueue_iterations(bcgs_ctx c, int n)
     }
     for (int i = 0; i < n; ++i) TRY(iteration(c));
     return BCGS_OK;
+}
+
+// destroy the private inner-solver contexts of BJ(BiCGS) / G(BiCGS) and free their memory
+void drop_inner(bcgs_ctx c)
+{
+    for (int k = 0; k < 4; ++k) {
+        if (c->inner[k]) bcgs_destroy(c->inner[k]);
+        if (c->inner_ws[k]) cudaFree(c->inner_ws[k]);
+        c->inner[k] = nullptr;
+        c->inner_ws[k] = nullptr;
+    }
 }
 
 void drop_graph(bcgs_ctx c)
@@ -575,7 +590,7 @@ bcgs_status validate_pc(bcgs_ctx c)
 {
     bcgs_grid_desc g{{c->lay.nx, c->lay.ny, c->lay.nz}, c->h, {0, 0, 0, 0, 0, 0}};
     memcpy(g.bc, c->bc, sizeof g.bc);
-    if (c->pc == BCGS_PC_NONE) return BCGS_OK;
+    if (c->pc == BCGS_PC_NONE || inner_pc(c)) return BCGS_OK;
     bcgs_status s = cheb_constants(&g, c->nranks * c->bpr, c->pc, c->degree, c->c_min, c->c_max,
                                    c->ov_a, c->ov_b, c->ivl, c->cst, c->rho);
     if (s != BCGS_OK)
@@ -742,6 +757,7 @@ void bcgs_destroy(bcgs_ctx c)
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->s) cudaStreamSynchronize(c->s);
+    drop_inner(c);
     harvest(c);
     drop_graph(c);
     for (auto e : c->free_ev) cudaEventDestroy(e);
@@ -837,8 +853,16 @@ bcgs_status bcgs_set_preconditioner(bcgs_ctx c, bcgs_pc pc, int32_t degree, doub
 {
     if (!c) return BCGS_E_INVALID;
     if (pc != BCGS_PC_NONE && pc != BCGS_PC_CHEB_GNOCOMM && pc != BCGS_PC_CHEB_BJ &&
-        pc != BCGS_PC_CHEB_G)
+        pc != BCGS_PC_CHEB_G && pc != BCGS_PC_BJ_BICGS && pc != BCGS_PC_G_BICGS)
         return fail(c, BCGS_E_INVALID, "unknown preconditioner %d", (int)pc);
+    drop_inner(c);
+    if (pc == BCGS_PC_BJ_BICGS || pc == BCGS_PC_G_BICGS) {   // P:393-394 defaults
+        if (pc == BCGS_PC_G_BICGS && (c->nranks > 1 || c->lg))
+            return fail(c, BCGS_E_CONFIG, "G(BiCGS) spans ranks: not built (nranks must be 1)");
+        degree = 0;
+        c->in_tol = pc == BCGS_PC_G_BICGS ? 1e-2 : 1e-6;
+        c->in_max = 500;
+    }
     if (degree < 0 || degree > BCGS_MAX_DEGREE)
         return fail(c, BCGS_E_INVALID, "degree %d outside [0, %d]", degree, BCGS_MAX_DEGREE);
     if (blocks_per_rank < 1 || c->lay.L % blocks_per_rank)
@@ -846,7 +870,7 @@ bcgs_status bcgs_set_preconditioner(bcgs_ctx c, bcgs_pc pc, int32_t degree, doub
                     (long long)c->lay.L, blocks_per_rank);
     if ((c->bc[4] || c->bc[5]) && pc != BCGS_PC_CHEB_G && c->lay.L / blocks_per_rank < 2)
         return fail(c, BCGS_E_CONFIG, "a Neumann z face needs >= 2 planes per block");
-    if (pc == BCGS_PC_CHEB_G) {
+    if (pc == BCGS_PC_CHEB_G || pc == BCGS_PC_G_BICGS) {
         blocks_per_rank = 1;   // the global operator has no block cuts
         if (c->nranks > 1 && degree > c->lay.L)
             return fail(c, BCGS_E_CONFIG, "G(CI) needs degree %d <= slab thickness %lld",
@@ -861,6 +885,19 @@ bcgs_status bcgs_set_preconditioner(bcgs_ctx c, bcgs_pc pc, int32_t degree, doub
     c->begun = 0;
     return validate_pc(c);
 }
+
+bcgs_status bcgs_set_inner_solver(bcgs_ctx c, double rel_tol, int32_t max_iter)
+{
+    if (!c) return BCGS_E_INVALID;
+    if (!(rel_tol > 0.0) || max_iter < 1 || max_iter > BCGS_HIST_CAP)
+        return fail(c, BCGS_E_INVALID, "inner solver: need tol > 0, 1 <= max_iter <= %d",
+                    BCGS_HIST_CAP);
+    c->in_tol = rel_tol;
+    c->in_max = max_iter;
+    return BCGS_OK;
+}
+
+int64_t bcgs_inner_iterations(bcgs_ctx c) { return c ? c->in_iters : -1; }
 
 bcgs_status bcgs_set_eigen_bounds(bcgs_ctx c, double a, double b)
 {
@@ -885,6 +922,7 @@ bcgs_status bcgs_begin(bcgs_ctx c, double rel_tol, int32_t max_iter, int32_t fix
     const int64_t n = npts(c);
     const size_t bytes = sizeof(double) * (size_t)n;
     k_init_state<<<1, 1, 0, c->s>>>(c->st, rel_tol, max_iter, fixed_iters);
+    c->in_iters = 0;
     // Alg. 3 l.1-4: r0 = b - A x0; r~ = r0; p0 = r0; ρ0 = r~ᵀr0
     if (c->have_x0) {
         TRY(halo(c, F(c, V_X)));
@@ -990,7 +1028,7 @@ bcgs_status bcgs_solve(bcgs_ctx c, double rel_tol, int32_t max_iter, int32_t fix
         int32_t done = 0, iter = 0;
         TRY(poll_state(c, &done, &iter));
         while (done == DONE_RUNNING && c->launched < max_iter) {
-            int batch = std::min(c->poll, max_iter - c->launched);
+            int batch = std::min(inner_pc(c) ? 1 : c->poll, max_iter - c->launched);
             TRY(bcgs_iterate(c, batch));
             TRY(poll_state(c, &done, &iter));
         }
@@ -1124,3 +1162,77 @@ void bcgs_kernel_times_reset(bcgs_ctx c)
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ inner-Krylov preconditioners
+// BJ(BiCGS) / G(BiCGS) (R29): M^-1 q = on every block s the result of an inner,
+// unpreconditioned Bi-CGSTAB (the same Alg. 3 driver, M = I) on (R_s A R_s^T) p̂_s = q_s
+// (Eq. 15), x0 = 0, relative tolerance in_tol, at most in_max iterations; the inner result is
+// used whatever the inner status.  The inner problem is a private context over one block
+// (zero Dirichlet ghosts at the cuts, the physical faces kept; a Neumann z face only in the
+// first / last block of the global decomposition), created on first use on the library's
+// stream with a workspace the library allocates; its reductions are GPU-local (no NCCL:
+// BJ(BiCGS) is "communication-free").
+namespace {
+
+bcgs_status inner_ctx(bcgs_ctx c, int key, bcgs_ctx* out)
+{
+    if (!c->inner[key]) {
+        const int nb = c->pc == BCGS_PC_G_BICGS ? 1 : c->bpr;
+        bcgs_grid_desc g{};
+        g.n[0] = c->lay.nx;
+        g.n[1] = c->lay.ny;
+        g.n[2] = c->lay.L / nb;
+        g.h = c->h;
+        for (int f = 0; f < 4; ++f) g.bc[f] = c->bc[f];
+        g.bc[4] = (key & 1) ? BCGS_BC_NEUMANN : BCGS_BC_DIRICHLET;
+        g.bc[5] = (key & 2) ? BCGS_BC_NEUMANN : BCGS_BC_DIRICHLET;
+        const size_t bytes = bcgs_workspace_bytes(&g, 1);
+        if (!bytes) return fail(c, BCGS_E_CONFIG, "inner solver: invalid block grid");
+        void* ws = nullptr;
+        CUDA_OK(c, cudaMalloc(&ws, bytes));
+        bcgs_ctx ic = nullptr;
+        bcgs_status st = create_ctx(&g, 0, 1, nullptr, nullptr, c->device, ws, bytes, c->s, &ic);
+        if (st != BCGS_OK) {
+            std::string e = ic ? ic->err : "";
+            if (ic) bcgs_destroy(ic);
+            cudaFree(ws);
+            return fail(c, st, "inner solver context: %s", e.c_str());
+        }
+        c->inner[key] = ic;
+        c->inner_ws[key] = ws;
+    }
+    *out = c->inner[key];
+    return BCGS_OK;
+}
+
+bcgs_status precond_inner(bcgs_ctx c, const double* q, double* out, const DevState* st)
+{
+    if (st) {   // an outer stop earlier in this iteration (breakdown at α): nothing to do
+        CUDA_OK(c, cudaMemcpyAsync(c->h_pinned, &st->done, sizeof(int32_t),
+                                   cudaMemcpyDeviceToHost, c->s));
+        CUDA_OK(c, cudaStreamSynchronize(c->s));
+        if (((int32_t*)c->h_pinned)[0] != DONE_RUNNING) return BCGS_OK;
+    }
+    Prof pf(c, KC_PRECOND, 0.0);
+    const int nb = c->pc == BCGS_PC_G_BICGS ? 1 : c->bpr;
+    const int64_t blk = (c->lay.L / nb) * c->lay.plane;
+    const int total = c->nranks * nb;
+    for (int s = 0; s < nb; ++s) {
+        const int gb = c->rank * nb + s;
+        const int key = ((c->bc[4] && gb == 0) ? 1 : 0) | ((c->bc[5] && gb == total - 1) ? 2 : 0);
+        bcgs_ctx ic = nullptr;
+        TRY(inner_ctx(c, key, &ic));
+        bcgs_status e = bcgs_set_rhs(ic, q + s * blk, BCGS_MEM_DEVICE);
+        if (e != BCGS_OK) return fail(c, e, "inner set_rhs: %s", ic->err.c_str());
+        bcgs_report rep{};
+        e = bcgs_solve(ic, c->in_tol, c->in_max, 0, &rep);
+        if (e != BCGS_OK && e != BCGS_NOT_CONVERGED && e != BCGS_BREAKDOWN)
+            return fail(c, e, "inner solve: %s", ic->err.c_str());
+        c->in_iters += rep.iterations;
+        e = bcgs_get_solution(ic, out + s * blk, BCGS_MEM_DEVICE);
+        if (e != BCGS_OK) return fail(c, e, "inner get_solution: %s", ic->err.c_str());
+    }
+    return BCGS_OK;
+}
+
+}  // namespace

@@ -157,6 +157,13 @@ struct bcgs_ctx_s {
     int degree = 0, bpr = 1;
     double c_min = 10.0, c_max = 1.0 - 1e-4, ov_a = 0.0, ov_b = 0.0;
     double ivl[2] = {0, 0}, cst[7] = {}, rho[BCGS_MAX_DEGREE + 2] = {};
+    // inner-Krylov preconditioners BJ(BiCGS) / G(BiCGS) (R29): private unpreconditioned
+    // contexts over one block, keyed by the block's Neumann z faces (bit 0 z-, bit 1 z+)
+    double in_tol = 1e-6;
+    int in_max = 500;
+    int64_t in_iters = 0;
+    bcgs_ctx_s* inner[4] = {};
+    void* inner_ws[4] = {};
     int have_x0 = 0;
     double face[6] = {0, 0, 0, 0, 0, 0};
     // solve bookkeeping
@@ -207,6 +214,7 @@ inline bcgs_status fail(bcgs_ctx c, bcgs_status s, const char* fmt, ...)
     } while (0)
 
 inline double* F(bcgs_ctx c, int v) { return c->vec[v]; }
+inline bool inner_pc(bcgs_ctx c) { return c->pc == BCGS_PC_BJ_BICGS || c->pc == BCGS_PC_G_BICGS; }
 inline int64_t npts(bcgs_ctx c) { return c->lay.L * c->lay.plane; }
 
 #define TRY(x)                        \

@@ -22,25 +22,36 @@ ap.add_argument("--cmins", default="1,10,100")
 ap.add_argument("--slabs", default="1,8")
 ap.add_argument("--c4", action="store_true", help="BJ vs GNoComm at P = 1,2,4,8 (k = 4)")
 ap.add_argument("--sweep", action="store_true")
+ap.add_argument("--table2", action="store_true",
+                help="Table II analogue (P:425-437): the paper's §IV problem, tol 1e-10, every "
+                     "preconditioner, BJ variants on --slabs-bj blocks")
+ap.add_argument("--slabs-bj", type=int, default=8)
 a = ap.parse_args()
 n = a.n
 h = si.unit_cube_h(n)
 
 
-def run(pc, k, bpr, c_min=10.0):
-    s = bcgs.Solver(n, h)
-    s.set_preconditioner(pc, k, c_min=c_min, blocks_per_rank=bpr)
-    s.set_rhs_random(si.SEED)
+def run(pc, k, bpr, c_min=10.0, paper=False):
+    if paper:   # §IV workload: mixed faces, smooth RHS, relative tol 1e-10
+        f, hp, faces = si.paper_problem(n)
+        s = bcgs.Solver(n, hp, bc=faces)
+        s.set_preconditioner(pc, k, c_min=c_min, blocks_per_rank=bpr)
+        s.set_rhs(torch.from_numpy(f).cuda())
+    else:
+        s = bcgs.Solver(n, h)
+        s.set_preconditioner(pc, k, c_min=c_min, blocks_per_rank=bpr)
+        s.set_rhs_random(si.SEED)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    rep = s.solve(tol=a.tol, max_iter=5000)
+    rep = s.solve(tol=1e-10 if paper else a.tol, max_iter=5000)
     wall = time.perf_counter() - t0
     it = rep["iterations"]
     out = {"n": n, "pc": pc, "k": k, "c_min": c_min, "slabs": bpr, "iterations": it,
            "status": rep["status_name"], "seconds": round(rep["seconds"], 4),
            "wall_s": round(wall, 4), "ms_per_iter": round(1e3 * rep["seconds"] / max(it, 1), 3),
            "stencils_per_iter": 2 * k + 2, "rel_residual": rep["rel_residual"],
-           "true_rel_residual": rep["true_rel_residual"]}
+           "true_rel_residual": rep["true_rel_residual"], "workload": "paper" if paper else
+           "random", "inner_iterations": s.inner_iterations()}
     print(json.dumps(out), flush=True)
     s.close()
 
@@ -51,6 +62,11 @@ if a.sweep:
         for k in [int(x) for x in a.degrees.split(",")]:
             for cm in [float(x) for x in a.cmins.split(",")]:
                 run("gnocomm", k, bpr, cm)
+if a.table2:   # P:393-397 settings: CI k = 24 with (100, 1-1e-4); BiCGS inner 1e-2 / 1e-6
+    P = a.slabs_bj
+    for pc, k, bpr in (("none", 0, 1), ("g_bicgs", 0, 1), ("bj_bicgs", 0, P), ("bj", 24, P),
+                       ("g", 24, 1), ("gnocomm", 24, P), ("gnocomm", 24, 1)):
+        run(pc, k, bpr, c_min=100.0, paper=True)
 if a.c4:
     for bpr in (1, 2, 4, 8):
         run("bj", 4, bpr)
