@@ -213,7 +213,7 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    total = args.warmup + 2 * args.steps
+    total = args.warmup + (5 if world > 1 else 2) * args.steps
     clocks = ClockSampler(local)
     clocks.start()
     s.begin(fixed_iters=total)
@@ -242,9 +242,26 @@ def main():
     clk = clocks.stop()
     ktimes = s.kernel_times()
     s.set_option(bcgs.OPT_PROFILE, 0)
+    comm = None
+    if world > 1:
+        # exposed halo / reduction share by ablation: the same K iterations with
+        # the face halos (bit 0) and / or the cross-rank reductions (bit 1) skipped.  The maths
+        # is wrong while ablated; the timing is right.  Max over ranks like the headline.
+        abl = {}
+        for bits in (1, 2, 3):
+            s.set_option(bcgs.OPT_ABLATE, bits)
+            abl[bits] = max_over_ranks(timed(args.steps, 0), dist, dev)
+        s.set_option(bcgs.OPT_ABLATE, 0)
+    rep = s.finish()
     rep = s.finish()
     ms_iter = max_over_ranks(ms_iter, dist, dev)
     ms_iter_prof = max_over_ranks(ms_iter_prof, dist, dev)
+    if world > 1:
+        comm = {"ms_full": ms_iter, "ms_no_halo": abl[1], "ms_no_reductions": abl[2],
+                "ms_no_comm": abl[3], "halo_share": 1.0 - abl[1] / ms_iter,
+                "reduction_share": 1.0 - abl[2] / ms_iter, "comm_share": 1.0 - abl[3] / ms_iter,
+                "method": "ablation: BCGS_OPT_ABLATE skips the face halos (1) / the cross-rank "
+                          "Dot2 all-gathers (2) / both (3); share = 1 - T_ablated / T_full"}
 
     its = 1000.0 / ms_iter
     gdof = n ** 3 * its / 1e9
@@ -329,6 +346,7 @@ def main():
                                    "achieved_gbs": iter_gbs, "peak_gbs": peak,
                                    "frac": iter_gbs / peak},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "comm": comm,
             "kernel_ms_per_step": {kk: v["ms"] / args.steps for kk, v in ktimes.items()},
             "ms_per_step_profiled_pass": ms_iter_prof,
             "clocks": clk, "report": {kk: rep[kk] for kk in ("iterations", "rel_residual",

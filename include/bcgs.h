@@ -99,10 +99,14 @@ typedef enum {
     BCGS_OPT_DEFER_X = 5,      /* 1 = apply x += αp̂ + ωr̂ inside the next p-kernel (off)    */
     BCGS_OPT_STENCIL_CFG = 6,  /* stencil+dot launch configuration 0..4 (tuning)          */
     BCGS_OPT_XCONC = 7,        /* 1 = x update on a concurrent low-priority stream (off)  */
-    BCGS_OPT_MULTIPASS = 8     /* multi-pass temporal blocking (passes of 2..4 sweeps) for */
+    BCGS_OPT_MULTIPASS = 8,    /* multi-pass temporal blocking (passes of 2..4 sweeps) for */
                                /* degree > value (default 4; clamped to >= 4).  Degrees   */
                                /* above 8 always run multi-pass when the TMA kernels can  */
                                /* (nx even).  Bitwise the same result either way.         */
+    BCGS_OPT_ABLATE = 9,       /* comm ablation for timing the exposed halo / reduction     */
+                               /* share: bit 0 skips the face halos, bit 1  */
+                               /* the cross-rank reductions (each rank uses its own pairs).*/
+                               /* The maths is WRONG while set; 0 = off (default)          */
 } bcgs_option;
 
 /* Boundary condition kind of a physical face (Eq. 4 / Eq. 5). */

@@ -225,7 +225,7 @@ bcgs_status local_exchange_end(bcgs_ctx c, bool all, cudaStream_t hs)
 
 bcgs_status halo_on(bcgs_ctx c, double* v, cudaStream_t hs)
 {
-    if (c->nranks == 1) return BCGS_OK;
+    if (c->nranks == 1 || (c->ablate & 1)) return BCGS_OK;   // ablation: timing only
     Prof pf(c, KC_HALO, 0.0, hs);
     const size_t pl = (size_t)c->lay.plane;
     if (c->lg) {
@@ -264,6 +264,12 @@ bcgs_status halo(bcgs_ctx c, double* v) { return halo_on(c, v, c->s); }
 bcgs_status allgather_pairs(bcgs_ctx c, int nd)
 {
     Prof pf(c, KC_ALLGATHER, 0.0);
+    if (c->ablate & 2) {   // ablation (timing only): every slot = this rank's pairs, no comm
+        for (int r = 0; r < c->nranks; ++r)
+            CUDA_OK(c, cudaMemcpyAsync(c->gath + (size_t)r * nd, c->rank_out, nd * sizeof(dd),
+                                       cudaMemcpyDeviceToDevice, c->s));
+        return BCGS_OK;
+    }
     if (c->lg) {
         TRY(local_exchange_begin(c, c->s));
         for (int r = 0; r < c->nranks; ++r) {
@@ -525,12 +531,12 @@ bcgs_status enqueue_iterations(bcgs_ctx c, int n)
 // destroy the private inner-solver contexts of BJ(BiCGS) / G(BiCGS) and free their memory
 void drop_inner(bcgs_ctx c)
 {
-    for (int k = 0; k < 4; ++k) {
+    for (size_t k = 0; k < c->inner.size(); ++k) {
         if (c->inner[k]) bcgs_destroy(c->inner[k]);
         if (c->inner_ws[k]) cudaFree(c->inner_ws[k]);
-        c->inner[k] = nullptr;
-        c->inner_ws[k] = nullptr;
     }
+    c->inner.clear();
+    c->inner_ws.clear();
 }
 
 void drop_graph(bcgs_ctx c)
@@ -799,6 +805,7 @@ bcgs_status bcgs_set_option(bcgs_ctx c, int32_t option, int64_t value)
     case BCGS_OPT_STENCIL_CFG: c->stencil_cfg = (int)value; break;
     case BCGS_OPT_XCONC: c->xconc_opt = (int)value; break;
     case BCGS_OPT_MULTIPASS: c->mp_min = std::max<int>(4, (int)value); break;
+    case BCGS_OPT_ABLATE: c->ablate = (int)(value & 3); break;
     default: return fail(c, BCGS_E_INVALID, "unknown option %d", option);
     }
     drop_graph(c);
@@ -1167,16 +1174,21 @@ void bcgs_kernel_times_reset(bcgs_ctx c)
 // BJ(BiCGS) / G(BiCGS) (R29): M^-1 q = on every block s the result of an inner,
 // unpreconditioned Bi-CGSTAB (the same Alg. 3 driver, M = I) on (R_s A R_s^T) p̂_s = q_s
 // (Eq. 15), x0 = 0, relative tolerance in_tol, at most in_max iterations; the inner result is
-// used whatever the inner status.  The inner problem is a private context over one block
-// (zero Dirichlet ghosts at the cuts, the physical faces kept; a Neumann z face only in the
-// first / last block of the global decomposition), created on first use on the library's
-// stream with a workspace the library allocates; its reductions are GPU-local (no NCCL:
-// BJ(BiCGS) is "communication-free").
+// used whatever the inner status.  Each block's inner problem is a private context (zero
+// Dirichlet ghosts at the cuts, the physical faces kept; a Neumann z face only in the first /
+// last block of the global decomposition) created on first use, with a workspace the library
+// allocates and its own stream: the blocks' inner solves run concurrently, each polled
+// separately.  Their reductions are GPU-local (no NCCL: BJ(BiCGS) is "communication-free",
+// P:207).
 namespace {
 
-bcgs_status inner_ctx(bcgs_ctx c, int key, bcgs_ctx* out)
+bcgs_status inner_ctx(bcgs_ctx c, int s, int key, bcgs_ctx* out)
 {
-    if (!c->inner[key]) {
+    if ((int)c->inner.size() <= s) {
+        c->inner.resize(s + 1, nullptr);
+        c->inner_ws.resize(s + 1, nullptr);
+    }
+    if (!c->inner[s]) {
         const int nb = c->pc == BCGS_PC_G_BICGS ? 1 : c->bpr;
         bcgs_grid_desc g{};
         g.n[0] = c->lay.nx;
@@ -1198,10 +1210,10 @@ bcgs_status inner_ctx(bcgs_ctx c, int key, bcgs_ctx* out)
             cudaFree(ws);
             return fail(c, st, "inner solver context: %s", e.c_str());
         }
-        c->inner[key] = ic;
-        c->inner_ws[key] = ws;
+        c->inner[s] = ic;
+        c->inner_ws[s] = ws;
     }
-    *out = c->inner[key];
+    *out = c->inner[s];
     return BCGS_OK;
 }
 
@@ -1217,20 +1229,41 @@ bcgs_status precond_inner(bcgs_ctx c, const double* q, double* out, const DevSta
     const int nb = c->pc == BCGS_PC_G_BICGS ? 1 : c->bpr;
     const int64_t blk = (c->lay.L / nb) * c->lay.plane;
     const int total = c->nranks * nb;
+    std::vector<bcgs_ctx> ics(nb, nullptr);
+    // start every block's solve (bcgs_solve split into begin / iterate / poll / finish)
     for (int s = 0; s < nb; ++s) {
         const int gb = c->rank * nb + s;
         const int key = ((c->bc[4] && gb == 0) ? 1 : 0) | ((c->bc[5] && gb == total - 1) ? 2 : 0);
-        bcgs_ctx ic = nullptr;
-        TRY(inner_ctx(c, key, &ic));
+        TRY(inner_ctx(c, s, key, &ics[s]));
+        bcgs_ctx ic = ics[s];
         bcgs_status e = bcgs_set_rhs(ic, q + s * blk, BCGS_MEM_DEVICE);
-        if (e != BCGS_OK) return fail(c, e, "inner set_rhs: %s", ic->err.c_str());
-        bcgs_report rep{};
-        e = bcgs_solve(ic, c->in_tol, c->in_max, 0, &rep);
-        if (e != BCGS_OK && e != BCGS_NOT_CONVERGED && e != BCGS_BREAKDOWN)
-            return fail(c, e, "inner solve: %s", ic->err.c_str());
-        c->in_iters += rep.iterations;
-        e = bcgs_get_solution(ic, out + s * blk, BCGS_MEM_DEVICE);
-        if (e != BCGS_OK) return fail(c, e, "inner get_solution: %s", ic->err.c_str());
+        if (e == BCGS_OK) e = bcgs_begin(ic, c->in_tol, c->in_max, 0);
+        if (e != BCGS_OK) return fail(c, e, "inner solve: %s", ic->err.c_str());
+    }
+    std::vector<char> active(nb, 1);
+    int left = nb;
+    while (left > 0) {
+        for (int s = 0; s < nb; ++s) {
+            if (!active[s]) continue;
+            bcgs_ctx ic = ics[s];
+            int32_t done = 0, iter = 0;
+            bcgs_status e = poll_state(ic, &done, &iter);
+            if (e != BCGS_OK) return fail(c, e, "inner poll: %s", ic->err.c_str());
+            if (done == DONE_RUNNING && ic->launched < c->in_max) {
+                e = bcgs_iterate(ic, std::min(ic->poll, c->in_max - ic->launched));
+                if (e != BCGS_OK) return fail(c, e, "inner iterate: %s", ic->err.c_str());
+                continue;
+            }
+            bcgs_report rep{};
+            e = bcgs_finish(ic, &rep);
+            if (e != BCGS_OK && e != BCGS_NOT_CONVERGED && e != BCGS_BREAKDOWN)
+                return fail(c, e, "inner finish: %s", ic->err.c_str());
+            c->in_iters += rep.iterations;
+            e = bcgs_get_solution(ic, out + s * blk, BCGS_MEM_DEVICE);
+            if (e != BCGS_OK) return fail(c, e, "inner get_solution: %s", ic->err.c_str());
+            active[s] = 0;
+            --left;
+        }
     }
     return BCGS_OK;
 }

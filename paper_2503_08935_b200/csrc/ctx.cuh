@@ -151,19 +151,20 @@ struct bcgs_ctx_s {
     cudaStream_t s_x = nullptr;       // low-priority stream of the concurrent x update
     cudaEvent_t ev_omega = nullptr, ev_xdone = nullptr;              // BCGS_OPT_DEFER_X (measured slower at 512^3: off)
     int kernels = 1, use_graph = 1, profile = 0, poll = 8, tb_variant = 7;
+    int ablate = 0;   // BCGS_OPT_ABLATE: 1 skip halos, 2 skip cross-rank reductions (timing)
     int mp_min = 4;   // multi-pass temporal blocking for degree > mp_min (BCGS_OPT_MULTIPASS)
     // preconditioner
     bcgs_pc pc = BCGS_PC_NONE;
     int degree = 0, bpr = 1;
     double c_min = 10.0, c_max = 1.0 - 1e-4, ov_a = 0.0, ov_b = 0.0;
     double ivl[2] = {0, 0}, cst[7] = {}, rho[BCGS_MAX_DEGREE + 2] = {};
-    // inner-Krylov preconditioners BJ(BiCGS) / G(BiCGS) (R29): private unpreconditioned
-    // contexts over one block, keyed by the block's Neumann z faces (bit 0 z-, bit 1 z+)
+    // inner-Krylov preconditioners BJ(BiCGS) / G(BiCGS) (R29): one private unpreconditioned
+    // context per block (solved concurrently, each on its own stream)
     double in_tol = 1e-6;
     int in_max = 500;
     int64_t in_iters = 0;
-    bcgs_ctx_s* inner[4] = {};
-    void* inner_ws[4] = {};
+    std::vector<bcgs_ctx_s*> inner;
+    std::vector<void*> inner_ws;
     int have_x0 = 0;
     double face[6] = {0, 0, 0, 0, 0, 0};
     // solve bookkeeping

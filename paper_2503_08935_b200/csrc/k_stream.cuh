@@ -36,6 +36,10 @@ __global__ void __launch_bounds__(SBX * SBY) k_stencil2_dot(const double* __rest
     const int k0 = kb + blockIdx.z * SZC, k1 = min(ke, k0 + SZC);
     constexpr int NDA = (ND > 0) ? ND : 1;
     double p[NDA] = {}, s[NDA] = {};
+    // ND == 2: second accumulator pair per dot for the odd x point -- two independent Dot2
+    // chains (ILP, 0.70 -> 0.67 ms at 512^3); merged before the block reduction (Dot2 is
+    // order-insensitive, R19)
+    double p2[NDA] = {}, s2[NDA] = {};
     if (i < nx && j < ny) {
         const int64_t plane = (int64_t)nx * ny;
         int64_t c = i + (int64_t)nx * j + plane * k0;
@@ -59,19 +63,23 @@ __global__ void __launch_bounds__(SBX * SBY) k_stencil2_dot(const double* __rest
             o.x = stencil_row(zc.x, xm, zc.y, ym.x, yp.x, zmk.x, zpk.x, h2inv);
             o.y = stencil_row(zc.y, zc.x, xp, ym.y, yp.y, zmk.y, zpk.y, h2inv);
             *reinterpret_cast<double2*>(out + c) = o;
-            if (ND >= 1) {
+            if (ND >= 1) {   // ND == 1: one chain measured faster (0.53 vs 0.58 ms at 512^3)
                 dot2_acc(p[0], s[0], av.x, o.x);
-                dot2_acc(p[0], s[0], av.y, o.y);
+                if (ND >= 2) dot2_acc(p2[0], s2[0], av.y, o.y);
+                else dot2_acc(p[0], s[0], av.y, o.y);
             }
             if (ND >= 2) {
                 dot2_acc(p[ND - 1], s[ND - 1], o.x, o.x);
-                dot2_acc(p[ND - 1], s[ND - 1], o.y, o.y);
+                dot2_acc(p2[ND - 1], s2[ND - 1], o.y, o.y);
             }
             zm = zc;
             zc = zp;
         }
     }
     if (ND > 0) {
+#pragma unroll
+        for (int d = 0; d < NDA; ++d)
+            if (ND >= 2) dd_add(p[d], s[d], p2[d], s2[d]);
         const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
         block_reduce_dd<NDA>(p, s, part + (int64_t)bid * ND);
     }

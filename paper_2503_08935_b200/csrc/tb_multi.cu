@@ -29,11 +29,16 @@ static int pass_sizes(int k, int* sz)
     return np;
 }
 
+// warps per CTA of a pass kernel (2 rows each): 20, except the 4-sweep continuation pass
+// whose q / x_{j0-2} register rings need more than the 96 registers 640 threads allow
+constexpr int mp_nw(int K, int mode) { return (mode == MODE_C && K >= 4) ? 16 : 20; }
+
 template <int K, int MODE, bool O2>
 static bcgs_status pass_k(bcgs_ctx c, TbArgs& a, int nz, bool neu)
 {
-    if (neu) return launch_tb4_k<K, 2, 16, 4, MODE, 1, false, false, true, O2>(c, a, nz);
-    return launch_tb4_k<K, 2, 16, 4, MODE, 1, false, false, false, O2>(c, a, nz);
+    constexpr int NW = mp_nw(K, MODE);
+    if (neu) return launch_tb4_k<K, 2, NW, 4, MODE, 1, false, false, true, O2>(c, a, nz);
+    return launch_tb4_k<K, 2, NW, 4, MODE, 1, false, false, false, O2>(c, a, nz);
 }
 
 template <int K>
@@ -51,7 +56,7 @@ static bcgs_status pass_mode(bcgs_ctx c, TbArgs& a, int nz, int mode, bool o2, b
 static bcgs_status pass(bcgs_ctx c, TbArgs& a, int K, int mode, bool o2, bool neu)
 {
     // z-chunking as launch_tb: minimise waves x (planes per chunk + 2K) over the 148 SMs
-    const int hx = (K + 1) / 2 * 2, tx = 32 - 2 * hx, ty = 32 - 2 * K;
+    const int hx = (K + 1) / 2 * 2, tx = 32 - 2 * hx, ty = 2 * mp_nw(K, mode) - 2 * K;
     const int64_t tiles = ((a.nx + tx - 1) / tx) * (int64_t)((a.ny + ty - 1) / ty) * c->bpr;
     int64_t best_n = 1;
     double best = 1e300;

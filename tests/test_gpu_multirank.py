@@ -126,3 +126,38 @@ def test_gci_multirank_equals_single_gpu(bc):
     assert reps[0]["iterations"] == rep["iterations"]
     assert np.array_equal(hists[0], s.residual_history())
     assert np.array_equal(x, s.solution().cpu().numpy())
+
+
+def test_comm_ablation_runs_and_is_inert_when_off(bc, orc):
+    """BCGS_OPT_ABLATE (bench.py's exposed halo / reduction share): with halos and
+    cross-rank reductions skipped a fixed-iteration run still completes (finite scalars) and
+    differs from the real one; switching it off restores the bitwise oracle result."""
+    n3, h, P = (32, 32, 32), 1.0 / 33, 2
+    results = {}
+    for abl in (3, 0):
+        grp = bc.local_group(n3, h, P)
+        reps, errs = [None] * P, []
+
+        def work(r):
+            try:
+                grp[r].set_option(bc.OPT_ABLATE, abl)
+                grp[r].set_preconditioner("gnocomm", 4)
+                grp[r].set_rhs_random(si.SEED)
+                reps[r] = grp[r].solve(fixed_iters=5)
+            except Exception as ex:
+                errs.append(ex)
+
+        th = [threading.Thread(target=work, args=(r,)) for r in range(P)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=600)
+        assert not errs, errs
+        results[abl] = np.concatenate([s.solution().cpu().numpy() for s in grp])
+        assert all(r["iterations"] == 5 for r in reps)
+        for s in grp:
+            s.close()
+    assert np.all(np.isfinite(results[3])) and not np.array_equal(results[3], results[0])
+    b = orc.rhs_random(n3[::-1], si.SEED)
+    o = orc.bicgstab(b, h, pc="gnocomm", k=4, nslab=P, fixed_it=5)
+    assert np.array_equal(results[0], o.x)

@@ -51,7 +51,10 @@ if len(src) > 2:
     for r in src[2:]:
         if len(r) <= ia:
             continue
-        n = int(r[ia] or 0)
+        try:
+            n = int(r[ia] or 0)
+        except ValueError:   # the header row repeats per kernel in multi-kernel reports
+            continue
         tot += n
         toks = r[isrc].split()
         if not toks:

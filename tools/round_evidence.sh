@@ -11,4 +11,11 @@ nproc > gpurun_out/host_$TAG.txt; lscpu | grep -i "model name" >> gpurun_out/hos
 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k regex:"k_cheb_tb4|k_update_xr2|k_stencil2_dot" --launch-skip 24 --launch-count 5 -o gpurun_out/full_$TAG python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k regex:"k_cheb_tb4" --launch-skip 6 --launch-count 6 -o gpurun_out/mp24_$TAG python tools/mp_bench.py --n 512 --degrees 24 --reps 1 > /dev/null 2>&1
+# summaries on the box (the .ncu-rep files are too large to bring back)
+for r in full_$TAG mp24_$TAG; do
+  python tools/ncu_summary.py gpurun_out/$r.ncu-rep > gpurun_out/${r}_summary.txt 2>&1
+  ncu -i gpurun_out/$r.ncu-rep --page raw --csv > gpurun_out/${r}_raw.csv 2>/dev/null
+  ncu -i gpurun_out/$r.ncu-rep --page details --csv > gpurun_out/${r}_details.csv 2>/dev/null
+  rm -f gpurun_out/$r.ncu-rep
+done
 ls -la gpurun_out
