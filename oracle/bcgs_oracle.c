@@ -400,7 +400,8 @@ void orc_pc_interval(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab
  * ---------------------------------------------------------------------------------------- */
 int orc_bicgstab_ex(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, int bcm,
                     int pc, int k, double c_min, double c_max, double lmin_ov, double lmax_ov,
-                    double tol_in, int max_in, const double* b, const double* x0, double tol,
+                    double tol_in, int max_in, int flags, const double* b, const double* x0,
+                    double tol,
                     int max_it, int fixed_it, double* x, double* hist, double* scal,
                     int* iters_out, double* true_rel, long long* inner_total);
 
@@ -413,7 +414,7 @@ static void apply_inner_bicgs(int64_t nx, int64_t ny, int64_t nz, double h, int6
     for (int64_t s = 0; s < nslab; ++s) {
         int bcm_s = (bcm & 15) | (s == 0 ? (bcm & 16) : 0) | (s == nslab - 1 ? (bcm & 32) : 0);
         int its = 0;
-        orc_bicgstab_ex(nx, ny, Lb, h, 1, bcm_s, 0, 0, 0.0, 0.0, 0.0, 0.0, 0.0, 0,
+        orc_bicgstab_ex(nx, ny, Lb, h, 1, bcm_s, 0, 0, 0.0, 0.0, 0.0, 0.0, 0.0, 0, 0,
                         q + s * Lb * pl, NULL, tol_in, max_in, 0, out + s * Lb * pl, hist,
                         NULL, &its, NULL, NULL);
         if (inner_total) *inner_total += its;
@@ -445,7 +446,8 @@ static void apply_inner_bicgs(int64_t nx, int64_t ny, int64_t nz, double h, int6
  * ---------------------------------------------------------------------------------------- */
 int orc_bicgstab_ex(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, int bcm,
                     int pc, int k, double c_min, double c_max, double lmin_ov, double lmax_ov,
-                    double tol_in, int max_in, const double* b, const double* x0, double tol,
+                    double tol_in, int max_in, int flags, const double* b, const double* x0,
+                    double tol,
                     int max_it, int fixed_it, double* x, double* hist, double* scal,
                     int* iters_out, double* true_rel, long long* inner_total)
 {
@@ -539,6 +541,15 @@ int orc_bicgstab_ex(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab,
         orc_apply_A_bc(nx, ny, nz, h, 1, bcm, rh, t);
         double ts = orc_dot(pl, nz, t, r);
         double tt = orc_dot(pl, nz, t, t);
+        /* flags bit 0 (R31, SURVEY §8(e) 2-sync rewrite): also r~ᵀs, r~ᵀt, sᵀs here, so that
+         * MPI5 disappears: ρ_new = r~ᵀs - ω r~ᵀt and ||r||² = sᵀs - 2ω tᵀs + ω² tᵀt (algebraic
+         * identities for r = s - ω t) */
+        double rts = 0.0, rtt = 0.0, ss = 0.0;
+        if (flags & 1) {
+            rts = orc_dot(pl, nz, rt, r);
+            rtt = orc_dot(pl, nz, rt, t);
+            ss = orc_dot(pl, nz, r, r);
+        }
         double omega = (tt == 0.0) ? 0.0 : ts / tt;  /* P:293, guard R6 */
         if (sc) { sc[2] = ts; sc[3] = tt; sc[4] = omega; }
         /* KernelBiCGS4: x = x + α p̂ + ω r̂ */
@@ -547,8 +558,15 @@ int orc_bicgstab_ex(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab,
         /* KernelBiCGS5: r = r - ω t, r0ᵀr, rᵀr; MPI5 */
 #pragma omp parallel for schedule(static)
         for (int64_t c = 0; c < n; ++c) r[c] = fma(-omega, t[c], r[c]);
-        double rho_new = orc_dot(pl, nz, rt, r);
-        double rr = orc_dot(pl, nz, r, r);
+        double rho_new, rr;
+        if (flags & 1) {     /* R31: fma forms, ||r||² clamped at 0 (cancellation) */
+            rho_new = fma(-omega, rtt, rts);
+            rr = fma(-omega, fma(-omega, tt, 2.0 * ts), ss);
+            if (rr < 0.0) rr = 0.0;
+        } else {
+            rho_new = orc_dot(pl, nz, rt, r);
+            rr = orc_dot(pl, nz, r, r);
+        }
         double rel = sqrt(rr) / nb;
         hist[i] = rel;
         if (sc) { sc[5] = rho_new; sc[6] = rr; sc[7] = 0.0; }
@@ -599,7 +617,7 @@ int orc_bicgstab_bc(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab,
                     double* x, double* hist, double* scal, int* iters_out, double* true_rel)
 {
     return orc_bicgstab_ex(nx, ny, nz, h, nslab, bcm, pc, k, c_min, c_max, lmin_ov, lmax_ov,
-                           0.0, 0, b, x0, tol, max_it, fixed_it, x, hist, scal, iters_out,
+                           0.0, 0, 0, b, x0, tol, max_it, fixed_it, x, hist, scal, iters_out,
                            true_rel, NULL);
 }
 
