@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--pc", default="gnocomm", choices=["gnocomm", "bj", "none"])
     ap.add_argument("--degree", type=int, default=4)
     ap.add_argument("--kernels", type=int, default=1, help="0 = reference kernels, 1 = fused")
+    ap.add_argument("--sync2", action="store_true",
+                    help="2-sync rewrite (R31): 2 reductions per iteration instead of 3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -204,6 +206,7 @@ def main():
     h = si.unit_cube_h(n)
     s = bcgs.Solver(n, h, rank=rank, nranks=world, nccl_id=nccl_id, device=local)
     s.set_option(bcgs.OPT_KERNELS, args.kernels)
+    s.set_option(bcgs.OPT_SYNC2, 1 if args.sync2 else 0)
     s.set_preconditioner(args.pc, k)
     s.set_rhs_random(si.SEED)
 
@@ -339,6 +342,7 @@ def main():
                        "grid": n, "preconditioner": args.pc, "degree": k,
                        "c_min": 10.0, "c_max": 1 - 1e-4, "decomposition": f"z-slab x{world}",
                        "kernels": "fused" if args.kernels else "reference",
+                       "reductions_per_iteration": 2 if args.sync2 else 3,
                        "l2": "inputs larger than L2 (each field 8*N^3/P bytes >> 126 MB)",
                        "rhs": "splitmix64 uniform[-1,1), seed 20250311"},
             "gdof_s": gdof,

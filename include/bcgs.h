@@ -107,6 +107,11 @@ typedef enum {
                                /* share: bit 0 skips the face halos, bit 1  */
                                /* the cross-rank reductions (each rank uses its own pairs).*/
                                /* The maths is WRONG while set; 0 = off (default)          */
+    BCGS_OPT_SYNC2 = 10,       /* 1 = 2-sync rewrite (R31): r~ᵀs, r~ᵀt, sᵀs  */
+                               /* join the a9 reduction, ρ_new and ||r||² follow from the  */
+                               /* identities for r = s - ω t -> 2 reductions per iteration */
+                               /* instead of 3 (fused path only; rounding differs from the */
+                               /* default, the oracle implements the same flag)            */
 } bcgs_option;
 
 /* Boundary condition kind of a physical face (Eq. 4 / Eq. 5). */

@@ -200,6 +200,7 @@ __global__ void k_init_state(DevState* st, double tol, int max_iter, int fixed)
     st->iter = 0;
     st->x_applied = 0;
     st->omega_iter = 0;
+    st->pend = DONE_RUNNING;
 }
 
 // ------------------------------------------------------------------ communication
@@ -806,6 +807,7 @@ bcgs_status bcgs_set_option(bcgs_ctx c, int32_t option, int64_t value)
     case BCGS_OPT_XCONC: c->xconc_opt = (int)value; break;
     case BCGS_OPT_MULTIPASS: c->mp_min = std::max<int>(4, (int)value); break;
     case BCGS_OPT_ABLATE: c->ablate = (int)(value & 3); break;
+    case BCGS_OPT_SYNC2: c->sync2_opt = (int)value; drop_graph(c); break;
     default: return fail(c, BCGS_E_INVALID, "unknown option %d", option);
     }
     drop_graph(c);
@@ -930,6 +932,14 @@ bcgs_status bcgs_begin(bcgs_ctx c, double rel_tol, int32_t max_iter, int32_t fix
     const size_t bytes = sizeof(double) * (size_t)n;
     k_init_state<<<1, 1, 0, c->s>>>(c->st, rel_tol, max_iter, fixed_iters);
     c->in_iters = 0;
+    c->sync2 = 0;
+    if (c->sync2_opt) {   // R31 is built on the fused path (vectorised streaming kernels)
+        if (!(c->kernels == 1 && fused::supported(c, c->degree, c->pc != BCGS_PC_NONE) &&
+              c->lay.nx % 2 == 0 && !(c->pc == BCGS_PC_CHEB_G && c->nranks > 1)))
+            return fail(c, BCGS_E_CONFIG, "BCGS_OPT_SYNC2 needs the fused path (kernels = 1, a "
+                        "Chebyshev preconditioner, even nx)");
+        c->sync2 = 1;
+    }
     // Alg. 3 l.1-4: r0 = b - A x0; r~ = r0; p0 = r0; ρ0 = r~ᵀr0
     if (c->have_x0) {
         TRY(halo(c, F(c, V_X)));

@@ -84,9 +84,10 @@ inline bool make_layout(const bcgs_grid_desc* g, int32_t nranks, Layout* lay)
     lay->off_state = off; off = align_up(off + sizeof(DevState));
     lay->off_hist = off;  off = align_up(off + sizeof(double) * (BCGS_HIST_CAP + 1));
     lay->off_scal = off;  off = align_up(off + sizeof(double) * 8 * BCGS_HIST_CAP);
-    lay->off_part = off;  off = align_up(off + sizeof(dd) * 2 * (size_t)lay->n_part);
-    lay->off_rank = off;  off = align_up(off + sizeof(dd) * 2);
-    lay->off_gath = off;  off = align_up(off + sizeof(dd) * 2 * (size_t)nranks);
+    // up to 5 Dot2 pairs per reduction (2-sync ω stage, R31)
+    lay->off_part = off;  off = align_up(off + sizeof(dd) * 5 * (size_t)lay->n_part);
+    lay->off_rank = off;  off = align_up(off + sizeof(dd) * 5);
+    lay->off_gath = off;  off = align_up(off + sizeof(dd) * 5 * (size_t)nranks);
     lay->total = off;
     return true;
 }
@@ -151,6 +152,7 @@ struct bcgs_ctx_s {
     cudaStream_t s_x = nullptr;       // low-priority stream of the concurrent x update
     cudaEvent_t ev_omega = nullptr, ev_xdone = nullptr;              // BCGS_OPT_DEFER_X (measured slower at 512^3: off)
     int kernels = 1, use_graph = 1, profile = 0, poll = 8, tb_variant = 7;
+    int sync2_opt = 0, sync2 = 0;   // BCGS_OPT_SYNC2 (R31); active for the current solve
     int ablate = 0;   // BCGS_OPT_ABLATE: 1 skip halos, 2 skip cross-rank reductions (timing)
     int mp_min = 4;   // multi-pass temporal blocking for degree > mp_min (BCGS_OPT_MULTIPASS)
     // preconditioner

@@ -34,6 +34,12 @@ __global__ void k_update_xr_s(double* __restrict__ x, const double* __restrict__
     block_reduce_dd<2>(p, q, part + (int64_t)blockIdx.x * 2);
 }
 
+// 2-sync (R31): apply the stop decided at the ω stage once x and r are updated
+__global__ void k_commit(DevState* st)
+{
+    if (!st->done && st->pend) st->done = st->pend;
+}
+
 // tile (TX, TY) of a kernel variant for degree k
 void variant_tile(int variant, int k, int* tx, int* ty)
 {
@@ -151,7 +157,8 @@ void on_begin(bcgs_ctx c)
         cudaEventRecord(c->ev_xdone, c->s_x);
     }
     const bool neu = c->mbc.m || c->mbc.zlo >= 0 || c->mbc.zhi >= 0;
-    c->defer_x = (c->defer_x_opt && !g_multi && !neu && c->kernels == 1 &&
+    if (c->sync2) c->xconc = 0;
+    c->defer_x = (c->defer_x_opt && !c->sync2 && !g_multi && !neu && c->kernels == 1 &&
                   c->pc != BCGS_PC_NONE && (c->lay.nx % 2) == 0 && c->degree <= c->mp_min &&
                   defer_x_ok(c)) ? 1 : 0;
 }
@@ -177,7 +184,7 @@ bcgs_status flush_x(bcgs_ctx c)
 // have arrived.  Writes the Dot2 partials of all launches contiguously; *nparts = count.
 template <int ND>
 bcgs_status halo_stencil(bcgs_ctx c, double* v, const double* a, double* out, int kc,
-                         int* nparts)
+                         int* nparts, const double* rt = nullptr)
 {
     const int nx = (int)c->lay.nx, ny = (int)c->lay.ny, L = (int)c->lay.L;
     const int cfg = std::min(std::max(c->stencil_cfg, 0), stream::NCFG - 1);
@@ -187,11 +194,11 @@ bcgs_status halo_stencil(bcgs_ctx c, double* v, const double* a, double* out, in
         const dim3 g = stream::stencil2_grid(nx, ny, ke - kb, cfg);
         dd* pp = c->part + (int64_t)nb * ND;
         switch (cfg) {
-        case 1: stream::k_stencil2_dot<ND, 32, 8, 16><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st); break;
-        case 2: stream::k_stencil2_dot<ND, 32, 4, 16><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st); break;
-        case 3: stream::k_stencil2_dot<ND, 64, 4, 8><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st); break;
-        case 4: stream::k_stencil2_dot<ND, 32, 16, 4><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st); break;
-        default: stream::k_stencil2_dot<ND, 32, 8, 8><<<g, sb, 0, c->s>>>(v, a, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st); break;
+        case 1: stream::k_stencil2_dot<ND, 32, 8, 16><<<g, sb, 0, c->s>>>(v, a, rt, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st); break;
+        case 2: stream::k_stencil2_dot<ND, 32, 4, 16><<<g, sb, 0, c->s>>>(v, a, rt, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st); break;
+        case 3: stream::k_stencil2_dot<ND, 64, 4, 8><<<g, sb, 0, c->s>>>(v, a, rt, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st); break;
+        case 4: stream::k_stencil2_dot<ND, 32, 16, 4><<<g, sb, 0, c->s>>>(v, a, rt, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st); break;
+        default: stream::k_stencil2_dot<ND, 32, 8, 8><<<g, sb, 0, c->s>>>(v, a, rt, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st); break;
         }
         nb += (int)(g.x * g.y * g.z);
     };
@@ -263,13 +270,26 @@ bcgs_status iteration(bcgs_ctx c)
         Prof pf(c, KC_FUSED_P2, 32.0 * n);
         TRY(launch_tb<MODE_S>(c, a));
     }
-    if (vec) {
+    if (vec && c->sync2) {   // R31: MPI4 + MPI5 in one reduction of five Dot2 pairs
+        TRY(halo_stencil<5>(c, F(c, V_RH), F(c, V_S), F(c, V_T), KC_STENCIL2, &np2, F(c, V_RT)));
+    } else if (vec) {
         TRY(halo_stencil<2>(c, F(c, V_RH), F(c, V_S), F(c, V_T), KC_STENCIL2, &np2));
     } else {
         TRY(halo(c, F(c, V_RH)));
         Prof pf(c, KC_STENCIL2, 24.0 * n);
         ref::k_stencil_dot<2><<<sg, sb, 0, c->s>>>(F(c, V_RH), F(c, V_S), F(c, V_T), g, 0,
                                                   c->part, st);
+    }
+    if (c->sync2) {   // ω, ρ_new, ||r||², test, β now; the stop applies after a11 + a12
+        TRY(reduce<5>(c, np2, STAGE_OMEGA2));
+        Prof pf(c, KC_FUSED_XR, 56.0 * n);
+        stream::k_update_xr2<0><<<kEwBlocks, 256, 0, c->s>>>(
+            (double2*)F(c, V_X), (const double2*)F(c, V_PH), (const double2*)F(c, V_RH),
+            (const double2*)F(c, V_S), (double2*)F(c, V_R), (const double2*)F(c, V_T),
+            nullptr, n / 2, nullptr, st);
+        k_commit<<<1, 1, 0, c->s>>>(st);
+        CUDA_OK(c, cudaGetLastError());
+        return BCGS_OK;
     }
     TRY(reduce<2>(c, np2, STAGE_OMEGA));
     if (c->xconc) {   // a11 on the low-priority stream, overlapping a12 and the next p-kernel
@@ -292,7 +312,7 @@ bcgs_status iteration(bcgs_ctx c)
     } else {
         Prof pf(c, KC_FUSED_XR, 64.0 * n);
         if (vec)
-            stream::k_update_xr2<<<kEwBlocks, 256, 0, c->s>>>(
+            stream::k_update_xr2<2><<<kEwBlocks, 256, 0, c->s>>>(
                 (double2*)F(c, V_X), (const double2*)F(c, V_PH), (const double2*)F(c, V_RH),
                 (const double2*)F(c, V_S), (double2*)F(c, V_R), (const double2*)F(c, V_T),
                 (const double2*)F(c, V_RT), n / 2, c->part, st);

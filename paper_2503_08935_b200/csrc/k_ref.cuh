@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(1024) k_finalize(const dd* __restrict__ part, 
 #pragma unroll
             for (int d = 0; d < ND; ++d) rank_out[d] = res[d];
         } else {
-            double v[2] = {0.0, 0.0};
+            double v[ND > 2 ? ND : 2] = {};
 #pragma unroll
             for (int d = 0; d < ND; ++d) {
                 double P = 0.0, S = 0.0;
@@ -323,7 +323,7 @@ __global__ void k_scalars(const dd* __restrict__ gathered, int nranks, int stage
                           DevState* st, double* hist, double* scal)
 {
     if (stage != STAGE_SETUP && stage != STAGE_DOT && st->done) return;
-    double v[2] = {0.0, 0.0};
+    double v[ND > 2 ? ND : 2] = {};
     for (int d = 0; d < ND; ++d) {
         double P = 0.0, S = 0.0;
         for (int r = 0; r < nranks; ++r) dd_add(P, S, gathered[r * ND + d].hi,

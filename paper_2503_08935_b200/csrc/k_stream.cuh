@@ -22,9 +22,11 @@ constexpr int CFG_BX[NCFG] = {32, 32, 32, 64, 32}, CFG_BY[NCFG] = {8, 8, 4, 4, 1
 // w = A v (global operator; ghost planes hold halo data or zeros) and Dot2 partials of
 // a·w (ND >= 1) and w·w (ND == 2).  Each thread owns 2 adjacent x points of one row and
 // marches SZC planes; requires nx even (16-byte aligned rows).
+// ND == 5 (2-sync, R31): a = s, rt = r~: partials tᵀs, tᵀt, r~ᵀs, r~ᵀt, sᵀs.
 template <int ND, int SBX, int SBY, int SZC>
 __global__ void __launch_bounds__(SBX * SBY) k_stencil2_dot(const double* __restrict__ v,
                                                             const double* __restrict__ a,
+                                                            const double* __restrict__ rt,
                                                             double* __restrict__ out, int nx,
                                                             int ny, int kb, int ke, double h2inv,
                                                             ref::MirrorBc bc,
@@ -68,9 +70,18 @@ __global__ void __launch_bounds__(SBX * SBY) k_stencil2_dot(const double* __rest
                 if (ND >= 2) dot2_acc(p2[0], s2[0], av.y, o.y);
                 else dot2_acc(p[0], s[0], av.y, o.y);
             }
-            if (ND >= 2) {
-                dot2_acc(p[ND - 1], s[ND - 1], o.x, o.x);
-                dot2_acc(p2[ND - 1], s2[ND - 1], o.y, o.y);
+            if (ND == 2 || ND == 5) {
+                dot2_acc(p[1], s[1], o.x, o.x);
+                dot2_acc(p2[1], s2[1], o.y, o.y);
+            }
+            if (ND == 5) {
+                const double2 rv = __ldg(reinterpret_cast<const double2*>(rt + c));
+                dot2_acc(p[2], s[2], rv.x, av.x);
+                dot2_acc(p2[2], s2[2], rv.y, av.y);
+                dot2_acc(p[3], s[3], rv.x, o.x);
+                dot2_acc(p2[3], s2[3], rv.y, o.y);
+                dot2_acc(p[4], s[4], av.x, av.x);
+                dot2_acc(p2[4], s2[4], av.y, av.y);
             }
             zm = zc;
             zc = zp;
@@ -95,6 +106,8 @@ inline dim3 stencil2_grid(int64_t nx, int64_t ny, int64_t nplanes, int cfg = 0)
 // a11 + a12: x = fma(ω, r̂, fma(α, p̂, x)); r = fma(-ω, t, s); partials r~·r, r·r.
 // n2 = number of double2 elements; UNR double2 groups per thread per iteration.
 constexpr int XR_UNR = 2;
+// ND = 2: partials r~ᵀr, rᵀr (a12); ND = 0 (2-sync, R31): no dots, r~ not read
+template <int ND = 2>
 __global__ void __launch_bounds__(256) k_update_xr2(double2* __restrict__ x,
                                                     const double2* __restrict__ ph,
                                                     const double2* __restrict__ rh,
@@ -120,7 +133,7 @@ __global__ void __launch_bounds__(256) k_update_xr2(double2* __restrict__ x,
             vrh[u] = __ldg(rh + e);
             vs[u] = __ldg(s + e);
             vt[u] = __ldg(t + e);
-            vrt[u] = __ldg(rt + e);
+            if (ND) vrt[u] = __ldg(rt + e);
         }
 #pragma unroll
         for (int u = 0; u < XR_UNR; ++u) {
@@ -132,14 +145,17 @@ __global__ void __launch_bounds__(256) k_update_xr2(double2* __restrict__ x,
             rn.y = upd_r(vs[u].y, vt[u].y, omega);
             x[e] = xn;
             r[e] = rn;
-            dot2_acc(p[0], q[0], vrt[u].x, rn.x);
-            dot2_acc(p[0], q[0], vrt[u].y, rn.y);
-            dot2_acc(p[1], q[1], rn.x, rn.x);
-            dot2_acc(p[1], q[1], rn.y, rn.y);
+            if (ND) {
+                dot2_acc(p[0], q[0], vrt[u].x, rn.x);
+                dot2_acc(p[0], q[0], vrt[u].y, rn.y);
+                dot2_acc(p[1], q[1], rn.x, rn.x);
+                dot2_acc(p[1], q[1], rn.y, rn.y);
+            }
         }
     }
     for (; c < n2; c += stride) {
-        const double2 vx = x[c], vph = ph[c], vrh = rh[c], vs = s[c], vt = t[c], vrt = rt[c];
+        const double2 vx = x[c], vph = ph[c], vrh = rh[c], vs = s[c], vt = t[c];
+        const double2 vrt = ND ? rt[c] : make_double2(0.0, 0.0);
         double2 xn, rn;
         xn.x = upd_x(vx.x, vph.x, vrh.x, alpha, omega);
         xn.y = upd_x(vx.y, vph.y, vrh.y, alpha, omega);
@@ -147,12 +163,14 @@ __global__ void __launch_bounds__(256) k_update_xr2(double2* __restrict__ x,
         rn.y = upd_r(vs.y, vt.y, omega);
         x[c] = xn;
         r[c] = rn;
-        dot2_acc(p[0], q[0], vrt.x, rn.x);
-        dot2_acc(p[0], q[0], vrt.y, rn.y);
-        dot2_acc(p[1], q[1], rn.x, rn.x);
-        dot2_acc(p[1], q[1], rn.y, rn.y);
+        if (ND) {
+            dot2_acc(p[0], q[0], vrt.x, rn.x);
+            dot2_acc(p[0], q[0], vrt.y, rn.y);
+            dot2_acc(p[1], q[1], rn.x, rn.x);
+            dot2_acc(p[1], q[1], rn.y, rn.y);
+        }
     }
-    block_reduce_dd<2>(p, q, part + (int64_t)blockIdx.x * 2);
+    if (ND) block_reduce_dd<2>(p, q, part + (int64_t)blockIdx.x * 2);
 }
 
 // a12 alone (deferred-x mode, x is updated inside the next p-kernel): r = fma(-ω, t, s);

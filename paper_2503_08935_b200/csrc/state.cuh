@@ -21,6 +21,7 @@ struct DevState {
     int32_t omega_iter;   // last iteration that reached its ω (x update due)
     double xa, xw;        // α, ω of iteration omega_iter (for the concurrent x update)
     double scratch[8];    // results of stand-alone dot calls
+    int32_t pend;         // 2-sync (R31): stop decided at the ω stage, applied after a11/a12
 };
 
 // Reduction stages (one per MPI_Allreduce site of Alg. 3).
@@ -29,7 +30,8 @@ enum : int32_t {
     STAGE_ALPHA = 1,   // {r~ᵀw}               MPI2 + α
     STAGE_OMEGA = 2,   // {tᵀs, tᵀt}           MPI4 + ω
     STAGE_RHO = 3,     // {r~ᵀr, rᵀr}          MPI5 + test + ρ, β
-    STAGE_DOT = 4      // stand-alone dot -> scratch
+    STAGE_DOT = 4,     // stand-alone dot -> scratch
+    STAGE_OMEGA2 = 5   // 2-sync (R31): {tᵀs, tᵀt, r~ᵀs, r~ᵀt, sᵀs} -> ω, ρ_new, ||r||², test
 };
 
 // Executed by a single thread once the global Dot2 values are known.
@@ -110,6 +112,50 @@ __device__ __forceinline__ void stage_update(DevState* st, int stage, const doub
         st->rho = rho_new;
         sc[7] = beta;
         if (st->fixed_iters <= 0 && i >= st->max_iter) st->done = DONE_MAXIT;
+        break;
+    }
+    case STAGE_OMEGA2: {
+        // MPI4 + MPI5 in one reduction: r = s - ω t gives
+        // r~ᵀr = r~ᵀs - ω r~ᵀt and ||r||² = sᵀs - 2ω tᵀs + ω² tᵀt (clamped at 0).  The stop
+        // is recorded in `pend` and applied after the x / r update kernel (k_commit).
+        const int i = st->iter + 1;
+        double* sc = scal + 8 * (i - 1);
+        const double ts = v[0], tt = v[1];
+        st->ts = ts;
+        st->tt = tt;
+        const double omega = (tt == 0.0) ? 0.0 : ts / tt;   // P:293, R6
+        st->omega = omega;
+        sc[2] = ts;
+        sc[3] = tt;
+        sc[4] = omega;
+        const double rho_new = fma(-omega, v[3], v[2]);
+        double rr = fma(-omega, fma(-omega, tt, 2.0 * ts), v[4]);
+        if (rr < 0.0) rr = 0.0;
+        st->rho_new = rho_new;
+        st->rr = rr;
+        const double rel = sqrt(rr) / st->nb;    // R4
+        st->rel = rel;
+        st->iter = i;
+        hist[i] = rel;
+        sc[5] = rho_new;
+        sc[6] = rr;
+        sc[7] = 0.0;
+        if (st->fixed_iters > 0) {
+            if (i == st->fixed_iters) { st->pend = DONE_OK; break; }
+        } else if (rel < st->tol) {
+            st->pend = DONE_OK;
+            break;
+        }
+        if (omega == 0.0 || rho_new == 0.0 || !isfinite(rho_new) || !isfinite(rr) ||
+            !isfinite(omega)) {
+            st->pend = DONE_BREAKDOWN;
+            break;
+        }
+        const double beta = (rho_new / st->rho) * (st->alpha / omega);   // R20
+        st->beta = beta;
+        st->rho = rho_new;
+        sc[7] = beta;
+        if (st->fixed_iters <= 0 && i >= st->max_iter) st->pend = DONE_MAXIT;
         break;
     }
     default: {
