@@ -24,7 +24,10 @@ constexpr int CFG_BX[NCFG] = {32, 32, 32, 64, 32}, CFG_BY[NCFG] = {8, 8, 4, 4, 1
 // marches SZC planes; requires nx even (16-byte aligned rows).
 // ND == 5 (2-sync, R31): a = s, rt = r~: partials tᵀs, tᵀt, r~ᵀs, r~ᵀt, sᵀs.
 template <int ND, int SBX, int SBY, int SZC>
-__global__ void __launch_bounds__(SBX * SBY) k_stencil2_dot(const double* __restrict__ v,
+// occupancy targets (registers): ND <= 1: 6 x 256 threads (<= 40), ND = 2: 4 (<= 64),
+// ND = 5: 3 (<= 80, no spills) -- the kernel is latency-bound (long scoreboard)
+__global__ void __launch_bounds__(SBX * SBY, (ND == 5 ? 768 : ND == 2 ? 1024 : 1536) / (SBX * SBY))
+k_stencil2_dot(const double* __restrict__ v,
                                                             const double* __restrict__ a,
                                                             const double* __restrict__ rt,
                                                             double* __restrict__ out, int nx,
@@ -41,7 +44,7 @@ __global__ void __launch_bounds__(SBX * SBY) k_stencil2_dot(const double* __rest
     // ND == 2: second accumulator pair per dot for the odd x point -- two independent Dot2
     // chains (ILP, 0.70 -> 0.67 ms at 512^3); merged before the block reduction (Dot2 is
     // order-insensitive, R19)
-    double p2[NDA] = {}, s2[NDA] = {};
+    double p2[2] = {}, s2[2] = {};
     if (i < nx && j < ny) {
         const int64_t plane = (int64_t)nx * ny;
         int64_t c = i + (int64_t)nx * j + plane * k0;
@@ -74,14 +77,14 @@ __global__ void __launch_bounds__(SBX * SBY) k_stencil2_dot(const double* __rest
                 dot2_acc(p[1], s[1], o.x, o.x);
                 dot2_acc(p2[1], s2[1], o.y, o.y);
             }
-            if (ND == 5) {
+            if (ND == 5) {   // one chain per extra dot: registers for occupancy (latency)
                 const double2 rv = __ldg(reinterpret_cast<const double2*>(rt + c));
                 dot2_acc(p[2], s[2], rv.x, av.x);
-                dot2_acc(p2[2], s2[2], rv.y, av.y);
+                dot2_acc(p[2], s[2], rv.y, av.y);
                 dot2_acc(p[3], s[3], rv.x, o.x);
-                dot2_acc(p2[3], s2[3], rv.y, o.y);
+                dot2_acc(p[3], s[3], rv.y, o.y);
                 dot2_acc(p[4], s[4], av.x, av.x);
-                dot2_acc(p2[4], s2[4], av.y, av.y);
+                dot2_acc(p[4], s[4], av.y, av.y);
             }
             zm = zc;
             zc = zp;
@@ -89,8 +92,7 @@ __global__ void __launch_bounds__(SBX * SBY) k_stencil2_dot(const double* __rest
     }
     if (ND > 0) {
 #pragma unroll
-        for (int d = 0; d < NDA; ++d)
-            if (ND >= 2) dd_add(p[d], s[d], p2[d], s2[d]);
+        for (int d = 0; d < (ND >= 2 ? 2 : 0); ++d) dd_add(p[d], s[d], p2[d], s2[d]);
         const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
         block_reduce_dd<NDA>(p, s, part + (int64_t)bid * ND);
     }
