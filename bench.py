@@ -27,6 +27,15 @@ sys.path.insert(0, ROOT)
 
 METRIC = "fp64 Bi-CGSTAB iters/s & GDoF/s at 512^3; % of HBM roofline"
 ALG_BYTES_PER_PT = 200.0   # compulsory bytes per point per outer iteration
+ALG_BYTES_NONE = 168.0     # M = I: the same rows without the preconditioner
+
+
+def workload(n: int, pc: str, k: int) -> str:
+    """BASELINE.json config names: C2 = 256^3, C3 = 512^3, C5 = 1024^3 (here on one GPU)."""
+    tag = {256: "C2 ", 512: "C3 ", 1024: "C5 "}.get(n, "")
+    name = {"gnocomm": "GNoComm(CI)", "bj": "BJ(CI)", "g": "G(CI)", "none": "BiCGS (M = I)"}.get(pc, pc)
+    return f"{tag}{n}^3 {name} k={k}"
+
 # FP64 flops per point of one launch of the fused Chebyshev kernels at degree k (DESIGN.md §5):
 # sweep 1: 12, sweep 2: 16, sweeps 3..k: 15 each; + the fused vector update (p: 4, s: 2)
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
@@ -165,7 +174,7 @@ def reference_arm(args, rank, world):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt * scale * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C3 {n}^3 {args.pc} k={args.degree}", "grid": n,
+            "config": {"workload": workload(n, args.pc, args.degree), "grid": n,
                        "preconditioner": args.pc, "degree": args.degree},
             "gdof_s": n ** 3 * v / 1e9,
             "cpu_baseline": {"value": v, "unit": "iters/s", "cores": oracle.threads(),
@@ -270,7 +279,8 @@ def main():
     gdof = n ** 3 * its / 1e9
     peak, peak_src = peaks()
     pts_local = n * n * (n // world)
-    iter_gbs = ALG_BYTES_PER_PT * pts_local / (ms_iter * 1e-3) / 1e9
+    alg_bpp = ALG_BYTES_NONE if args.pc == "none" else ALG_BYTES_PER_PT
+    iter_gbs = alg_bpp * pts_local / (ms_iter * 1e-3) / 1e9
 
     # dominant kernel of the timed region (largest total device time)
     ours = {kname: v for kname, v in ktimes.items() if kname not in ("halo", "allgather")}
@@ -337,8 +347,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_iter,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C3 {n}^3 GNoComm(CI) k={k}" if args.pc == "gnocomm"
-                       else f"{n}^3 {args.pc} k={k}",
+            "config": {"workload": workload(n, args.pc, k),
                        "grid": n, "preconditioner": args.pc, "degree": k,
                        "c_min": 10.0, "c_max": 1 - 1e-4, "decomposition": f"z-slab x{world}",
                        "kernels": "fused" if args.kernels else "reference",
@@ -346,7 +355,7 @@ def main():
                        "l2": "inputs larger than L2 (each field 8*N^3/P bytes >> 126 MB)",
                        "rhs": "splitmix64 uniform[-1,1), seed 20250311"},
             "gdof_s": gdof,
-            "iteration_roofline": {"alg_bytes_per_pt": ALG_BYTES_PER_PT,
+            "iteration_roofline": {"alg_bytes_per_pt": alg_bpp,
                                    "achieved_gbs": iter_gbs, "peak_gbs": peak,
                                    "frac": iter_gbs / peak},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

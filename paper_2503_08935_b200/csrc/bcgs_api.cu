@@ -503,6 +503,8 @@ bcgs_status iteration(bcgs_ctx c)
     if (c->pc == BCGS_PC_CHEB_G && c->nranks > 1) return iteration_ref(c);   // k-deep halos
     if (c->kernels == 1 && fused::supported(c, c->degree, c->pc != BCGS_PC_NONE))
         return fused::iteration(c);
+    if (c->kernels == 1 && c->pc == BCGS_PC_NONE && c->lay.nx % 2 == 0)
+        return fused::iteration_none(c);
     return iteration_ref(c);
 }
 

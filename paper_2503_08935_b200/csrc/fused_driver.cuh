@@ -220,6 +220,42 @@ bcgs_status halo_stencil(bcgs_ctx c, double* v, const double* a, double* out, in
     return BCGS_OK;
 }
 
+// Unpreconditioned iteration (M = I: BiCGS, Table II row 1; config C1) on the streaming
+// kernels: no copies for p̂ = p and r̂ = s.  168 B/pt: w = A p + r~ᵀw (24), s (24),
+// t = A s + tᵀs, tᵀt (24), x / r + r~ᵀr, rᵀr (64), p (32).
+bcgs_status iteration_none(bcgs_ctx c)
+{
+    const int64_t n = npts(c);
+    DevState* st = c->st;
+    int np1 = 0, np2 = 0;
+    TRY(halo_stencil<1>(c, F(c, V_P), F(c, V_RT), F(c, V_W), KC_STENCIL1, &np1));
+    TRY(reduce<1>(c, np1, STAGE_ALPHA));
+    {
+        Prof pf(c, KC_AXPY, 24.0 * n);
+        stream::k_axpy_s2<<<kEwBlocks, 256, 0, c->s>>>((double2*)F(c, V_S),
+                                                       (const double2*)F(c, V_R),
+                                                       (const double2*)F(c, V_W), n / 2, st);
+    }
+    TRY(halo_stencil<2>(c, F(c, V_S), F(c, V_S), F(c, V_T), KC_STENCIL2, &np2));
+    TRY(reduce<2>(c, np2, STAGE_OMEGA));
+    {
+        Prof pf(c, KC_FUSED_XR, 64.0 * n);
+        stream::k_update_xr2<2><<<kEwBlocks, 256, 0, c->s>>>(
+            (double2*)F(c, V_X), (const double2*)F(c, V_P), (const double2*)F(c, V_S),
+            (const double2*)F(c, V_S), (double2*)F(c, V_R), (const double2*)F(c, V_T),
+            (const double2*)F(c, V_RT), n / 2, c->part, st);
+    }
+    TRY(reduce<2>(c, kEwBlocks, STAGE_RHO));
+    {
+        Prof pf(c, KC_UPDATE_P, 32.0 * n);
+        stream::k_update_p2<<<kEwBlocks, 256, 0, c->s>>>((double2*)F(c, V_P),
+                                                         (const double2*)F(c, V_R),
+                                                         (const double2*)F(c, V_W), n / 2, st);
+    }
+    CUDA_OK(c, cudaGetLastError());
+    return BCGS_OK;
+}
+
 bcgs_status iteration(bcgs_ctx c)
 {
     const int64_t n = npts(c);

@@ -281,6 +281,7 @@ inline bool supported(bcgs_ctx c, int degree, bool has_pc)
     return has_pc && degree >= 1 && (degree <= KMAX_TB || multipass_ok(c));
 }
 bcgs_status iteration(bcgs_ctx c);
+bcgs_status iteration_none(bcgs_ctx c);
 void on_begin(bcgs_ctx c);
 bool precond_supported(bcgs_ctx c);
 bcgs_status precond_apply(bcgs_ctx c, const double* q, double* out);

@@ -278,4 +278,35 @@ __global__ void __launch_bounds__(256) k_xupd_conc(double2* __restrict__ x,
 
 __global__ void k_xmark_conc(DevState* st) { st->x_applied = st->omega_iter; }
 
+// M = I (plain Bi-CGSTAB, P:145-174 / Alg. 3 with p̂ = p, r̂ = s): a6 s = fma(-α, w, r) into
+// its own buffer, and a14 p = fma(β, fma(-ω, w, p), r) in place (element-wise), 16-byte I/O.
+__global__ void __launch_bounds__(256) k_axpy_s2(double2* __restrict__ s,
+                                                 const double2* __restrict__ r,
+                                                 const double2* __restrict__ w, int64_t n2,
+                                                 const DevState* __restrict__ st)
+{
+    if (st->done) return;
+    const double alpha = st->alpha;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n2;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const double2 rv = __ldg(r + c), wv = __ldg(w + c);
+        s[c] = make_double2(upd_s(rv.x, wv.x, alpha), upd_s(rv.y, wv.y, alpha));
+    }
+}
+
+__global__ void __launch_bounds__(256) k_update_p2(double2* __restrict__ p,
+                                                   const double2* __restrict__ r,
+                                                   const double2* __restrict__ w, int64_t n2,
+                                                   const DevState* __restrict__ st)
+{
+    if (st->done) return;
+    const double beta = st->beta, omega = st->omega;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n2;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const double2 rv = __ldg(r + c), wv = __ldg(w + c), pv = p[c];
+        p[c] = make_double2(upd_p(rv.x, pv.x, wv.x, beta, omega),
+                            upd_p(rv.y, pv.y, wv.y, beta, omega));
+    }
+}
+
 }  // namespace stream

@@ -302,3 +302,21 @@ def test_concurrent_x_update_parity(bc, orc, n, pc, k, bpr):
     o = orc.bicgstab(b, h, pc=pc, k=k, nslab=bpr, tol=1e-8)
     assert rep["iterations"] == o.iterations
     assert np.array_equal(host(s.solution()), o.x)
+
+
+def test_unpreconditioned_streaming_path(bc, orc):
+    """M = I on the fused path: no p̂ / r̂ copies (no precond_sweep launches), bitwise oracle."""
+    n = 48
+    h = si.unit_cube_h(n)
+    s = bc.Solver(n, h)
+    s.set_preconditioner("none", 0)
+    s.set_option(bc.OPT_PROFILE, 1)
+    s.set_rhs_random(si.SEED)
+    rep = s.solve(tol=1e-8)
+    kt = s.kernel_times()
+    assert "precond_sweep" not in kt and kt["update_p"]["calls"] >= rep["iterations"] - 1
+    o = orc.bicgstab(orc.rhs_random((n, n, n), si.SEED), h, pc="none", tol=1e-8)
+    assert rep["iterations"] == o.iterations
+    assert np.array_equal(s.residual_history(), o.history)
+    assert np.array_equal(host(s.solution()), o.x)
+    s.close()
