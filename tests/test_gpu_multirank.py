@@ -143,7 +143,7 @@ def test_comm_ablation_runs_and_is_inert_when_off(bc, orc):
                 grp[r].set_option(bc.OPT_ABLATE, abl)
                 grp[r].set_preconditioner("gnocomm", 4)
                 grp[r].set_rhs_random(si.SEED)
-                reps[r] = grp[r].solve(fixed_iters=5)
+                reps[r] = grp[r].solve(fixed_iters=25 if abl else 5)
             except Exception as ex:
                 errs.append(ex)
 
@@ -154,7 +154,8 @@ def test_comm_ablation_runs_and_is_inert_when_off(bc, orc):
             t.join(timeout=600)
         assert not errs, errs
         results[abl] = np.concatenate([s.solution().cpu().numpy() for s in grp])
-        assert all(r["iterations"] == 5 for r in reps)
+        # bench.py times 20 ablated iterations after warm-up: the wrong scalars must not stop
+        assert all(r["iterations"] == (25 if abl else 5) for r in reps)
         for s in grp:
             s.close()
     assert np.all(np.isfinite(results[3])) and not np.array_equal(results[3], results[0])
