@@ -8,7 +8,8 @@ TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and ``be
 ``-ffp-contract=off``); this module only marshals numpy arrays through ctypes.
 ``dense.py`` holds the dense Kronecker assembly of Eq. 6 used as a pin on tiny grids.
 
-Parity status: every oracle function is pinned by ``tests/test_oracle_pins.py``.
+Parity status: every oracle function is pinned by ``tests/test_oracle_pins.py``,
+``test_oracle_bc.py``, ``test_oracle_inner.py`` and ``test_oracle_sync2.py``.
 """
 from __future__ import annotations
 

@@ -23,7 +23,9 @@
  * "_bc" entry points); non-zero boundary data are folded into the right-hand side once
  * (orc_fold_boundary_bc).
  *
- * Parity status: every function below is pinned by tests/test_oracle_pins.py against values
+ * Parity status: every function below is pinned by tests/test_oracle_pins.py (and, for the
+ * mixed faces, the inner-Krylov preconditioners and the 2-sync flag, by test_oracle_bc.py,
+ * test_oracle_inner.py and test_oracle_sync2.py) against values
  * that do not come from this file (dense Kronecker assembly, closed-form spectra, closed-form
  * Chebyshev polynomials, dense direct solves, manufactured solutions, exact summation,
  * splitmix64's published test vector).  No function is "parity unpinned".
