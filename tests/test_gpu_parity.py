@@ -147,6 +147,20 @@ def test_solve_parity_128(bc, orc, kernels):
     assert_parity(*compare_solve(bc, orc, 128, "gnocomm", 4, 1, kernels))
 
 
+@pytest.mark.parametrize("n,pc,k,bpr", [(64, "gnocomm", 1, 1), (64, "gnocomm", 4, 8),
+                                        (128, "gnocomm", 4, 8), (128, "bj", 4, 8),
+                                        (128, "gnocomm", 8, 2), (64, "bj", 16, 4)])
+def test_solve_parity_matrix(bc, orc, n, pc, k, bpr):
+    """SURVEY §8(c) parity matrix rows not covered above: GNoComm k = 1, P = 8 slab blocks
+    (8 / 16 planes), BJ at P = 8, and multi-pass degrees, full solves to 1e-8, bitwise."""
+    assert_parity(*compare_solve(bc, orc, n, pc, k, bpr, 1))
+
+
+def test_c2_256_eight_slabs_first_20(bc, orc):
+    """256³ with 8 slab blocks (the P = 8 preconditioner of SURVEY §8(c)), 20 iterations."""
+    assert_parity(*compare_solve(bc, orc, 256, "gnocomm", 4, 8, 1, fixed=20))
+
+
 @pytest.mark.parametrize("kernels", KERNELS)
 def test_c2_256_first_20_iterations(bc, orc, kernels):
     """Config C2 (256³, Chebyshev degree 4): first 20 iterations, bitwise."""
