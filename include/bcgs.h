@@ -95,7 +95,9 @@ typedef enum {
     BCGS_OPT_POLL = 3,         /* iterations launched between done-flag polls (tol mode)  */
     BCGS_OPT_TB_VARIANT = 4,   /* temporally blocked kernel layout (tuning): 2 = square   */
                                /* tile (any k, odd nx), 5 = TMA warp-row 16 warps,       */
-                               /* 7 = TMA warp-row 24 warps (default; k <= 4)            */
+                               /* 7 = TMA warp-row 24 warps (default; k <= 4),          */
+                               /* 9 = 7 in x-pair clusters sharing the x-halo through   */
+                               /*     DSMEM (experimental, slower: DESIGN.md §8)         */
     BCGS_OPT_DEFER_X = 5,      /* 1 = apply x += αp̂ + ωr̂ inside the next p-kernel (off)    */
     BCGS_OPT_STENCIL_CFG = 6,  /* stencil+dot launch configuration 0..4 (tuning)          */
     BCGS_OPT_XCONC = 7,        /* 1 = x update on a concurrent low-priority stream (off)  */

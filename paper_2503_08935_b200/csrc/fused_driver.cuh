@@ -49,6 +49,8 @@ void variant_tile(int variant, int k, int* tx, int* ty)
         if (k >= 7) { *tx = 16; *ty = 8; } else if (k >= 5) { *tx = 32; *ty = 8; }
     } else if (variant == 7 && k <= 4) {
         *tx = 32 - 2 * hx; *ty = 48 - 2 * k;               // 24 warps x RY = 2
+    } else if (variant == 9 && k <= 4) {
+        *tx = 32 - hx; *ty = 48 - 2 * k;                   // x-pair clusters: per CTA
     } else {
         *tx = 32 - 2 * hx; *ty = 32 - 2 * k;               // 16 warps x RY = 2 (variant 5)
     }

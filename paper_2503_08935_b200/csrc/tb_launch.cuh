@@ -107,13 +107,13 @@ inline bool make_maps(bcgs_ctx c, TbMaps* maps, const TbArgs& a, int mode, int b
 }
 
 template <int K, int RY, int NW, int NS, int MODE, int MINB = 1, bool XUPD = false,
-          bool XSH = false, bool NEU = false, bool O2 = false>
+          bool XSH = false, bool NEU = false, bool O2 = false, bool XP = false>
 bcgs_status launch_tb4_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
 {
-    using S = Tb4Shape<K, RY, NW, NS>;
+    using S = Tb4Shape<K, RY, NW, NS, XP>;
     constexpr size_t smem = S::smem + (XUPD ? S::xupd_bytes : 0);
     static_assert(smem <= 227 * 1024, "tb4 shared memory budget");
-    auto kern = k_cheb_tb4<K, RY, NW, NS, MODE, MINB, XUPD, XSH, NEU, O2>;
+    auto kern = k_cheb_tb4<K, RY, NW, NS, MODE, MINB, XUPD, XSH, NEU, O2, XP>;
     static bool attr = false;
     if (!attr) {
         CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -123,6 +123,24 @@ bcgs_status launch_tb4_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
     TbMaps maps;
     if (!make_maps(c, &maps, a, MODE, S::EY))
         return fail(c, BCGS_E_CUDA, "cuTensorMapEncodeTiled failed");
+    if constexpr (XP) {   // cluster pairs along x: 64 - 2 HX output columns per pair
+        constexpr int TXP = 64 - 2 * S::HX;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)(2 * ((a.nx + TXP - 1) / TXP)),
+                           (unsigned)((a.ny + S::TY - 1) / S::TY), (unsigned)nchunk_total);
+        cfg.blockDim = dim3(NW * 32);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = c->s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CUDA_OK(c, cudaLaunchKernelEx(&cfg, kern, (TbArgs)a, maps));
+        return BCGS_OK;
+    }
     dim3 grid((unsigned)((a.nx + S::TX - 1) / S::TX), (unsigned)((a.ny + S::TY - 1) / S::TY),
               (unsigned)nchunk_total);
     kern<<<grid, NW * 32, smem, c->s>>>(a, maps);
@@ -148,6 +166,8 @@ bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz)
         if (c->tb_variant == 5 && tma_ok(c)) return launch_tb4_k<K, 2, 16, 4, MODE>(c, a, nz);
         if constexpr (K <= 4) {
             if (c->tb_variant == 7 && tma_ok(c)) return launch_tb4_k<K, 2, 24, 3, MODE>(c, a, nz);
+            if (c->tb_variant == 9 && tma_ok(c))   // x-pair clusters (experimental)
+                return launch_tb4_k<K, 2, 24, 3, MODE, 1, false, false, false, false, true>(c, a, nz);
         }
     }
     return launch_tb_k<K, MODE>(c, a, nz);

@@ -286,7 +286,7 @@ def test_deferred_x_update_parity(bc, orc, n, pc, k, bpr):
     assert np.array_equal(host(s.solution()), o.x)
 
 
-@pytest.mark.parametrize("variant", [2, 5, 7])
+@pytest.mark.parametrize("variant", [2, 5, 7, 9])
 @pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
 def test_tb_variants_bitwise(bc, orc, variant, k):
     """Every temporally blocked layout (square tile / TMA warp-row 16 or 24 warps) gives the
