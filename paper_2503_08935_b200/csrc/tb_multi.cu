@@ -15,6 +15,19 @@
 
 namespace fused {
 
+// warps per CTA of a pass kernel (2 rows each): 20, except the 4-sweep continuation pass
+// whose q / x_{j0-2} register rings need more than the 96 registers 640 threads allow
+constexpr int mp_nw(int K, int mode) { return (mode == MODE_C && K >= 4) ? 16 : 20; }
+
+template <int K, int MODE, bool O2>
+static bcgs_status pass_k(bcgs_ctx c, TbArgs& a, int nz, bool neu)
+{
+    constexpr int NW = mp_nw(K, MODE);
+    if (neu) return launch_tb4_k<K, 2, NW, 4, MODE, 1, false, false, true, O2>(c, a, nz);
+    return launch_tb4_k<K, 2, NW, 4, MODE, 1, false, false, false, O2>(c, a, nz);
+}
+
+#ifndef TB_MULTI_CONT
 // capability: TMA maps over the slab fields and >= 2 passes of >= 2 sweeps
 bool multipass_ok(bcgs_ctx c)
 {
@@ -29,17 +42,8 @@ static int pass_sizes(int k, int* sz)
     return np;
 }
 
-// warps per CTA of a pass kernel (2 rows each): 20, except the 4-sweep continuation pass
-// whose q / x_{j0-2} register rings need more than the 96 registers 640 threads allow
-constexpr int mp_nw(int K, int mode) { return (mode == MODE_C && K >= 4) ? 16 : 20; }
-
-template <int K, int MODE, bool O2>
-static bcgs_status pass_k(bcgs_ctx c, TbArgs& a, int nz, bool neu)
-{
-    constexpr int NW = mp_nw(K, MODE);
-    if (neu) return launch_tb4_k<K, 2, NW, 4, MODE, 1, false, false, true, O2>(c, a, nz);
-    return launch_tb4_k<K, 2, NW, 4, MODE, 1, false, false, false, O2>(c, a, nz);
-}
+// continuation passes: tb_multi_c.cu (a separate translation unit: parallel nvcc)
+bcgs_status pass_cont(bcgs_ctx c, TbArgs& a, int K, int nz, bool o2, bool neu);
 
 template <int K>
 static bcgs_status pass_mode(bcgs_ctx c, TbArgs& a, int nz, int mode, bool o2, bool neu)
@@ -48,8 +52,7 @@ static bcgs_status pass_mode(bcgs_ctx c, TbArgs& a, int nz, int mode, bool o2, b
     case MODE_PLAIN: return pass_k<K, MODE_PLAIN, true>(c, a, nz, neu);
     case MODE_P: return pass_k<K, MODE_P, true>(c, a, nz, neu);
     case MODE_S: return pass_k<K, MODE_S, true>(c, a, nz, neu);
-    default:
-        return o2 ? pass_k<K, MODE_C, true>(c, a, nz, neu) : pass_k<K, MODE_C, false>(c, a, nz, neu);
+    default: return pass_cont(c, a, K, nz, o2, neu);
     }
 }
 
@@ -76,13 +79,7 @@ static bcgs_status pass(bcgs_ctx c, TbArgs& a, int K, int mode, bool o2, bool ne
         return K == 4 ? pass_mode<4>(c, a, nz, mode, true, neu)
                       : pass_mode<3>(c, a, nz, mode, true, neu);
     }
-    if (mode == MODE_C) {
-        switch (K) {
-        case 2: return pass_mode<2>(c, a, nz, MODE_C, o2, neu);
-        case 3: return pass_mode<3>(c, a, nz, MODE_C, o2, neu);
-        case 4: return pass_mode<4>(c, a, nz, MODE_C, o2, neu);
-        }
-    }
+    if (mode == MODE_C && K >= 2 && K <= 4) return pass_cont(c, a, K, nz, o2, neu);
     return fail(c, BCGS_E_INVALID, "multi-pass: no kernel for a pass of %d sweeps", K);
 }
 
@@ -128,5 +125,18 @@ bcgs_status launch_multipass(bcgs_ctx c, TbArgs& a, int mode)
     }
     return BCGS_OK;
 }
+
+#else   // TB_MULTI_CONT: the continuation-pass kernels
+
+bcgs_status pass_cont(bcgs_ctx c, TbArgs& a, int K, int nz, bool o2, bool neu)
+{
+    switch (K) {
+    case 2: return o2 ? pass_k<2, MODE_C, true>(c, a, nz, neu) : pass_k<2, MODE_C, false>(c, a, nz, neu);
+    case 3: return o2 ? pass_k<3, MODE_C, true>(c, a, nz, neu) : pass_k<3, MODE_C, false>(c, a, nz, neu);
+    case 4: return o2 ? pass_k<4, MODE_C, true>(c, a, nz, neu) : pass_k<4, MODE_C, false>(c, a, nz, neu);
+    }
+    return fail(c, BCGS_E_INVALID, "multi-pass: no continuation kernel for %d sweeps", K);
+}
+#endif
 
 }  // namespace fused
