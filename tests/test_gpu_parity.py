@@ -247,6 +247,12 @@ def test_c2_256_full_solve(bc, orc):
     assert_parity(*compare_solve(bc, orc, 256, "gnocomm", 4, 1, 1))
 
 
+def test_c3_512_k24_multipass_first_iteration(bc, orc):
+    """The paper's degree k = 24 at 512³ through the multi-pass kernels (6 passes per
+    application, full-size launch configuration): iteration 1 bitwise."""
+    assert_parity(*compare_solve(bc, orc, 512, "gnocomm", 24, 1, 1, fixed=1))
+
+
 def test_c4_512_block_jacobi_8_slabs(bc, orc):
     """Config C4 at full size: BJ(CI) k=4 on 8 z-slabs (the 8-GPU decomposition emulated
     with blocks_per_rank = 8), first 3 iterations bitwise."""
