@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define BCGS_ABI_VERSION 3
+#define BCGS_ABI_VERSION 4
 #define BCGS_MAX_DEGREE 64       /* Chebyshev degree k (sweeps per application) cap      */
 #define BCGS_HIST_CAP 16384      /* max outer iterations recorded per solve              */
 
@@ -93,14 +93,11 @@ typedef enum {
                                /*     not while profiling or with bcgs_create_local)   */
     BCGS_OPT_PROFILE = 2,      /* 1 = CUDA events around every kernel (bcgs_kernel_times) */
     BCGS_OPT_POLL = 3,         /* iterations launched between done-flag polls (tol mode)  */
-    BCGS_OPT_TB_VARIANT = 4,   /* temporally blocked kernel layout (tuning): 2 = square   */
-                               /* tile (any k, odd nx), 5 = TMA warp-row 16 warps,       */
-                               /* 7 = TMA warp-row 24 warps (default; k <= 4),          */
-                               /* 9 = 7 in x-pair clusters sharing the x-halo through   */
-                               /*     DSMEM (experimental, slower: DESIGN.md §8)         */
-    BCGS_OPT_DEFER_X = 5,      /* 1 = apply x += αp̂ + ωr̂ inside the next p-kernel (off)    */
-    BCGS_OPT_STENCIL_CFG = 6,  /* stencil+dot launch configuration 0..4 (tuning)          */
-    BCGS_OPT_XCONC = 7,        /* 1 = x update on a concurrent low-priority stream (off)  */
+    BCGS_OPT_TB_VARIANT = 4,   /* temporally blocked kernel layout: 7 = TMA warp-row      */
+                               /* kernel (default; 24 warps for k <= 4, 16 warps with     */
+                               /* Neumann faces), 2 = square tile (also used for odd nx). */
+                               /* Other values: BCGS_E_INVALID.  (Options 5-7 of ABI 3,   */
+                               /* layouts measured slower, were removed in ABI 4.)        */
     BCGS_OPT_MULTIPASS = 8,    /* multi-pass temporal blocking (passes of 2..4 sweeps) for */
                                /* degree > value (default 4; clamped to >= 4).  Degrees   */
                                /* above 8 always run multi-pass when the TMA kernels can  */

@@ -22,8 +22,8 @@ STATUS_NAMES = {0: "ok", 1: "invalid", 2: "config", 3: "spectrum", 4: "cuda", 5:
                 6: "not_converged", 7: "breakdown", 8: "state"}
 PC = {"none": 0, "gnocomm": 1, "bj": 2, "g": 3, "bj_bicgs": 4, "g_bicgs": 5}
 MEM_DEVICE, MEM_HOST = 0, 1
-OPT_KERNELS, OPT_GRAPH, OPT_PROFILE, OPT_POLL, OPT_TB_VARIANT, OPT_DEFER_X = 0, 1, 2, 3, 4, 5
-OPT_STENCIL_CFG, OPT_XCONC, OPT_MULTIPASS, OPT_ABLATE, OPT_SYNC2 = 6, 7, 8, 9, 10
+OPT_KERNELS, OPT_GRAPH, OPT_PROFILE, OPT_POLL, OPT_TB_VARIANT = 0, 1, 2, 3, 4
+OPT_MULTIPASS, OPT_ABLATE, OPT_SYNC2 = 8, 9, 10
 HIST_CAP = 16384
 MAX_DEGREE = 64
 

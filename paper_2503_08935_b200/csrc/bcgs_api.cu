@@ -198,8 +198,6 @@ __global__ void k_init_state(DevState* st, double tol, int max_iter, int fixed)
     st->fixed_iters = fixed;
     st->done = DONE_RUNNING;
     st->iter = 0;
-    st->x_applied = 0;
-    st->omega_iter = 0;
     st->pend = DONE_RUNNING;
 }
 
@@ -513,7 +511,7 @@ bcgs_status enqueue_iterations(bcgs_ctx c, int n)
     // graphs: single rank only (multi-rank runs launch directly; NCCL inside captured graphs
     // is supported but not exercised in round 1)
     // (inner-Krylov preconditioners synchronise the host inside an iteration: no graph)
-    if (c->use_graph && !c->profile && !c->lg && c->nranks == 1 && !c->xconc && !inner_pc(c)) {
+    if (c->use_graph && !c->profile && !c->lg && c->nranks == 1 && !inner_pc(c)) {
         if (!c->gexec) {
             cudaGraph_t graph;
             CUDA_OK(c, cudaStreamBeginCapture(c->s, cudaStreamCaptureModeThreadLocal));
@@ -699,9 +697,6 @@ static bcgs_status create_ctx(const bcgs_grid_desc* grid, int32_t rank, int32_t 
     int prio_lo = 0, prio_hi = 0;
     CUDA_OK(c, cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     CUDA_OK(c, cudaStreamCreateWithPriority(&c->s, cudaStreamNonBlocking, prio_hi));
-    CUDA_OK(c, cudaStreamCreateWithPriority(&c->s_x, cudaStreamNonBlocking, prio_lo));
-    CUDA_OK(c, cudaEventCreateWithFlags(&c->ev_omega, cudaEventDisableTiming));
-    CUDA_OK(c, cudaEventCreateWithFlags(&c->ev_xdone, cudaEventDisableTiming));
     CUDA_OK(c, cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
     CUDA_OK(c, cudaMallocHost(&c->h_pinned, 64));
     if (nranks > 1) {
@@ -775,9 +770,6 @@ void bcgs_destroy(bcgs_ctx c)
     if (c->ev_pre) cudaEventDestroy(c->ev_pre);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
     if (c->s_comm) cudaStreamDestroy(c->s_comm);
-    if (c->s_x) cudaStreamSynchronize(c->s_x), cudaStreamDestroy(c->s_x);
-    if (c->ev_omega) cudaEventDestroy(c->ev_omega);
-    if (c->ev_xdone) cudaEventDestroy(c->ev_xdone);
     if (c->ev_done) cudaEventDestroy(c->ev_done);
     if (c->lg) {
         bool last = true;
@@ -803,10 +795,12 @@ bcgs_status bcgs_set_option(bcgs_ctx c, int32_t option, int64_t value)
     case BCGS_OPT_GRAPH: c->use_graph = (int)value; break;
     case BCGS_OPT_PROFILE: c->profile = (int)value; break;
     case BCGS_OPT_POLL: c->poll = std::max<int>(1, (int)value); break;
-    case BCGS_OPT_TB_VARIANT: c->tb_variant = (int)value; break;
-    case BCGS_OPT_DEFER_X: c->defer_x_opt = (int)value; break;
-    case BCGS_OPT_STENCIL_CFG: c->stencil_cfg = (int)value; break;
-    case BCGS_OPT_XCONC: c->xconc_opt = (int)value; break;
+    case BCGS_OPT_TB_VARIANT:
+        if (value != 2 && value != 7)
+            return fail(c, BCGS_E_INVALID, "temporally blocked layout %lld: 2 or 7",
+                        (long long)value);
+        c->tb_variant = (int)value;
+        break;
     case BCGS_OPT_MULTIPASS: c->mp_min = std::max<int>(4, (int)value); break;
     case BCGS_OPT_ABLATE: c->ablate = (int)(value & 3); break;
     case BCGS_OPT_SYNC2: c->sync2_opt = (int)value; drop_graph(c); break;
@@ -927,23 +921,27 @@ bcgs_status bcgs_begin(bcgs_ctx c, double rel_tol, int32_t max_iter, int32_t fix
     if (fixed_iters < 0 || fixed_iters > BCGS_HIST_CAP || max_iter < 0 ||
         (fixed_iters == 0 && (max_iter < 1 || max_iter > BCGS_HIST_CAP)))
         return fail(c, BCGS_E_INVALID, "iteration counts out of range (cap %d)", BCGS_HIST_CAP);
+    c->begun = 0;   // a failed begin leaves no solve to iterate
+    // configuration checks first: no device work on a configuration error
     TRY(validate_pc(c));
+    if (c->sync2_opt &&   // R31 is built on the fused path (vectorised streaming kernels)
+        !(c->kernels == 1 && fused::supported(c, c->degree, c->pc != BCGS_PC_NONE) &&
+          c->lay.nx % 2 == 0 && !(c->pc == BCGS_PC_CHEB_G && c->nranks > 1)))
+        return fail(c, BCGS_E_CONFIG, "BCGS_OPT_SYNC2 needs the fused path (kernels = 1, a "
+                    "Chebyshev preconditioner, even nx)");
     TRY(enter(c));
     c->t0 = std::chrono::steady_clock::now();
     const int64_t n = npts(c);
     const size_t bytes = sizeof(double) * (size_t)n;
     k_init_state<<<1, 1, 0, c->s>>>(c->st, rel_tol, max_iter, fixed_iters);
     c->in_iters = 0;
-    c->sync2 = 0;
-    if (c->sync2_opt) {   // R31 is built on the fused path (vectorised streaming kernels)
-        if (!(c->kernels == 1 && fused::supported(c, c->degree, c->pc != BCGS_PC_NONE) &&
-              c->lay.nx % 2 == 0 && !(c->pc == BCGS_PC_CHEB_G && c->nranks > 1)))
-            return fail(c, BCGS_E_CONFIG, "BCGS_OPT_SYNC2 needs the fused path (kernels = 1, a "
-                        "Chebyshev preconditioner, even nx)");
-        c->sync2 = 1;
-    }
-    // Alg. 3 l.1-4: r0 = b - A x0; r~ = r0; p0 = r0; ρ0 = r~ᵀr0
-    if (c->have_x0) {
+    c->sync2 = c->sync2_opt ? 1 : 0;
+    // Alg. 3 l.1-4: r0 = b - A x0; r~ = r0; p0 = r0; ρ0 = r~ᵀr0.  The initial
+    // guess set by bcgs_set_initial_guess applies to this solve only (V_X then holds the
+    // iterate); later solves start from x0 = 0 unless a new guess is set (R21).
+    const bool x0 = c->have_x0;
+    c->have_x0 = 0;
+    if (x0) {
         TRY(halo(c, F(c, V_X)));
         ref::k_stencil_dot<0><<<stencil_grid(c), dim3(ref::BX, ref::BY), 0, c->s>>>(
             F(c, V_X), nullptr, F(c, V_R), ref_grid(c, (int)c->lay.L), 0, nullptr, nullptr);
@@ -954,7 +952,6 @@ bcgs_status bcgs_begin(bcgs_ctx c, double rel_tol, int32_t max_iter, int32_t fix
     }
     CUDA_OK(c, cudaMemcpyAsync(F(c, V_RT), F(c, V_R), bytes, cudaMemcpyDeviceToDevice, c->s));
     CUDA_OK(c, cudaMemcpyAsync(F(c, V_P), F(c, V_R), bytes, cudaMemcpyDeviceToDevice, c->s));
-    fused::on_begin(c);
     ref::k_dot2<2><<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(F(c, V_B), F(c, V_B), F(c, V_RT),
                                                            F(c, V_R), n, c->part);
     CUDA_OK(c, cudaGetLastError());
@@ -997,7 +994,6 @@ bcgs_status bcgs_finish(bcgs_ctx c, bcgs_report* out)
 {
     if (!c) return BCGS_E_INVALID;
     if (!c->begun) return fail(c, BCGS_E_STATE, "bcgs_finish before bcgs_begin");
-    TRY(fused::flush_x(c));
     int32_t done = 0, iter = 0;
     TRY(poll_state(c, &done, &iter));
     // true residual (R22): ||b - A x|| / ||b||, once
@@ -1084,7 +1080,6 @@ bcgs_status bcgs_get_solution(bcgs_ctx c, double* x, int32_t mem)
 {
     if (!c || !x) return BCGS_E_INVALID;
     TRY(enter(c));
-    TRY(fused::flush_x(c));
     const size_t bytes = sizeof(double) * (size_t)npts(c);
     CUDA_OK(c, cudaMemcpyAsync(x, F(c, V_X), bytes,
                                mem == BCGS_MEM_HOST ? cudaMemcpyDeviceToHost

@@ -29,19 +29,20 @@ constexpr size_t kAlign = 256;
 enum KClass {
     KC_PRECOND = 0, KC_STENCIL1, KC_AXPY, KC_STENCIL2, KC_UPDATE_XR, KC_UPDATE_P,
     KC_FINALIZE, KC_HALO, KC_ALLGATHER, KC_SCALARS, KC_FUSED_P1, KC_FUSED_P2, KC_FUSED_XR,
-    KC_XCONC, KC_COUNT
+    KC_COUNT
 };
 inline const char* kClassName[KC_COUNT] = {
     "precond_sweep", "stencil_dot1", "axpy_s", "stencil_dot2", "update_xr", "update_p",
-    "finalize", "halo", "allgather", "scalars", "fused_p_cheb", "fused_s_cheb", "fused_xr",
-    "x_update_concurrent"};
+    "finalize", "halo", "allgather", "scalars", "fused_p_cheb", "fused_s_cheb", "fused_xr"};
 
 inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+constexpr int V_COUNT_MAX = 17;
 
 struct Layout {
     int64_t nx, ny, nz, L, plane, vec_elems;   // vec_elems = (L + 2) * plane
     int64_t n_part;
-    size_t off_vec[18];
+    size_t off_vec[V_COUNT_MAX];
     int64_t ext_elems;
     size_t off_ext[3];
     size_t off_state, off_hist, off_scal, off_part, off_rank, off_gath, total;
@@ -49,7 +50,7 @@ struct Layout {
 
 constexpr int V_X = 0, V_R = 1, V_RT = 2, V_P = 3, V_PH = 4, V_RH = 5, V_W = 6, V_T = 7,
               V_B = 8, V_C1 = 9, V_C2 = 10, V_IO = 11, V_W2 = 12, V_P2 = 13,
-              V_S = 14, V_PH2 = 15, V_Y3 = 16, V_Y4 = 17, V_COUNT = 18;
+              V_S = 14, V_Y3 = 15, V_Y4 = 16, V_COUNT = 17;
 // V_C1, V_C2, V_Y3, V_Y4: Chebyshev iterates (reference sweeps; multi-pass buffer pairs)
 
 inline int64_t stencil_blocks(int64_t nx, int64_t ny, int64_t L)
@@ -143,14 +144,6 @@ struct bcgs_ctx_s {
     dd *part = nullptr, *rank_out = nullptr, *gath = nullptr;
     double* h_pinned = nullptr;    // small pinned buffer for flag polls
     // options
-    int defer_x = 0;                  // fused path: a11 applied inside the next p-kernel
-    int defer_x_opt = 0;
-    int stencil_cfg = 0;              // BCGS_OPT_STENCIL_CFG (k_stream.cuh launch configs)
-    int xconc_opt = 0;                // BCGS_OPT_XCONC: x update on a concurrent stream (off)
-    int xconc = 0;                    // active for the current solve
-    int it_host = 0;                  // iterations enqueued since begin (host parity)
-    cudaStream_t s_x = nullptr;       // low-priority stream of the concurrent x update
-    cudaEvent_t ev_omega = nullptr, ev_xdone = nullptr;              // BCGS_OPT_DEFER_X (measured slower at 512^3: off)
     int kernels = 1, use_graph = 1, profile = 0, poll = 8, tb_variant = 7;
     int sync2_opt = 0, sync2 = 0;   // BCGS_OPT_SYNC2 (R31); active for the current solve
     int ablate = 0;   // BCGS_OPT_ABLATE: 1 skip halos, 2 skip cross-rank reductions (timing)

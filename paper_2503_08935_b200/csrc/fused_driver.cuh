@@ -40,19 +40,18 @@ __global__ void k_commit(DevState* st)
     if (!st->done && st->pend) st->done = st->pend;
 }
 
-// tile (TX, TY) of a kernel variant for degree k
-void variant_tile(int variant, int k, int* tx, int* ty)
+// output tile (TX, TY) of the kernel launch_variant picks for degree k (tb_launch.cuh)
+void variant_tile(bcgs_ctx c, bool neu, int k, int* tx, int* ty)
 {
     const int hx = (k + 1) / 2 * 2;                        // TMA: even x-halo
-    if (variant == 2 || k > 5) {
+    const bool tma = c->tb_variant != 2 && c->lay.nx % 2 == 0;
+    if (tma && neu && k <= 5) {
+        *tx = 32 - 2 * hx; *ty = 32 - 2 * k;               // 16 warps x RY = 2
+    } else if (tma && !neu && k <= 4) {
+        *tx = 32 - 2 * hx; *ty = 48 - 2 * k;               // 24 warps x RY = 2
+    } else {                                               // square tile
         *tx = 32; *ty = 16;
         if (k >= 7) { *tx = 16; *ty = 8; } else if (k >= 5) { *tx = 32; *ty = 8; }
-    } else if (variant == 7 && k <= 4) {
-        *tx = 32 - 2 * hx; *ty = 48 - 2 * k;               // 24 warps x RY = 2
-    } else if (variant == 9 && k <= 4) {
-        *tx = 32 - hx; *ty = 48 - 2 * k;                   // x-pair clusters: per CTA
-    } else {
-        *tx = 32 - 2 * hx; *ty = 32 - 2 * k;               // 16 warps x RY = 2 (variant 5)
     }
 }
 
@@ -80,9 +79,7 @@ bcgs_status launch_tb(bcgs_ctx c, TbArgs& a)
     // waves * (planes per chunk + 2k).
     int tx, ty;
     const bool neu = a.bc.m || a.bc.zlo >= 0 || a.bc.zhi >= 0;   // see launch_variant
-    variant_tile(neu ? ((c->tb_variant != 2 && k <= 5 && a.nx % 2 == 0) ? 5 : 2)
-                     : (MODE == MODE_P && c->defer_x) ? 5 : c->tb_variant,
-                 k, &tx, &ty);
+    variant_tile(c, neu, k, &tx, &ty);
     if (a.ext) a.Lb = a.zo1 - a.zo0;   // chunks over the output planes, one "block"
     const int nblk = a.ext ? 1 : c->bpr;
     const int64_t tiles = ((a.nx + tx - 1) / tx) * (int64_t)((a.ny + ty - 1) / ty) * nblk;
@@ -146,41 +143,6 @@ bcgs_status precond_apply(bcgs_ctx c, const double* q, double* out)
     return launch_tb<MODE_PLAIN>(c, a);
 }
 
-void on_begin(bcgs_ctx c)
-{
-    c->it_host = 0;
-    const bool g_multi = c->pc == BCGS_PC_CHEB_G && c->nranks > 1;   // ref path (k-deep halos)
-    c->xconc = (c->xconc_opt && !g_multi && c->kernels == 1 && c->pc != BCGS_PC_NONE &&
-                (c->lay.nx % 2) == 0 && !c->defer_x_opt &&
-                c->degree <= KMAX_TB && supported(c, c->degree, true)) ? 1 : 0;
-    if (c->xconc) {   // s_x starts after the setup (x = x0 written on s)
-        cudaEventRecord(c->ev_omega, c->s);
-        cudaStreamWaitEvent(c->s_x, c->ev_omega, 0);
-        cudaEventRecord(c->ev_xdone, c->s_x);
-    }
-    const bool neu = c->mbc.m || c->mbc.zlo >= 0 || c->mbc.zhi >= 0;
-    if (c->sync2) c->xconc = 0;
-    c->defer_x = (c->defer_x_opt && !c->sync2 && !g_multi && !neu && c->kernels == 1 &&
-                  c->pc != BCGS_PC_NONE && (c->lay.nx % 2) == 0 && c->degree <= c->mp_min &&
-                  defer_x_ok(c)) ? 1 : 0;
-}
-
-// deferred-x mode: bring x up to date (idempotent; stream-ordered)
-bcgs_status flush_x(bcgs_ctx c)
-{
-    if (c->xconc && c->begun) {   // join the concurrent x updates into the main stream
-        CUDA_OK(c, cudaEventRecord(c->ev_xdone, c->s_x));
-        CUDA_OK(c, cudaStreamWaitEvent(c->s, c->ev_xdone, 0));
-        return BCGS_OK;
-    }
-    if (!c->defer_x || !c->begun) return BCGS_OK;
-    stream::k_xflush<<<kEwBlocks, 256, 0, c->s>>>(F(c, V_X), F(c, V_PH), F(c, V_RH), npts(c),
-                                                 c->st);
-    stream::k_xmark<<<1, 1, 0, c->s>>>(c->st);
-    CUDA_OK(c, cudaGetLastError());
-    return BCGS_OK;
-}
-
 // a3 + a4 (a8 + a9): halo exchange of v overlapped with the stencil+dot of the interior
 // planes 1..L-2 (side stream + events), then the two boundary planes once the ghost planes
 // have arrived.  Writes the Dot2 partials of all launches contiguously; *nparts = count.
@@ -189,19 +151,13 @@ bcgs_status halo_stencil(bcgs_ctx c, double* v, const double* a, double* out, in
                          int* nparts, const double* rt = nullptr)
 {
     const int nx = (int)c->lay.nx, ny = (int)c->lay.ny, L = (int)c->lay.L;
-    const int cfg = std::min(std::max(c->stencil_cfg, 0), stream::NCFG - 1);
-    const dim3 sb(stream::CFG_BX[cfg], stream::CFG_BY[cfg]);
+    const dim3 sb(stream::SBX, stream::SBY);
     int nb = 0;
     auto launch = [&](int kb, int ke) {
-        const dim3 g = stream::stencil2_grid(nx, ny, ke - kb, cfg);
+        const dim3 g = stream::stencil2_grid(nx, ny, ke - kb);
         dd* pp = c->part + (int64_t)nb * ND;
-        switch (cfg) {
-        case 1: stream::k_stencil2_dot<ND, 32, 8, 16><<<g, sb, 0, c->s>>>(v, a, rt, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st); break;
-        case 2: stream::k_stencil2_dot<ND, 32, 4, 16><<<g, sb, 0, c->s>>>(v, a, rt, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st); break;
-        case 3: stream::k_stencil2_dot<ND, 64, 4, 8><<<g, sb, 0, c->s>>>(v, a, rt, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st); break;
-        case 4: stream::k_stencil2_dot<ND, 32, 16, 4><<<g, sb, 0, c->s>>>(v, a, rt, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st); break;
-        default: stream::k_stencil2_dot<ND, 32, 8, 8><<<g, sb, 0, c->s>>>(v, a, rt, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st); break;
-        }
+        stream::k_stencil2_dot<ND, stream::SBX, stream::SBY, stream::SZC><<<g, sb, 0, c->s>>>(
+            v, a, rt, out, nx, ny, kb, ke, c->h2inv, c->mbc, pp, c->st);
         nb += (int)(g.x * g.y * g.z);
     };
     Prof pf(c, kc, 24.0 * npts(c));
@@ -262,11 +218,7 @@ bcgs_status iteration(bcgs_ctx c)
 {
     const int64_t n = npts(c);
     DevState* st = c->st;
-    // concurrent-x mode: p̂ alternates between two buffers by iteration parity so that the
-    // x update of iteration i (reading p̂_i on s_x) overlaps the p-kernel of iteration i+1
-    const int par = c->xconc ? (c->it_host & 1) : 0;
-    double* ph = F(c, par ? V_PH2 : V_PH);
-    c->it_host += 1;
+    double* ph = F(c, V_PH);
     ref::Grid g = ref_grid(c, (int)c->lay.L);
     dim3 sg = stencil_grid(c), sb(ref::BX, ref::BY);
     const int nsb = (int)(sg.x * sg.y * sg.z);
@@ -279,10 +231,8 @@ bcgs_status iteration(bcgs_ctx c)
         a.side_a = F(c, V_P);
         a.side_b = F(c, V_P2);
         a.out = ph;
-        a.x = F(c, V_X);
-        a.rh = F(c, V_RH);
         a.st = st;
-        Prof pf(c, KC_FUSED_P1, (c->defer_x ? 72.0 : 40.0) * n);
+        Prof pf(c, KC_FUSED_P1, 40.0 * n);
         TRY(launch_tb<MODE_P>(c, a));
     }
     const bool vec = (c->lay.nx % 2) == 0;   // 16-byte rows: vectorised streaming kernels
@@ -296,8 +246,6 @@ bcgs_status iteration(bcgs_ctx c)
                                                   c->part, st);
     }
     TRY(reduce<1>(c, np1, STAGE_ALPHA));
-    // r̂ is overwritten by K2: the previous iteration's concurrent x update must be done
-    if (c->xconc) CUDA_OK(c, cudaStreamWaitEvent(c->s, c->ev_xdone, 0));
     {   // K2: a6 + a7
         TbArgs a{};
         a.r = F(c, V_R);
@@ -330,24 +278,7 @@ bcgs_status iteration(bcgs_ctx c)
         return BCGS_OK;
     }
     TRY(reduce<2>(c, np2, STAGE_OMEGA));
-    if (c->xconc) {   // a11 on the low-priority stream, overlapping a12 and the next p-kernel
-        CUDA_OK(c, cudaEventRecord(c->ev_omega, c->s));
-        CUDA_OK(c, cudaStreamWaitEvent(c->s_x, c->ev_omega, 0));
-        {
-            Prof pf(c, KC_XCONC, 32.0 * n, c->s_x);
-            stream::k_xupd_conc<<<kNumSMs, 256, 0, c->s_x>>>(
-                (double2*)F(c, V_X), (const double2*)F(c, V_PH), (const double2*)F(c, V_PH2),
-                (const double2*)F(c, V_RH), n / 2, st);
-            stream::k_xmark_conc<<<1, 1, 0, c->s_x>>>(st);
-        }
-        CUDA_OK(c, cudaEventRecord(c->ev_xdone, c->s_x));
-    }
-    if (vec && (c->defer_x || c->xconc)) {   // a12 only: x updated elsewhere
-        Prof pf(c, KC_FUSED_XR, 32.0 * n);
-        stream::k_update_r2<<<kEwBlocks, 256, 0, c->s>>>(
-            (const double2*)F(c, V_S), (double2*)F(c, V_R), (const double2*)F(c, V_T),
-            (const double2*)F(c, V_RT), n / 2, c->part, st);
-    } else {
+    {
         Prof pf(c, KC_FUSED_XR, 64.0 * n);
         if (vec)
             stream::k_update_xr2<2><<<kEwBlocks, 256, 0, c->s>>>(

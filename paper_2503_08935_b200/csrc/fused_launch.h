@@ -2,7 +2,6 @@
 // instantiated once per degree K in tb_k<K>.cu (parallel compilation).
 #pragma once
 namespace fused {
-bool defer_x_ok(bcgs_ctx c);   // tb_k1.cu
 bcgs_status launch_multipass(bcgs_ctx c, TbArgs& a, int mode);   // tb_multi.cu
 template <int K, int MODE>
 bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz);

@@ -41,8 +41,6 @@ struct TbArgs {
     // MODE_C: q = input field (qsel = 0) or the p buffer the p-kernel of this iteration
     // wrote (qsel = 1: selected by the iteration parity like side_a/side_b)
     int qsel;
-    double* x;            // MODE_P + XUPD: x_{i-1} += α p̂_{i-1} + ω r̂_{i-1} (deferred a11)
-    const double* rh;     //   r̂ of the previous iteration
     int nx, ny, Lb, zch, nchunk;
     // extended-slab mode (G(CI), ext = 1): zero ghosts outside planes [zv0, zv1), outputs
     // for planes [zo0, zo1) only, one block; plane indices are extended-slab indices.
@@ -282,7 +280,6 @@ inline bool supported(bcgs_ctx c, int degree, bool has_pc)
 }
 bcgs_status iteration(bcgs_ctx c);
 bcgs_status iteration_none(bcgs_ctx c);
-void on_begin(bcgs_ctx c);
 bool precond_supported(bcgs_ctx c);
 bcgs_status precond_apply(bcgs_ctx c, const double* q, double* out);
 bcgs_status precond_g_tb(bcgs_ctx c, const double* E, double* out, int v0, int v1);

@@ -13,11 +13,7 @@
 
 namespace stream {
 
-constexpr int SBX = 32, SBY = 8, SZC = 8;   // default: threads (x pairs) x rows, planes/thread
-// launch configurations selectable with BCGS_OPT_STENCIL_CFG (tuning)
-constexpr int NCFG = 5;
-constexpr int CFG_BX[NCFG] = {32, 32, 32, 64, 32}, CFG_BY[NCFG] = {8, 8, 4, 4, 16},
-              CFG_ZC[NCFG] = {8, 16, 16, 8, 4};
+constexpr int SBX = 32, SBY = 8, SZC = 8;   // threads (x pairs) x rows, planes per thread
 
 // w = A v (global operator; ghost planes hold halo data or zeros) and Dot2 partials of
 // a·w (ND >= 1) and w·w (ND == 2).  Each thread owns 2 adjacent x points of one row and
@@ -98,11 +94,10 @@ k_stencil2_dot(const double* __restrict__ v,
     }
 }
 
-inline dim3 stencil2_grid(int64_t nx, int64_t ny, int64_t nplanes, int cfg = 0)
+inline dim3 stencil2_grid(int64_t nx, int64_t ny, int64_t nplanes)
 {
-    return dim3((unsigned)((nx / 2 + CFG_BX[cfg] - 1) / CFG_BX[cfg]),
-                (unsigned)((ny + CFG_BY[cfg] - 1) / CFG_BY[cfg]),
-                (unsigned)((nplanes + CFG_ZC[cfg] - 1) / CFG_ZC[cfg]));
+    return dim3((unsigned)((nx / 2 + SBX - 1) / SBX), (unsigned)((ny + SBY - 1) / SBY),
+                (unsigned)((nplanes + SZC - 1) / SZC));
 }
 
 // a11 + a12: x = fma(ω, r̂, fma(α, p̂, x)); r = fma(-ω, t, s); partials r~·r, r·r.
@@ -174,109 +169,6 @@ __global__ void __launch_bounds__(256) k_update_xr2(double2* __restrict__ x,
     }
     if (ND) block_reduce_dd<2>(p, q, part + (int64_t)blockIdx.x * 2);
 }
-
-// a12 alone (deferred-x mode, x is updated inside the next p-kernel): r = fma(-ω, t, s);
-// partials r~·r and r·r.
-__global__ void __launch_bounds__(256) k_update_r2(const double2* __restrict__ s,
-                                                   double2* __restrict__ r,
-                                                   const double2* __restrict__ t,
-                                                   const double2* __restrict__ rt, int64_t n2,
-                                                   dd* __restrict__ part,
-                                                   const DevState* __restrict__ st)
-{
-    if (st->done) return;
-    const double omega = st->omega;
-    double p[2] = {0.0, 0.0}, q[2] = {0.0, 0.0};
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    for (; c + 3 * stride < n2; c += 4 * stride) {
-        double2 vs[4], vt[4], vrt[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            vs[u] = __ldg(s + c + u * stride);
-            vt[u] = __ldg(t + c + u * stride);
-            vrt[u] = __ldg(rt + c + u * stride);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            double2 rn;
-            rn.x = upd_r(vs[u].x, vt[u].x, omega);
-            rn.y = upd_r(vs[u].y, vt[u].y, omega);
-            r[c + u * stride] = rn;
-            dot2_acc(p[0], q[0], vrt[u].x, rn.x);
-            dot2_acc(p[0], q[0], vrt[u].y, rn.y);
-            dot2_acc(p[1], q[1], rn.x, rn.x);
-            dot2_acc(p[1], q[1], rn.y, rn.y);
-        }
-    }
-    for (; c < n2; c += stride) {
-        const double2 vs = s[c], vt = t[c], vrt = rt[c];
-        double2 rn;
-        rn.x = upd_r(vs.x, vt.x, omega);
-        rn.y = upd_r(vs.y, vt.y, omega);
-        r[c] = rn;
-        dot2_acc(p[0], q[0], vrt.x, rn.x);
-        dot2_acc(p[0], q[0], vrt.y, rn.y);
-        dot2_acc(p[1], q[1], rn.x, rn.x);
-        dot2_acc(p[1], q[1], rn.y, rn.y);
-    }
-    block_reduce_dd<2>(p, q, part + (int64_t)blockIdx.x * 2);
-}
-
-// deferred-x mode: apply the last completed iteration's x update if no p-kernel did.
-__global__ void k_xflush(double* __restrict__ x, const double* __restrict__ ph,
-                         const double* __restrict__ rh, int64_t n, const DevState* __restrict__ st)
-{
-    if (st->iter < 1 || st->x_applied == st->iter) return;
-    const double alpha = st->alpha, omega = st->omega;
-    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
-         c += (int64_t)gridDim.x * blockDim.x)
-        x[c] = upd_x(x[c], ph[c], rh[c], alpha, omega);
-}
-
-__global__ void k_xmark(DevState* st) { st->x_applied = st->iter; }
-
-// concurrent-x mode (a11 on its own low-priority stream, overlapping the ALU-bound
-// Chebyshev kernel of the next iteration): x = fma(ω, r̂, fma(α, p̂, x)) for iteration
-// omega_iter, with p̂ from the buffer of that iteration's parity and the (α, ω) snapshot.
-__global__ void __launch_bounds__(256) k_xupd_conc(double2* __restrict__ x,
-                                                   const double2* __restrict__ ph_a,
-                                                   const double2* __restrict__ ph_b,
-                                                   const double2* __restrict__ rh, int64_t n2,
-                                                   const DevState* __restrict__ st)
-{
-    const int it = st->omega_iter;
-    if (it < 1 || it == st->x_applied) return;
-    const double alpha = st->xa, omega = st->xw;
-    const double2* __restrict__ ph = ((it - 1) & 1) ? ph_b : ph_a;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    for (; c + 3 * stride < n2; c += 4 * stride) {
-        double2 vx[4], vp[4], vr[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            vx[u] = x[c + u * stride];
-            vp[u] = __ldg(ph + c + u * stride);
-            vr[u] = __ldg(rh + c + u * stride);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            double2 o;
-            o.x = upd_x(vx[u].x, vp[u].x, vr[u].x, alpha, omega);
-            o.y = upd_x(vx[u].y, vp[u].y, vr[u].y, alpha, omega);
-            x[c + u * stride] = o;
-        }
-    }
-    for (; c < n2; c += stride) {
-        const double2 vx = x[c], vp = ph[c], vr = rh[c];
-        double2 o;
-        o.x = upd_x(vx.x, vp.x, vr.x, alpha, omega);
-        o.y = upd_x(vx.y, vp.y, vr.y, alpha, omega);
-        x[c] = o;
-    }
-}
-
-__global__ void k_xmark_conc(DevState* st) { st->x_applied = st->omega_iter; }
 
 // M = I (plain Bi-CGSTAB, P:145-174 / Alg. 3 with p̂ = p, r̂ = s): a6 s = fma(-α, w, r) into
 // its own buffer, and a14 p = fma(β, fma(-ω, w, p), r) in place (element-wise), 16-byte I/O.

@@ -53,66 +53,18 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-// ---- x-pair clusters (XP): peer shared memory and cluster-scope mbarriers
-__device__ __forceinline__ uint32_t cluster_ctarank()
-{
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-
-__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank)
-{
-    uint32_t d;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(addr), "r"(rank));
-    return d;
-}
-
-// remote store into the peer's shared memory that signals the peer's mbarrier (tx bytes)
-__device__ __forceinline__ void st_async_f64(uint32_t addr, double v, uint32_t remote_bar)
-{
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];"
-                 ::"r"(addr), "d"(v), "r"(remote_bar) : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t remote_bar)
-{
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity)
-{
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAITC_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAITC_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ void cluster_sync_all()
-{
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
-                 ::: "memory");
-}
-
 struct TbMaps {
     CUtensorMap q, r, w, pa, pb;   // 3-D maps (nx, ny, L) of the slab fields, box (32, EY, 1)
 };
 
-template <int K, int RY, int NW, int NS, bool XP = false>
+template <int K, int RY, int NW, int NS>
 struct Tb4Shape {
     // x-halo HX = K rounded up to even: TMA needs 16-byte aligned box starts, so the first
     // staged column (tile x0 - HX) must be even.  For odd K the outermost column is unused.
     static constexpr int HX = (K + 1) / 2 * 2;
     static constexpr int EX = 32, EY = NW * RY, TX = EX - 2 * HX, TY = EY - 2 * K;
-    // XP (x-pair cluster): level-plane rows carry a guard column on each side that the
-    // peer CTA fills with its edge column (EXS = 34), the plane row of lane l at OFF + l
-    static constexpr int EXS = XP ? EX + 2 : EX, OFF = XP ? 1 : 0;
-    static constexpr int PAD = EXS;
-    static constexpr int PLANE = EXS * EY + 2 * PAD;      // level plane incl. guard rows
+    static constexpr int PAD = EX;
+    static constexpr int PLANE = EX * EY + 2 * PAD;       // level plane incl. guard rows
     static constexpr int BOX = EX * EY;                   // staged input box (doubles)
     // z-ring of the level-0 planes (>= K + 1, multiple of 3 for the phase-unrolled windows);
     // at least 6 so that, with NS dividing QW / 2, the stage slot, its mbarrier parity and the
@@ -122,19 +74,15 @@ struct Tb4Shape {
     static constexpr size_t level_bytes = sizeof(double) * 2 * K * PLANE;
     static constexpr size_t stage_bytes = sizeof(double) * (size_t)NS * 3 * BOX;
     static constexpr size_t smem = level_bytes + stage_bytes + 128;
-    static constexpr size_t xupd_bytes = sizeof(double) * 2 * 3 * NW * 32 * RY;
 };
 
-template <int K, int RY, int NW, int NS, int MODE, bool XUPD = false, bool XSH = false,
-          bool NEU = false, bool O2 = false, bool XP = false>
+template <int K, int RY, int NW, int NS, int MODE, bool NEU = false, bool O2 = false>
 struct Tb4Thread {
-    using S = Tb4Shape<K, RY, NW, NS, XP>;
-    static constexpr int EXS = S::EXS;
+    using S = Tb4Shape<K, RY, NW, NS>;
+    static constexpr int EXS = S::EX;
     static constexpr int EX = S::EX, TX = S::TX, TY = S::TY, PLANE = S::PLANE, QW = S::QW,
                          BOX = S::BOX;
     static constexpr bool CT = S::CT;
-    // XP: bytes the peer sends per step (its edge lane of every warp: RY rows x levels 0..K-1)
-    static constexpr uint32_t XP_BYTES = (uint32_t)(NW * RY * K * sizeof(double));
 
     double qw[QW][RY];                   // level 0 (q; MODE_C: x_{j0-1})
     double win[K > 1 ? K : 2][3][RY];
@@ -153,12 +101,6 @@ struct Tb4Thread {
     double alpha, beta, omega;
     const CUtensorMap* pmap;
     double* side;
-    bool xdo;          // XUPD: this launch applies the previous iteration's x update
-    uint32_t peer_sm;  // XP: shared::cluster address of the peer CTA's level planes
-    uint64_t* pbar;    // XP: [2] mbarriers the peer arrives on after publishing a step
-    uint32_t peer_pbar;   // XP: shared::cluster address of the peer's pbar[0]
-    int edge;          // XP: this CTA's lane whose value the peer needs (31 or 0)
-    double* xsm;       // XUPD: [2][3][XN] cp.async landing buffers
 
     static constexpr int ninputs() { return MODE == MODE_PLAIN ? 1 : (MODE == MODE_S ? 2 : 3); }
 
@@ -194,23 +136,6 @@ struct Tb4Thread {
     template <int PH, bool MASK>
     __device__ __forceinline__ void step(int t)
     {
-        // ---- deferred a11 of the previous iteration on plane t - K.  Its operands were
-        //      copied to shared memory by cp.async issued one step earlier (no registers held
-        //      across the sweeps); p̂_{i-1}(t-K) is read here, before this step's level K
-        //      overwrites it with p̂_i.  Then the copies for plane t+1-K are issued.
-        if (XUPD && xdo) {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-            const int mx = t - K;
-            if (mx >= c0 && mx < c1) {
-                const double* xb = xsm + (size_t)(t & 1) * 3 * XN + threadIdx.x * RY;
-#pragma unroll
-                for (int r = 0; r < RY; ++r)
-                    if (in_tile[r])
-                        a->x[(size_t)(col[r] + plane * (uint32_t)mx)] =
-                            upd_x(xb[r], xb[XN + r], xb[2 * XN + r], alpha, omega);
-            }
-            xissue(t + 1);
-        }
         // ---- level 0 from the TMA stage of plane t
         double q0[RY], qn[RY], y2n[RY];
         // steps run in blocks of QW from t0, so (t - t0) % QW == PH: with CT the stage slot,
@@ -253,18 +178,11 @@ struct Tb4Thread {
             if (MODE == MODE_C) qr[PH % QW][r] = qn[r];
         }
         const double* prev = sm + S::PAD + (CT ? ((PH + 1) & 1) : ((t - t0 + 1) & 1)) * (K * PLANE);
-        if (XP) {   // the peer's edge columns of step t-1 (phase n-1, pbar[(n-1) & 1])
-            const int n = t - t0;
-            if (n >= 1) {
-                mbar_wait(&pbar[(n - 1) & 1], ((n - 1) >> 1) & 1);
-                if (threadIdx.x == 0) mbar_expect_tx(&pbar[(n - 1) & 1], XP_BYTES);   // phase n+1
-            }
-        }
 #pragma unroll
         for (int j = 1; j <= K; ++j) {
             const int m = t - j;
             if (wdy <= K - j) {                       // warp-uniform level skip
-                const double* pl = prev + (j - 1) * PLANE + ey0 * EXS + S::OFF + lane;
+                const double* pl = prev + (j - 1) * PLANE + ey0 * EXS + lane;
                 bool mok = true;
                 if (MASK) mok = (unsigned)(m - b0) < (unsigned)(b1 - b0);
                 double v[RY];
@@ -286,10 +204,8 @@ struct Tb4Thread {
                         yc_p = r < RY - 1 ? win[j - 1][(PH + 2) % 3][r < RY - 1 ? r + 1 : 0]
                                           : pl[(r + 1) * EXS];
                     }
-                    // x-neighbours: from the neighbouring lanes' registers (XSH; the warp is one
-                    // extended row segment and the x-halo lanes are never active) or smem
-                    double xm = XSH ? __shfl_up_sync(0xffffffffu, zc, 1) : pl[r * EXS - 1];
-                    double xp = XSH ? __shfl_down_sync(0xffffffffu, zc, 1) : pl[r * EXS + 1];
+                    double xm = pl[r * EXS - 1];   // x-neighbours from the level plane
+                    double xp = pl[r * EXS + 1];
                     // R27 mirror ghosts: only next to a physical face, which only masked
                     // steps reach (non-interior tiles; the prologue covers plane b0)
                     if (NEU && MASK) {
@@ -334,23 +250,12 @@ struct Tb4Thread {
             for (int r = 0; r < RY; ++r) y2c[r] = y2n[r];
         }
         double* cur = sm + S::PAD + (CT ? (PH & 1) : ((t - t0) & 1)) * (K * PLANE) + ey0 * EXS +
-                      S::OFF + lane;
+                      lane;
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
-            if (XSH && r > 0 && r < RY - 1) continue;   // shuffles: only segment ends are read
             cur[r * EXS] = q0[r];
 #pragma unroll
             for (int j = 1; j < K; ++j) cur[j * PLANE + r * EXS] = win[j][PH % 3][r];
-            if (XP && lane == edge) {   // into the peer's guard column (mirror side)
-                const uint32_t off = (uint32_t)(reinterpret_cast<char*>(cur + r * EXS) -
-                                                reinterpret_cast<char*>(sm)) +
-                                     (edge == 0 ? 256u : (uint32_t)(-256));   // +-32 columns
-                const uint32_t rb = peer_pbar + 8u * (uint32_t)((t - t0) & 1);
-                st_async_f64(peer_sm + off, q0[r], rb);
-#pragma unroll
-                for (int j = 1; j < K; ++j)
-                    st_async_f64(peer_sm + off + (uint32_t)(j * PLANE * 8), win[j][PH % 3][r], rb);
-            }
         }
         __syncthreads();
         // the stage of plane t is free again: refill it with plane t + NS
@@ -360,27 +265,6 @@ struct Tb4Thread {
         }
     }
 
-    // XUPD: cp.async the a11 operands (x, p̂, r̂) of plane tt - K into slot tt & 1
-    static constexpr int XN = NW * 32 * RY;
-    __device__ __forceinline__ void xissue(int tt)
-    {
-        const int mx = tt - K;
-        if (mx >= c0 && mx < c1) {
-            double* xb = xsm + (size_t)(tt & 1) * 3 * XN + threadIdx.x * RY;
-#pragma unroll
-            for (int r = 0; r < RY; ++r) {
-                if (!in_tile[r]) continue;
-                const size_t e = col[r] + plane * (uint32_t)mx;
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(xb + r)),
-                             "l"(a->x + e));
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(xb + XN + r)),
-                             "l"(a->out + e));
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(xb + 2 * XN + r)),
-                             "l"(a->rh + e));
-            }
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    }
 
     template <bool MASK>
     __device__ __forceinline__ void run_blocks(int tb, int nblk)
@@ -422,13 +306,12 @@ struct Tb4Thread {
     }
 };
 
-template <int K, int RY, int NW, int NS, int MODE, int MINB = 1, bool XUPD = false,
-          bool XSH = false, bool NEU = false, bool O2 = false, bool XP = false>
-__global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constant__ TbArgs a,
-                                                       const __grid_constant__ TbMaps maps)
+template <int K, int RY, int NW, int NS, int MODE, bool NEU = false, bool O2 = false>
+__global__ void __launch_bounds__(NW * 32, 1) k_cheb_tb4(const __grid_constant__ TbArgs a,
+                                                    const __grid_constant__ TbMaps maps)
 {
-    using T = Tb4Thread<K, RY, NW, NS, MODE, XUPD, XSH, NEU, O2, XP>;
-    using S = Tb4Shape<K, RY, NW, NS, XP>;
+    using T = Tb4Thread<K, RY, NW, NS, MODE, NEU, O2>;
+    using S = Tb4Shape<K, RY, NW, NS>;
     constexpr int TX = S::TX, TY = S::TY, U = S::QW;
     extern __shared__ __align__(128) double smraw[];
 
@@ -440,13 +323,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constan
     th.stg = smraw;                                              // 128-B aligned TMA boxes
     th.sm = smraw + (size_t)NS * 3 * S::BOX;
     th.bar = reinterpret_cast<uint64_t*>(th.sm + 2 * K * S::PLANE);
-    th.pbar = th.bar + NS;                                       // XP: 2 more mbarriers
-    th.xsm = reinterpret_cast<double*>(reinterpret_cast<char*>(smraw) + S::smem);
     th.alpha = th.beta = th.omega = 0.0;
     th.first = false;
     th.pmap = nullptr;
     th.side = nullptr;
-    th.xdo = false;
     if (MODE == MODE_P) {
         const int par = st->iter & 1;
         th.first = (st->iter == 0);
@@ -454,10 +334,6 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constan
         th.omega = st->omega;
         th.pmap = par ? &maps.pb : &maps.pa;
         th.side = par ? a.side_a : a.side_b;
-        if (XUPD) {
-            th.alpha = st->alpha;            // α_{i-1}, ω_{i-1} of the pending x update
-            th.xdo = !th.first && st->x_applied != st->iter;
-        }
     } else if (MODE == MODE_S) {
         th.alpha = st->alpha;
         th.side = a.side_a;
@@ -469,15 +345,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constan
     th.lane = lane;
     th.ey0 = wy * RY;
     constexpr int HX = S::HX;
-    // XP: a cluster pair of CTAs (ranks 0, 1 along x) covers 64 extended columns whose
-    // x-halo is only at the pair's outer sides; output columns [HX, 64 - HX) of the pair
-    const int crank = XP ? (int)(blockIdx.x & 1) : 0;
-    const int pcol = crank * 32 + lane;                          // column within the pair
-    constexpr int TXP = XP ? 64 - 2 * HX : TX;
-    th.tx0 = (XP ? (int)(blockIdx.x >> 1) : (int)blockIdx.x) * TXP - HX + crank * 32;
+    th.tx0 = (int)blockIdx.x * TX - HX;
     th.ty0 = blockIdx.y * TY - K;
     const int gx = th.tx0 + lane;
-    const int dx = max(HX - pcol, pcol - (HX + TXP - 1));
+    const int dx = max(HX - lane, lane - (HX + TX - 1));
     int wdy = 1 << 20;
     th.mir = ((gx == 0 && (a.bc.m & 1)) ? 1 : 0) | ((gx == a.nx - 1 && (a.bc.m & 2)) ? 2 : 0);
 #pragma unroll
@@ -524,26 +395,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constan
     for (int i = threadIdx.x; i < 2 * K * S::PLANE; i += blockDim.x) th.sm[i] = 0.0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) mbar_init(&th.bar[s], 1);
-        if (XP) {   // phases 0 and 1 armed: the peer's data of its first two steps
-            mbar_init(&th.pbar[0], 1);
-            mbar_init(&th.pbar[1], 1);
-            mbar_expect_tx(&th.pbar[0], T::XP_BYTES);
-            mbar_expect_tx(&th.pbar[1], T::XP_BYTES);
-        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (XP) {
-        const uint32_t peer = (uint32_t)(crank ^ 1);
-        th.peer_sm = mapa_shared(smem_u32(th.sm), peer);
-        th.peer_pbar = mapa_shared(smem_u32(th.pbar), peer);
-        th.edge = crank == 0 ? 31 : 0;
-        cluster_sync_all();   // both CTAs zeroed their planes and initialised their barriers
-    } else {
-        __syncthreads();
-    }
+    __syncthreads();
     if (threadIdx.x == 0)
         for (int tt = th.t0; tt < th.t0 + NS && tt < th.b1 && tt <= th.t1; ++tt) th.issue(tt);
-    if (XUPD && th.xdo) th.xissue(th.t0);
 
     // interior tile: the extended tile lies inside the grid -> masks only near block ends
     const bool interior = th.tx0 >= 0 && th.tx0 + 32 <= a.nx && th.ty0 >= 0 &&
@@ -569,11 +425,6 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_cheb_tb4(const __grid_constan
         t += NB * U;
     }
     th.run_tail(t, tail);
-    if (XP) {   // the peer's last step landed here; then no CTA exits before its peer
-        const int nl = nsteps - 1;
-        mbar_wait(&th.pbar[nl & 1], (nl >> 1) & 1);
-        cluster_sync_all();
-    }
 }
 
 }  // namespace fused

@@ -17,9 +17,6 @@ struct DevState {
     int32_t done;         // DONE_*
     int32_t fixed_iters;  // > 0: run exactly this many
     int32_t max_iter;
-    int32_t x_applied;    // deferred-x modes: last iteration whose x update is in x
-    int32_t omega_iter;   // last iteration that reached its ω (x update due)
-    double xa, xw;        // α, ω of iteration omega_iter (for the concurrent x update)
     double scratch[8];    // results of stand-alone dot calls
     int32_t pend;         // 2-sync (R31): stop decided at the ω stage, applied after a11/a12
 };
@@ -55,7 +52,6 @@ __device__ __forceinline__ void stage_update(DevState* st, int stage, const doub
         break;
     }
     case STAGE_ALPHA: {
-        st->x_applied = st->iter;   // the fused p-kernel of this iteration applied x_{iter}
         const int i = st->iter + 1;
         double* sc = scal + 8 * (i - 1);
         const double rw = v[0];
@@ -78,9 +74,6 @@ __device__ __forceinline__ void stage_update(DevState* st, int stage, const doub
         sc[2] = v[0];
         sc[3] = v[1];
         sc[4] = st->omega;
-        st->xa = st->alpha;
-        st->xw = st->omega;
-        st->omega_iter = i;
         break;
     }
     case STAGE_RHO: {

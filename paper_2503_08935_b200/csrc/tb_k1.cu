@@ -5,5 +5,4 @@ namespace fused {
 template bcgs_status launch_variant<1, 0>(bcgs_ctx, TbArgs&, int);
 template bcgs_status launch_variant<1, 1>(bcgs_ctx, TbArgs&, int);
 template bcgs_status launch_variant<1, 2>(bcgs_ctx, TbArgs&, int);
-bool defer_x_ok(bcgs_ctx c) { return defer_x_possible(c); }
 }  // namespace fused

@@ -2,9 +2,24 @@
 // only by the per-degree translation units tb_k<K>.cu, which instantiate launch_variant<K,.>;
 // the driver (bcgs_api.cu) sees the extern declarations in fused_launch.h.
 #pragma once
+#include <atomic>
+
 #include "ctx.cuh"
 
 namespace fused {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: `done` (one per kernel
+// instantiation, owned by its launcher) remembers the devices it has been set on (bit d),
+// race-free across host threads.
+template <typename KernelFn>
+bcgs_status ensure_smem_attr(bcgs_ctx c, KernelFn kern, size_t bytes, std::atomic<uint64_t>& done)
+{
+    const uint64_t bit = 1ull << (c->device & 63);
+    if (done.load(std::memory_order_acquire) & bit) return BCGS_OK;
+    CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    done.fetch_or(bit, std::memory_order_acq_rel);
+    return BCGS_OK;
+}
 
 template <int K> struct Tile;
 template <> struct Tile<1> { static constexpr int X = 32, Y = 16; };
@@ -22,12 +37,8 @@ bcgs_status launch_tb_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
     constexpr int TX = Tile<K>::X, TY = Tile<K>::Y;
     using S = TbShape<K, TX, TY>;
     auto kern = k_cheb_tb<K, TX, TY, MODE, NEU>;
-    static bool attr = false;
-    if (!attr) {
-        CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)S::smem));
-        attr = true;
-    }
+    static std::atomic<uint64_t> attr_dev{0};
+    TRY(ensure_smem_attr(c, kern, S::smem, attr_dev));
     dim3 grid((unsigned)((a.nx + TX - 1) / TX), (unsigned)((a.ny + TY - 1) / TY),
               (unsigned)nchunk_total);
     kern<<<grid, S::NT, S::smem, c->s>>>(a);
@@ -43,17 +54,15 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 
 inline EncodeTiledFn encode_fn()
 {
-    static EncodeTiledFn fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
+    static const EncodeTiledFn fn = [] {   // thread-safe one-time lookup
         void* p = nullptr;
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
                 cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = (EncodeTiledFn)p;
-    }
+            return (EncodeTiledFn)p;
+        return (EncodeTiledFn) nullptr;
+    }();
     return fn;
 }
 
@@ -80,9 +89,6 @@ inline bool tma_ok(bcgs_ctx c)
     return encode_fn() != nullptr && c->lay.nx % 2 == 0 && elems < (1ull << 32);
 }
 
-// deferred x update needs the TMA warp-row kernel (K <= 5)
-inline bool defer_x_possible(bcgs_ctx c) { return tma_ok(c) && c->degree >= 1 && c->degree <= 5; }
-
 inline bool make_maps(bcgs_ctx c, TbMaps* maps, const TbArgs& a, int mode, int box_y,
                       int box_x = 32)
 {
@@ -106,69 +112,39 @@ inline bool make_maps(bcgs_ctx c, TbMaps* maps, const TbArgs& a, int mode, int b
     return ok;
 }
 
-template <int K, int RY, int NW, int NS, int MODE, int MINB = 1, bool XUPD = false,
-          bool XSH = false, bool NEU = false, bool O2 = false, bool XP = false>
+template <int K, int RY, int NW, int NS, int MODE, bool NEU = false, bool O2 = false>
 bcgs_status launch_tb4_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
 {
-    using S = Tb4Shape<K, RY, NW, NS, XP>;
-    constexpr size_t smem = S::smem + (XUPD ? S::xupd_bytes : 0);
-    static_assert(smem <= 227 * 1024, "tb4 shared memory budget");
-    auto kern = k_cheb_tb4<K, RY, NW, NS, MODE, MINB, XUPD, XSH, NEU, O2, XP>;
-    static bool attr = false;
-    if (!attr) {
-        CUDA_OK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem));
-        attr = true;
-    }
+    using S = Tb4Shape<K, RY, NW, NS>;
+    static_assert(S::smem <= 227 * 1024, "tb4 shared memory budget");
+    auto kern = k_cheb_tb4<K, RY, NW, NS, MODE, NEU, O2>;
+    static std::atomic<uint64_t> attr_dev{0};
+    TRY(ensure_smem_attr(c, kern, S::smem, attr_dev));
     TbMaps maps;
     if (!make_maps(c, &maps, a, MODE, S::EY))
         return fail(c, BCGS_E_CUDA, "cuTensorMapEncodeTiled failed");
-    if constexpr (XP) {   // cluster pairs along x: 64 - 2 HX output columns per pair
-        constexpr int TXP = 64 - 2 * S::HX;
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3((unsigned)(2 * ((a.nx + TXP - 1) / TXP)),
-                           (unsigned)((a.ny + S::TY - 1) / S::TY), (unsigned)nchunk_total);
-        cfg.blockDim = dim3(NW * 32);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = c->s;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = 2;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        CUDA_OK(c, cudaLaunchKernelEx(&cfg, kern, (TbArgs)a, maps));
-        return BCGS_OK;
-    }
     dim3 grid((unsigned)((a.nx + S::TX - 1) / S::TX), (unsigned)((a.ny + S::TY - 1) / S::TY),
               (unsigned)nchunk_total);
-    kern<<<grid, NW * 32, smem, c->s>>>(a, maps);
+    kern<<<grid, NW * 32, S::smem, c->s>>>(a, maps);
     CUDA_OK(c, cudaGetLastError());
     return BCGS_OK;
 }
 
+// Kernel layout per degree: k <= 4 the TMA warp-row kernel with 24 warps
+// (BCGS_OPT_TB_VARIANT 7, default); Neumann faces the 16-warp TMA kernel with mirror ghosts
+// (k <= 5); otherwise (odd nx: no TMA, variant 2, one-pass k = 5..8) the square tile.
 template <int K, int MODE>
 bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz)
 {
-    // Neumann faces present (R27): the mirror-ghost instantiations (16-warp TMA kernel for
-    // k <= 5, else the square tile); the all-Dirichlet kernels carry no mirror logic
-    if (a.bc.m || a.bc.zlo >= 0 || a.bc.zhi >= 0) {
+    if (a.bc.m || a.bc.zlo >= 0 || a.bc.zhi >= 0) {   // R27 mirror-ghost instantiations
         if constexpr (K <= 5) {
             if (tma_ok(c) && c->tb_variant != 2)
-                return launch_tb4_k<K, 2, 16, 4, MODE, 1, false, false, true>(c, a, nz);
+                return launch_tb4_k<K, 2, 16, 4, MODE, true>(c, a, nz);
         }
         return launch_tb_k<K, MODE, true>(c, a, nz);
     }
-    if constexpr (K <= 5) {   // register budget: warp-row layouts up to K = 5
-        if (MODE == MODE_P && c->defer_x)   // deferred a11 fused into the p-kernel (16 warps)
-            return launch_tb4_k<K, 2, 16, (K <= 4 ? 4 : 3), MODE, 1, true>(c, a, nz);
-        if (c->tb_variant == 5 && tma_ok(c)) return launch_tb4_k<K, 2, 16, 4, MODE>(c, a, nz);
-        if constexpr (K <= 4) {
-            if (c->tb_variant == 7 && tma_ok(c)) return launch_tb4_k<K, 2, 24, 3, MODE>(c, a, nz);
-            if (c->tb_variant == 9 && tma_ok(c))   // x-pair clusters (experimental)
-                return launch_tb4_k<K, 2, 24, 3, MODE, 1, false, false, false, false, true>(c, a, nz);
-        }
+    if constexpr (K <= 4) {   // register budget of the 24-warp layout
+        if (c->tb_variant != 2 && tma_ok(c)) return launch_tb4_k<K, 2, 24, 3, MODE>(c, a, nz);
     }
     return launch_tb_k<K, MODE>(c, a, nz);
 }

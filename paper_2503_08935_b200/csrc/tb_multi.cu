@@ -23,8 +23,8 @@ template <int K, int MODE, bool O2>
 static bcgs_status pass_k(bcgs_ctx c, TbArgs& a, int nz, bool neu)
 {
     constexpr int NW = mp_nw(K, MODE);
-    if (neu) return launch_tb4_k<K, 2, NW, 4, MODE, 1, false, false, true, O2>(c, a, nz);
-    return launch_tb4_k<K, 2, NW, 4, MODE, 1, false, false, false, O2>(c, a, nz);
+    if (neu) return launch_tb4_k<K, 2, NW, 4, MODE, true, O2>(c, a, nz);
+    return launch_tb4_k<K, 2, NW, 4, MODE, false, O2>(c, a, nz);
 }
 
 #ifndef TB_MULTI_CONT

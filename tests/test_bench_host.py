@@ -40,3 +40,12 @@ def test_peaks_source_is_reported():
 def test_max_over_ranks_single_process_is_identity():
     b = load_bench()
     assert b.max_over_ranks(3.5) == 3.5
+
+
+def test_reference_arm_samples_the_full_grid_for_driver_runs():
+    """The driver's --steps 20 --warmup 5 run times the oracle on the same 512^3 workload as
+    our arm; only longer runs fall back to a slab (bounded wall time)."""
+    b = load_bench()
+    assert b.reference_sample_planes(512, 20, 5) == 512
+    ls = b.reference_sample_planes(512, 200, 10)
+    assert 8 <= ls < 512 and ls % 8 == 0

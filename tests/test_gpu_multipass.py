@@ -38,7 +38,7 @@ def apply_pair(bc, orc, n3, h, pc, k, bpr, mp_min=None, faces=None):
     s.kernel_times_reset()
     out = host(s.apply_preconditioner(dev(q)))
     kt = s.kernel_times()
-    ivl, _, _ = bc.chebyshev_constants(n3, h, bpr, pc, k, bc=faces)
+    ivl = orc.pc_interval(n3[::-1], h, bpr, pc, bc=faces)   # the oracle's own interval
     ref = orc.apply_cheb(q, h, bpr, k, ivl[0], ivl[1], bc=faces)
     return out, ref, kt
 

@@ -10,7 +10,7 @@ import torch  # noqa: E402
 import synth_inputs as si  # noqa: E402
 from paper_2503_08935_b200 import bcgs  # noqa: E402
 
-for n3, pc, k, bpr, kern, var in [((64, 48, 32), "gnocomm", 4, 2, 1, 7), ((64, 48, 32), "bj", 3, 1, 1, 5),
+for n3, pc, k, bpr, kern, var in [((64, 48, 32), "gnocomm", 4, 2, 1, 7), ((64, 48, 32), "bj", 3, 1, 1, 2),
                                   ((40, 24, 32), "gnocomm", 2, 1, 1, 7), ((33, 20, 16), "gnocomm", 4, 1, 1, 7),
                                   ((32, 32, 32), "gnocomm", 4, 1, 0, 7),
                                   # multi-pass (k = 5: passes 3 + 2, k = 11: 4 + 4 + 3)
