@@ -285,6 +285,10 @@ def main():
     # device no-ops and the timing would be meaningless
     short = 0.0 if rep["iterations"] == total else 1.0
     valid = max_over_ranks(short, dist, dev) == 0.0
+    # a reduction parked for the exact path (R19) turns the rest of the enqueued iterations
+    # into no-ops until the host resolves it: the timed passes must not contain one
+    n_exact = s.exact_dots()
+    valid = valid and max_over_ranks(float(n_exact), dist, dev) == 0.0
     comm = None
     if world > 1:
         # exposed halo / reduction share by ablation: K_a iterations of a fresh
@@ -405,8 +409,9 @@ def main():
         }
         if not valid:
             line["valid"] = False
-            line["invalid_reason"] = (f"the solve stopped after {rep['iterations']} of {total} "
-                                      f"enqueued iterations ({rep['status_name']})")
+            line["invalid_reason"] = (f"the solve ran {rep['iterations']} of {total} enqueued "
+                                      f"iterations ({rep['status_name']}); {n_exact} dots took "
+                                      f"the exact path")
         print(json.dumps(line), flush=True)
     s.close()
     if world > 1:

@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define BCGS_ABI_VERSION 4
+#define BCGS_ABI_VERSION 5
 #define BCGS_MAX_DEGREE 64       /* Chebyshev degree k (sweeps per application) cap      */
 #define BCGS_HIST_CAP 16384      /* max outer iterations recorded per solve              */
 
@@ -61,7 +61,8 @@ typedef enum {
     BCGS_E_NCCL = 5,          /* NCCL error                                               */
     BCGS_NOT_CONVERGED = 6,   /* max_iter reached without rel residual < tol (R23)        */
     BCGS_BREAKDOWN = 7,       /* exact zero / non-finite r~ᵀw, ω or ρ (R7)                */
-    BCGS_E_STATE = 8          /* call out of order (e.g. iterate before begin)            */
+    BCGS_E_STATE = 8,         /* call out of order (e.g. iterate before begin)            */
+    BCGS_E_COMM = 9           /* p2p transport: a peer did not answer within the timeout  */
 } bcgs_status;
 
 /* Preconditioner M of Alg. 3 l.6/12; Table I. */
@@ -90,7 +91,8 @@ typedef enum {
     BCGS_OPT_KERNELS = 0,      /* 0 = reference kernels (one sweep per launch, one op per */
                                /*     launch); 1 = fused / temporally blocked (default)   */
     BCGS_OPT_GRAPH = 1,        /* 1 = replay iterations from a captured CUDA graph (default;*/
-                               /*     not while profiling or with bcgs_create_local)   */
+                               /*     one rank or the p2p transport; not while profiling   */
+                               /*     or with bcgs_create_local); 2 = also capture NCCL    */
     BCGS_OPT_PROFILE = 2,      /* 1 = CUDA events around every kernel (bcgs_kernel_times) */
     BCGS_OPT_POLL = 3,         /* iterations launched between done-flag polls (tol mode)  */
     BCGS_OPT_TB_VARIANT = 4,   /* temporally blocked kernel layout: 7 = TMA warp-row      */
@@ -111,6 +113,14 @@ typedef enum {
                                /* identities for r = s - ω t -> 2 reductions per iteration */
                                /* instead of 3 (fused path only; rounding differs from the */
                                /* default, the oracle implements the same flag)            */
+    BCGS_OPT_EXACT_DOT = 11,   /* 1 = every dot product through the exact superaccumulator */
+                               /* path (R19 fallback) instead of certified   */
+                               /* Dot2; the results are the same (correctly rounded) --   */
+                               /* for testing the fallback.  0 = certified Dot2 (default) */
+    BCGS_OPT_COMM_TIMEOUT = 12 /* seconds a transport wait may take: NCCL host waits abort  */
+                               /* the communicator after it (default 300; async errors    */
+                               /* abort at once); p2p device waits give up (default 60).  */
+                               /* Both end the solve with an error status, never a hang.  */
 } bcgs_option;
 
 /* Boundary condition kind of a physical face (Eq. 4 / Eq. 5). */
@@ -170,6 +180,24 @@ bcgs_status bcgs_create(const bcgs_grid_desc* grid, int32_t rank, int32_t nranks
 bcgs_status bcgs_create_local(const bcgs_grid_desc* grid, int32_t nranks, int32_t cuda_device,
                               void* const* d_workspaces, size_t ws_bytes, void* cuda_stream,
                               bcgs_ctx* outs);
+/* Peer-memory transport: halos and reductions are
+ * kernels that store into the peers' memory and signal sequence-numbered flags (one-shot
+ * reductions, no host synchronisation, multi-rank iterations replayed as CUDA graphs).
+ * One process per rank: bcgs_create_p2p, then every rank exchanges its 128-byte
+ * bcgs_p2p_handle record (the caller's process group: all-gather) and calls
+ * bcgs_p2p_connect with the nranks records in rank order (CUDA IPC; ranks on the same or
+ * on NVLink-connected devices).  The mailbox (and the landing zones of the halos) is
+ * allocated and freed by the library.  In one process: bcgs_create_local_p2p (direct
+ * pointers; drive each context from its own host thread).  Peer waits time out after 60 s
+ * (BCGS_E_COMM) instead of hanging. */
+bcgs_status bcgs_create_p2p(const bcgs_grid_desc* grid, int32_t rank, int32_t nranks,
+                            int32_t cuda_device, void* d_workspace, size_t ws_bytes,
+                            void* cuda_stream, bcgs_ctx* out);
+bcgs_status bcgs_p2p_handle(bcgs_ctx ctx, void* out128);
+bcgs_status bcgs_p2p_connect(bcgs_ctx ctx, const void* all_handles);
+bcgs_status bcgs_create_local_p2p(const bcgs_grid_desc* grid, int32_t nranks,
+                                  int32_t cuda_device, void* const* d_workspaces,
+                                  size_t ws_bytes, void* cuda_stream, bcgs_ctx* outs);
 void bcgs_destroy(bcgs_ctx ctx);
 const char* bcgs_last_error(bcgs_ctx ctx);
 bcgs_status bcgs_set_option(bcgs_ctx ctx, int32_t option, int64_t value);
@@ -197,6 +225,13 @@ bcgs_status bcgs_set_preconditioner(bcgs_ctx ctx, bcgs_pc pc, int32_t degree, do
 bcgs_status bcgs_set_inner_solver(bcgs_ctx ctx, double rel_tol, int32_t max_iter);
 /* Total inner iterations since the last bcgs_begin (Table II "it. / outer it."). */
 int64_t bcgs_inner_iterations(bcgs_ctx ctx);
+/* Dot products recomputed on the exact path since the last bcgs_begin (R19: a Dot2 result
+ * that could not be certified as correctly rounded, or BCGS_OPT_EXACT_DOT); -1 on error. */
+int32_t bcgs_exact_dots(bcgs_ctx ctx);
+/* Diagnostics of the last Dot2 result the certification refused (R19): stage, dot index,
+ * chain depth D, r = fl(hi + lo), e = (hi + lo) - r, the error bound E, the gaps above and
+ * below |r|, Σ|a_i b_i|, then the number of refusals since bcgs_create (10 doubles). */
+bcgs_status bcgs_certification_info(bcgs_ctx ctx, double* out10);
 /* Override the Chebyshev interval [a', b'] (0 < a' < b'); (0, 0) restores the default. */
 bcgs_status bcgs_set_eigen_bounds(bcgs_ctx ctx, double a, double b);
 
@@ -224,7 +259,8 @@ bcgs_status bcgs_get_solution(bcgs_ctx ctx, double* x, int32_t mem);
 /* Single steps of the path on device slabs, for parity tests and micro-benchmarks.
  * apply_operator: out = A in (global operator with halo exchange; block_local != 0 gives
  * the block-diagonal slab operator of Eq. 12-14).  apply_preconditioner: out = M^-1 in
- * with the configured preconditioner.  dot: global Dot2 (R19) -> *host_out. */
+ * with the configured preconditioner.  dot: the global dot product, correctly rounded
+ * (R19: certified Dot2, else the exact path) -> *host_out. */
 bcgs_status bcgs_apply_operator(bcgs_ctx ctx, const double* d_in, double* d_out,
                                 int32_t block_local);
 bcgs_status bcgs_apply_preconditioner(bcgs_ctx ctx, const double* d_in, double* d_out);

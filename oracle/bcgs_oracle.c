@@ -10,8 +10,9 @@
  *
  * Style: plain loops, one stencil sweep per pass, one vector operation per pass, fp64,
  * compiled with -ffp-contract=off: the compiler contracts nothing; the contract's fused
- * multiply-adds (DESIGN.md §3 R17/R18/R20, and Dot2's TwoProd) are written as explicit fma().  OpenMP is used only over z-planes of element-wise passes
- * (order-independent) and for per-plane dot partials that are combined in ascending z.
+ * multiply-adds (DESIGN.md §3 R17/R18/R20) are written as explicit fma().  OpenMP is used
+ * only over z-planes of element-wise passes (order-independent) and for exact dot-product
+ * accumulators (integer sums: order-independent).
  *
  * Citations: "P:n" = line n of the paper's LaTeX source.  Section / equation /
  * algorithm numbers are given next to every citation.
@@ -142,12 +143,20 @@ void orc_apply_A(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab,
 }
 
 /* ------------------------------------------------------------------------------------------
- * Dot products: Dot2 of Ogita, Rump & Oishi (compensated dot, DESIGN.md §3 R19).  The paper
- * computes r~ᵀw, tᵀr, tᵀt, r0ᵀr, rᵀr (Alg. 3) and notes that
- * reduction order changes results; Dot2 makes the result (almost always) the
- * correctly rounded value, independent of order.
- * Per z-plane: sequential Dot2 in index order -> pair (p_k, s_k).  Planes are combined in
- * ascending z: (P, q) = TwoSum(P, p_k); S = S + (q + s_k).  Result fl(P + S).
+ * Dot products (DESIGN.md §3 R19): the CORRECTLY ROUNDED value of the exact sum,
+ * RN(Σ a_i b_i), round to nearest, ties to even.  The paper computes r~ᵀw, tᵀr, tᵀt, r0ᵀr,
+ * rᵀr (Alg. 3) and notes that floating-point reductions give
+ * order-dependent results ("numerical issues due to floating-point arithmetic", P:207;
+ * iteration counts vary with the reduction order); the exact sum rounded once has a
+ * plain definition that no summation order can change.
+ *
+ * Method (plain, no cleverness): every double is m * 2^e with an integer m < 2^53 and
+ * e >= -1074, so a product is the 106-bit integer ma*mb times 2^(ea+eb) with
+ * ea + eb >= -2148.  The exact sum is kept as a big two's-complement integer X with
+ * Σ = X * 2^XBASE, XBASE = -2176, in XLIMB 64-bit limbs; each product is added (or
+ * subtracted) at its bit offset with full carry propagation.  At the end X is rounded to
+ * 53 significant bits (or to the subnormal grid 2^-1074), ties to even.  A non-finite
+ * operand gives NaN; a sum beyond the double range gives +-inf.
  * ---------------------------------------------------------------------------------------- */
 static inline void two_sum(double a, double b, double* s, double* e)
 {
@@ -164,7 +173,8 @@ static inline void two_prod(double a, double b, double* p, double* e)
     *p = x;
 }
 
-/* Dot2 of n contiguous elements -> (hi, lo) pair, result = hi + lo */
+/* Dot2 (Ogita, Rump & Oishi) of n contiguous elements -> (hi, lo): used only by
+ * orc_dot_pair below (the per-rank compensated partial of a slab decomposition). */
 static void dot2_run(int64_t n, const double* a, const double* b, double* hi, double* lo)
 {
     double p = 0.0, s = 0.0;
@@ -178,23 +188,150 @@ static void dot2_run(int64_t n, const double* a, const double* b, double* hi, do
     *lo = s;
 }
 
-/* Dot over a field of nplanes planes of plen elements each. */
+#define XBASE (-2176)
+#define XLIMB 72 /* 4608 bits: products < 2^2048, sums of < 2^64 of them < 2^2112 */
+
+typedef struct {
+    uint64_t w[XLIMB]; /* two's complement, limb 0 least significant */
+    int bad;           /* a non-finite operand was seen */
+} exact_acc;
+
+/* x = m * 2^e, m < 2^53 an integer (x finite) */
+static void split_double(double x, uint64_t* m, int* e, int* neg)
+{
+    uint64_t bits;
+    memcpy(&bits, &x, sizeof bits);
+    *neg = (int)(bits >> 63);
+    int ex = (int)((bits >> 52) & 0x7FF);
+    uint64_t frac = bits & ((1ull << 52) - 1);
+    if (ex == 0) {
+        *m = frac;
+        *e = -1074;
+    } else {
+        *m = frac | (1ull << 52);
+        *e = ex - 1075;
+    }
+}
+
+/* X += sign * v * 2^off, v < 2^128, 0 <= off */
+static void acc_add(exact_acc* X, unsigned __int128 v, int off, int negative)
+{
+    int q = off / 64, r = off % 64;
+    uint64_t part[3];
+    part[0] = (uint64_t)(v << r);
+    part[1] = (uint64_t)((r == 0) ? (v >> 64) : (v >> (64 - r)));
+    part[2] = (uint64_t)((r == 0) ? 0 : ((v >> 64) >> (64 - r)));
+    if (!negative) {
+        unsigned __int128 carry = 0;
+        for (int k = q; k < XLIMB; ++k) {
+            unsigned __int128 t = (unsigned __int128)X->w[k] + carry +
+                                  (k - q < 3 ? part[k - q] : 0);
+            X->w[k] = (uint64_t)t;
+            carry = t >> 64;
+            if (k - q >= 2 && carry == 0) break;
+        }
+    } else {
+        uint64_t borrow = 0;
+        for (int k = q; k < XLIMB; ++k) {
+            uint64_t sub = (k - q < 3 ? part[k - q] : 0);
+            uint64_t old = X->w[k];
+            uint64_t t = old - sub - borrow;
+            borrow = (old < sub || (old - sub) < borrow) ? 1 : 0;
+            X->w[k] = t;
+            if (k - q >= 2 && borrow == 0) break;
+        }
+    }
+}
+
+static void acc_add_product(exact_acc* X, double a, double b)
+{
+    if (!isfinite(a) || !isfinite(b)) {
+        X->bad = 1;
+        return;
+    }
+    uint64_t ma, mb;
+    int ea, eb, na, nb;
+    split_double(a, &ma, &ea, &na);
+    split_double(b, &mb, &eb, &nb);
+    if (ma == 0 || mb == 0) return;
+    unsigned __int128 M = (unsigned __int128)ma * mb;
+    acc_add(X, M, ea + eb - XBASE, na != nb);
+}
+
+/* X += Y (exact) */
+static void acc_merge(exact_acc* X, const exact_acc* Y)
+{
+    unsigned __int128 carry = 0;
+    for (int k = 0; k < XLIMB; ++k) {
+        unsigned __int128 t = (unsigned __int128)X->w[k] + Y->w[k] + carry;
+        X->w[k] = (uint64_t)t;
+        carry = t >> 64;
+    }
+    X->bad |= Y->bad;
+}
+
+/* round X * 2^XBASE to the nearest double, ties to even */
+static double acc_round(const exact_acc* X)
+{
+    if (X->bad) return NAN;
+    uint64_t mag[XLIMB];
+    int negative = (int)(X->w[XLIMB - 1] >> 63);
+    if (negative) { /* magnitude = ~X + 1 */
+        unsigned __int128 carry = 1;
+        for (int k = 0; k < XLIMB; ++k) {
+            unsigned __int128 t = (unsigned __int128)(~X->w[k]) + carry;
+            mag[k] = (uint64_t)t;
+            carry = t >> 64;
+        }
+    } else {
+        memcpy(mag, X->w, sizeof mag);
+    }
+    int top = XLIMB - 1;
+    while (top >= 0 && mag[top] == 0) --top;
+    if (top < 0) return 0.0;
+    int msb = top * 64 + 63 - __builtin_clzll(mag[top]);
+    int lsb = msb - 52; /* 53 significant bits ... */
+    if (lsb < -1074 - XBASE) lsb = -1074 - XBASE; /* ... or the subnormal grid 2^-1074 */
+#define XBIT(pos) ((pos) < 0 ? 0u : (unsigned)((mag[(pos) / 64] >> ((pos) % 64)) & 1u))
+    uint64_t sig = 0;
+    for (int pos = msb; pos >= lsb; --pos) sig = (sig << 1) | XBIT(pos);
+    unsigned round_bit = XBIT(lsb - 1);
+    int sticky = 0;
+    for (int pos = lsb - 2; pos >= 0; --pos)
+        if (XBIT(pos)) {
+            sticky = 1;
+            break;
+        }
+#undef XBIT
+    if (round_bit && (sticky || (sig & 1u))) {
+        sig += 1;
+        if (sig == (1ull << 53)) {
+            sig >>= 1;
+            lsb += 1;
+        }
+    }
+    double v = ldexp((double)sig, lsb + XBASE); /* exact, or inf beyond the range */
+    return negative ? -v : v;
+}
+
+/* Dot over a field of nplanes planes of plen elements each: RN(exact sum).  OpenMP threads
+ * accumulate disjoint planes into private exact accumulators, merged exactly. */
 double orc_dot(int64_t plen, int64_t nplanes, const double* a, const double* b)
 {
-    double* ph = (double*)malloc(sizeof(double) * (size_t)(nplanes > 0 ? nplanes : 1));
-    double* pl = (double*)malloc(sizeof(double) * (size_t)(nplanes > 0 ? nplanes : 1));
-#pragma omp parallel for schedule(static)
-    for (int64_t k = 0; k < nplanes; ++k)
-        dot2_run(plen, a + k * plen, b + k * plen, &ph[k], &pl[k]);
-    double P = 0.0, S = 0.0;
-    for (int64_t k = 0; k < nplanes; ++k) {
-        double q;
-        two_sum(P, ph[k], &P, &q);
-        S = S + (q + pl[k]);
+    exact_acc total;
+    memset(&total, 0, sizeof total);
+#pragma omp parallel
+    {
+        exact_acc mine;
+        memset(&mine, 0, sizeof mine);
+#pragma omp for schedule(static)
+        for (int64_t k = 0; k < nplanes; ++k)
+            for (int64_t i = 0; i < plen; ++i)
+                acc_add_product(&mine, a[k * plen + i], b[k * plen + i]);
+#pragma omp critical
+        acc_merge(&total, &mine);
     }
-    free(ph);
-    free(pl);
-    return P + S;
+    return acc_round(&total);
 }
 
 /* Dot2 pair (hi, lo) of a field -- the per-rank partial a z-slab decomposition would

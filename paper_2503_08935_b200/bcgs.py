@@ -17,13 +17,13 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 # BCGS_LIB: load another build of the same library (A/B timing of kernel changes)
 LIB_PATH = os.environ.get("BCGS_LIB") or os.path.join(_PKG, "lib", "libbcgs.so")
 
-OK, E_INVALID, E_CONFIG, E_SPECTRUM, E_CUDA, E_NCCL, NOT_CONVERGED, BREAKDOWN, E_STATE = range(9)
+OK, E_INVALID, E_CONFIG, E_SPECTRUM, E_CUDA, E_NCCL, NOT_CONVERGED, BREAKDOWN, E_STATE, E_COMM = range(10)
 STATUS_NAMES = {0: "ok", 1: "invalid", 2: "config", 3: "spectrum", 4: "cuda", 5: "nccl",
-                6: "not_converged", 7: "breakdown", 8: "state"}
+                6: "not_converged", 7: "breakdown", 8: "state", 9: "comm"}
 PC = {"none": 0, "gnocomm": 1, "bj": 2, "g": 3, "bj_bicgs": 4, "g_bicgs": 5}
 MEM_DEVICE, MEM_HOST = 0, 1
 OPT_KERNELS, OPT_GRAPH, OPT_PROFILE, OPT_POLL, OPT_TB_VARIANT = 0, 1, 2, 3, 4
-OPT_MULTIPASS, OPT_ABLATE, OPT_SYNC2 = 8, 9, 10
+OPT_MULTIPASS, OPT_ABLATE, OPT_SYNC2, OPT_EXACT_DOT, OPT_COMM_TIMEOUT = 8, 9, 10, 11, 12
 HIST_CAP = 16384
 MAX_DEGREE = 64
 
@@ -39,6 +39,8 @@ EXPORTS = [
     "bcgs_residual_history", "bcgs_scalar_history", "bcgs_get_solution",
     "bcgs_apply_operator", "bcgs_apply_preconditioner", "bcgs_dot", "bcgs_kernel_times",
     "bcgs_kernel_times_reset", "bcgs_set_inner_solver", "bcgs_inner_iterations",
+    "bcgs_exact_dots", "bcgs_certification_info", "bcgs_create_p2p", "bcgs_p2p_handle", "bcgs_p2p_connect",
+    "bcgs_create_local_p2p",
 ]
 
 
@@ -114,6 +116,12 @@ def load() -> ctypes.CDLL:
         "bcgs_kernel_times_reset": (None, [P]),
         "bcgs_set_inner_solver": (i32, [P, f64, i32]),
         "bcgs_inner_iterations": (i64, [P]),
+        "bcgs_exact_dots": (ctypes.c_int32, [P]),
+        "bcgs_certification_info": (i32, [P, P]),
+        "bcgs_create_p2p": (i32, [P, i32, i32, i32, P, ctypes.c_size_t, P, P]),
+        "bcgs_p2p_handle": (i32, [P, P]),
+        "bcgs_p2p_connect": (i32, [P, P]),
+        "bcgs_create_local_p2p": (i32, [P, i32, i32, P, ctypes.c_size_t, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -167,7 +175,10 @@ class Solver:
 
     def __init__(self, n, h: float, *, rank: int = 0, nranks: int = 1,
                  nccl_id: bytes | None = None, device: int | None = None, stream=None,
-                 bc=None, _ctx=None, _workspace=None):
+                 bc=None, transport: str = "nccl", _ctx=None, _workspace=None):
+        """transport (nranks > 1): "nccl" (nccl_id from rank 0) or "p2p" (peer memory:
+        then every rank calls p2p_handle(), all-gathers the records and p2p_connect(...);
+        see connect_p2p)."""
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("bcgs.Solver needs a CUDA device (no CPU fallback)")
@@ -190,12 +201,29 @@ class Solver:
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{self.device}")
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         ctx = ctypes.c_void_p()
-        idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
-        st = self.lib.bcgs_create(ctypes.byref(self.desc), rank, nranks, idbuf, self.device,
-                                  self.workspace.data_ptr(), nbytes, self.stream.cuda_stream,
-                                  ctypes.byref(ctx))
+        if transport == "p2p" and nranks > 1:
+            st = self.lib.bcgs_create_p2p(ctypes.byref(self.desc), rank, nranks, self.device,
+                                          self.workspace.data_ptr(), nbytes,
+                                          self.stream.cuda_stream, ctypes.byref(ctx))
+        else:
+            idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+            st = self.lib.bcgs_create(ctypes.byref(self.desc), rank, nranks, idbuf, self.device,
+                                      self.workspace.data_ptr(), nbytes, self.stream.cuda_stream,
+                                      ctypes.byref(ctx))
         self.ctx = ctx
         self._check(st, "bcgs_create")
+
+    # ------------------------------------------------------------------ p2p transport
+    def p2p_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        self._check(self.lib.bcgs_p2p_handle(self.ctx, buf), "bcgs_p2p_handle")
+        return buf.raw
+
+    def p2p_connect(self, handles: list[bytes]):
+        blob = b"".join(handles)
+        assert len(blob) == 128 * self.nranks
+        buf = ctypes.create_string_buffer(blob, len(blob))
+        self._check(self.lib.bcgs_p2p_connect(self.ctx, buf), "bcgs_p2p_connect")
 
     # ------------------------------------------------------------------ plumbing
     def _check(self, st, what):
@@ -256,6 +284,17 @@ class Solver:
 
     def inner_iterations(self) -> int:
         return int(self.lib.bcgs_inner_iterations(self.ctx))
+
+    def exact_dots(self) -> int:
+        """Dots recomputed on the exact path since the last begin (R19)."""
+        return int(self.lib.bcgs_exact_dots(self.ctx))
+
+    def certification_info(self) -> dict:
+        out = np.zeros(10)
+        self._check(self.lib.bcgs_certification_info(self.ctx, out.ctypes.data),
+                    "bcgs_certification_info")
+        keys = ["stage", "dot", "D", "r", "e", "E", "gap_up", "gap_down", "sum_abs", "refused"]
+        return dict(zip(keys, map(float, out)))
 
     def set_eigen_bounds(self, a: float, b: float):
         self._check(self.lib.bcgs_set_eigen_bounds(self.ctx, a, b), "bcgs_set_eigen_bounds")
@@ -341,9 +380,20 @@ class Solver:
         self.lib.bcgs_kernel_times_reset(self.ctx)
 
 
-def local_group(n, h: float, nranks: int, device: int | None = None, bc=None) -> list:
-    """nranks Solver contexts on ONE GPU exchanging halos / reductions by device copies
-    (bcgs_create_local).  Drive each from its own thread."""
+def connect_p2p(solver: "Solver", group=None):
+    """All-gather the ranks' p2p records through torch.distributed (any backend) and connect."""
+    import torch.distributed as dist
+    recs = [None] * solver.nranks
+    dist.all_gather_object(recs, solver.p2p_handle(), group=group)
+    solver.p2p_connect(recs)
+
+
+def local_group(n, h: float, nranks: int, device: int | None = None, bc=None,
+                transport: str = "copy") -> list:
+    """nranks Solver contexts on ONE GPU (drive each from its own thread).  transport
+    "copy": halos / reductions by stream-ordered device copies + a host barrier (the NCCL
+    path's sequence, bcgs_create_local); "p2p": the peer-memory kernels of p2p.cuh with
+    direct pointers (bcgs_create_local_p2p)."""
     import torch
     lib = load()
     device = torch.cuda.current_device() if device is None else device
@@ -355,8 +405,8 @@ def local_group(n, h: float, nranks: int, device: int | None = None, bc=None) ->
     ptrs = (ctypes.c_void_p * nranks)(*[w.data_ptr() for w in wss])
     outs = (ctypes.c_void_p * nranks)()
     stream = torch.cuda.current_stream(device)
-    st = lib.bcgs_create_local(ctypes.byref(desc), nranks, device, ptrs, nbytes,
-                               stream.cuda_stream, outs)
+    create = lib.bcgs_create_local_p2p if transport == "p2p" else lib.bcgs_create_local
+    st = create(ctypes.byref(desc), nranks, device, ptrs, nbytes, stream.cuda_stream, outs)
     if st:
         raise BcgsError(st, "bcgs_create_local")
     return [Solver(n, h, rank=r, nranks=nranks, device=device, stream=stream, bc=bc,

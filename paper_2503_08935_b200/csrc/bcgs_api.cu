@@ -7,6 +7,7 @@
 // Dot2's TwoProd (dd.cuh).
 #include "ctx.cuh"
 #include "k_ref.cuh"
+#include "k_stream.cuh"
 
 namespace {
 
@@ -191,14 +192,74 @@ bcgs_status cheb_constants(const bcgs_grid_desc* g, int32_t nslab, bcgs_pc pc, i
 }
 
 // ------------------------------------------------------------------ init / state
-__global__ void k_init_state(DevState* st, double tol, int max_iter, int fixed)
+// The parked stage with its flagged dots replaced by the exactly rounded sums of the
+// superaccumulators limbs[r][d][XL] (+ a non-finite flag per rank at [r][5][0]).
+__global__ void k_resolve(DevState* st, const long long* __restrict__ limbs, int nranks,
+                          int64_t rank_stride, double* hist, double* scal)
 {
+    const int stage = st->pend_stage, mask = st->pend_mask;
+    if (!mask) return;
+    bool bad = false;
+    for (int r = 0; r < nranks; ++r) bad |= limbs[r * rank_stride + 5 * xdot::XL] != 0;
+    double v[5];
+    for (int d = 0; d < 5; ++d) {
+        v[d] = st->pend_v[d];
+        if (mask & (1 << d)) {
+            v[d] = xdot::round_limbs(limbs + d * xdot::XL, nranks, rank_stride, bad);
+            st->n_exact += 1;
+        }
+    }
+    st->pend_mask = 0;
+    if (stage != STAGE_DOT) st->done = DONE_RUNNING;
+    stage_update(st, stage, v, hist, scal);
+}
+
+__global__ void k_set_exact(DevState* st, int exact) { st->exact_mode = exact; }
+
+__global__ void k_init_state(DevState* st, double tol, int max_iter, int fixed, int exact)
+{
+    st->pend_stage = 0;
+    st->pend_mask = 0;
+    st->exact_mode = exact;
+    st->n_exact = 0;
     st->tol = tol;
     st->max_iter = max_iter;
     st->fixed_iters = fixed;
     st->done = DONE_RUNNING;
     st->iter = 0;
     st->pend = DONE_RUNNING;
+}
+
+// ------------------------------------------------------------------ host waits
+// Wait for the private stream.  NCCL contexts poll ncclCommGetAsyncError while waiting and
+// abort the communicator on an asynchronous error or after comm_timeout_s (a dead peer
+// would otherwise block the host forever); the p2p transport times out on the device.
+bcgs_status sync_stream(bcgs_ctx c)
+{
+    if (!c->comm) {
+        CUDA_OK(c, cudaStreamSynchronize(c->s));
+        return BCGS_OK;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        const cudaError_t e = cudaStreamQuery(c->s);
+        if (e == cudaSuccess) return BCGS_OK;
+        if (e != cudaErrorNotReady) CUDA_OK(c, e);
+        ncclResult_t ae = ncclSuccess;
+        ncclCommGetAsyncError(c->comm, &ae);
+        const double dt =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if ((ae != ncclSuccess && ae != ncclInProgress) || dt > c->comm_timeout_s) {
+            ncclCommAbort(c->comm);
+            c->comm = nullptr;
+            if (ae != ncclSuccess && ae != ncclInProgress)
+                return fail(c, BCGS_E_NCCL, "NCCL asynchronous error: %s (communicator aborted)",
+                            ncclGetErrorString(ae));
+            return fail(c, BCGS_E_NCCL, "NCCL wait exceeded %.0f s (communicator aborted)",
+                        c->comm_timeout_s);
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
 }
 
 // ------------------------------------------------------------------ communication
@@ -222,11 +283,29 @@ bcgs_status local_exchange_end(bcgs_ctx c, bool all, cudaStream_t hs)
     return BCGS_OK;
 }
 
-bcgs_status halo_on(bcgs_ctx c, double* v, cudaStream_t hs)
+// peer transport: send k planes of v (interior planes [0, k) down, [L - k, L) up) and land
+// the neighbours' planes in [gl, gl + k planes) and [gh, gh + k planes) (p2p.cuh)
+bcgs_status p2p_halo(bcgs_ctx c, const double* v, double* gl, double* gh, int k,
+                     cudaStream_t hs, int guarded)
+{
+    if (!c->p2p_ready) return fail(c, BCGS_E_STATE, "p2p transport not connected");
+    if (k > c->peers.cap)
+        return fail(c, BCGS_E_CONFIG, "halo of %d planes > p2p landing capacity %lld", k,
+                    (long long)c->peers.cap);
+    const int nb = (int)std::min<int64_t>(kNumSMs, (k * c->lay.plane + 255) / 256);
+    p2p::k_halo_send<<<nb, 256, 0, hs>>>(c->peers, v, c->lay.L, k, c->st, guarded);
+    p2p::k_halo_wait<<<1, 32, 0, hs>>>(c->peers, c->st, guarded);
+    p2p::k_halo_land<<<nb, 256, 0, hs>>>(c->peers, gl, gh, k, c->st, guarded);
+    CUDA_OK(c, cudaGetLastError());
+    return BCGS_OK;
+}
+
+bcgs_status halo_on(bcgs_ctx c, double* v, cudaStream_t hs, int guarded = 1)
 {
     if (c->nranks == 1 || (c->ablate & 1)) return BCGS_OK;   // ablation: timing only
     Prof pf(c, KC_HALO, 0.0, hs);
     const size_t pl = (size_t)c->lay.plane;
+    if (c->p2p) return p2p_halo(c, v, v - pl, v + c->lay.L * pl, 1, hs, guarded);
     if (c->lg) {
         const ptrdiff_t off = (char*)v - c->ws;   // same layout on every rank
         TRY(local_exchange_begin(c, hs));
@@ -258,8 +337,29 @@ bcgs_status halo_on(bcgs_ctx c, double* v, cudaStream_t hs)
 }
 
 bcgs_status halo(bcgs_ctx c, double* v) { return halo_on(c, v, c->s); }
+// outside an iteration (API calls, the x halo of begin / finish): not skipped when done
+bcgs_status halo_api(bcgs_ctx c, double* v) { return halo_on(c, v, c->s, 0); }
 
-// All-gather of every rank's ND Dot2 pairs (MPI2/4/5).
+// All-gather of `bytes` from every rank's `mine` (at the same workspace offset on every
+// rank) into dst[rank] (NCCL, or the in-process transport).
+bcgs_status allgather_bytes(bcgs_ctx c, const void* mine, void* dst, size_t bytes)
+{
+    if (c->lg) {
+        const ptrdiff_t off = (const char*)mine - c->ws;
+        TRY(local_exchange_begin(c, c->s));
+        for (int r = 0; r < c->nranks; ++r) {
+            bcgs_ctx p = c->lg->ctxs[r];
+            if (r != c->rank) CUDA_OK(c, cudaStreamWaitEvent(c->s, p->ev_ready, 0));
+            CUDA_OK(c, cudaMemcpyAsync((char*)dst + r * bytes, p->ws + off, bytes,
+                                       cudaMemcpyDeviceToDevice, c->s));
+        }
+        return local_exchange_end(c, true, c->s);
+    }
+    NCCL_OK(c, ncclAllGather(mine, dst, bytes, ncclUint8, c->comm, c->s));
+    return BCGS_OK;
+}
+
+// All-gather of every rank's ND Dot2 triples (MPI2/4/5).
 bcgs_status allgather_pairs(bcgs_ctx c, int nd)
 {
     Prof pf(c, KC_ALLGATHER, 0.0);
@@ -269,35 +369,91 @@ bcgs_status allgather_pairs(bcgs_ctx c, int nd)
                                        cudaMemcpyDeviceToDevice, c->s));
         return BCGS_OK;
     }
-    if (c->lg) {
-        TRY(local_exchange_begin(c, c->s));
-        for (int r = 0; r < c->nranks; ++r) {
-            bcgs_ctx p = c->lg->ctxs[r];
-            if (r != c->rank) CUDA_OK(c, cudaStreamWaitEvent(c->s, p->ev_ready, 0));
-            CUDA_OK(c, cudaMemcpyAsync(c->gath + (size_t)r * nd, p->rank_out, nd * sizeof(dd),
-                                       cudaMemcpyDeviceToDevice, c->s));
-        }
-        return local_exchange_end(c, true, c->s);
-    }
-    NCCL_OK(c, ncclAllGather(c->rank_out, c->gath, 2 * nd, ncclDouble, c->comm, c->s));
-    return BCGS_OK;
+    return allgather_bytes(c, c->rank_out, c->gath, nd * sizeof(dd));
 }
 
-// Reduce `nparts` partial pairs of ND dots, then run the scalar stage.
-template <int ND>
-bcgs_status reduce(bcgs_ctx c, int nparts, int stage)
+// Chain depth of a grid-stride element-wise producer (kEwBlocks x 256 threads): 2 x the
+// products per thread (R19 certification bound, dd.cuh); stencil producers pass 2 x 16.
+inline int ew_depth(int64_t n)
 {
+    const int64_t T = (int64_t)kEwBlocks * 256;
+    return (int)(2 * ((n + T - 1) / T + 2));
+}
+constexpr int kStencilDepth = 2 * 2 * stream::SZC;   // 2 points per plane and chain
+
+// Reduce `nparts` partial triples of ND dots, then complete the stage (certified) or park it
+// for the exact path.  src = the ND operand pairs (a_d, b_d), recorded for that path.
+// k3_mask bit d: dot d was accumulated with Dot3 chains (the r~ dots, dd.cuh)
+template <int ND>
+bcgs_status reduce(bcgs_ctx c, int nparts, int stage, int depth, int k3_mask,
+                   std::initializer_list<const double*> src)
+{
+    int i = 0;
+    for (const double* p : src) c->src[stage][i++] = p;
+    int self_mask = 0;   // a·a dots: their producers accumulate no Σ|h| (dot2_acc_self)
+    for (int d = 0; d < ND; ++d)
+        if (c->src[stage][2 * d] && c->src[stage][2 * d] == c->src[stage][2 * d + 1])
+            self_mask |= 1 << d;
+    const double nprod = (double)c->lay.nx * (double)c->lay.ny * (double)c->lay.nz;
+    if (c->p2p) {   // one kernel: finalize + one-shot peer exchange + rank-ordered combine
+        if (!c->p2p_ready) return fail(c, BCGS_E_STATE, "p2p transport not connected");
+        Prof pf(c, KC_FINALIZE, 0.0);
+        p2p::k_reduce_p2p<ND><<<1, 1024, 0, c->s>>>(c->peers, c->part, nparts, stage, c->st,
+                                                    c->hist, c->scal, depth, nprod, self_mask,
+                                                    k3_mask, (c->ablate & 2) ? 1 : 0);
+        CUDA_OK(c, cudaGetLastError());
+        return BCGS_OK;
+    }
     {
         Prof pf(c, KC_FINALIZE, 0.0);
         k_finalize<ND><<<1, 1024, 0, c->s>>>(c->part, nparts, stage, c->st, c->hist, c->scal,
-                                              c->rank_out, c->nranks);
+                                              c->rank_out, c->nranks, depth, nprod, self_mask,
+                                              k3_mask);
     }
     if (c->nranks > 1) {
         TRY(allgather_pairs(c, ND));
         Prof pf(c, KC_SCALARS, 0.0);
-        k_scalars<ND><<<1, 1, 0, c->s>>>(c->gath, c->nranks, stage, c->st, c->hist, c->scal);
+        k_scalars<ND><<<1, 1, 0, c->s>>>(c->gath, c->nranks, stage, c->st, c->hist, c->scal,
+                                         depth, nparts, nprod, self_mask, k3_mask);
     }
     CUDA_OK(c, cudaGetLastError());
+    return BCGS_OK;
+}
+
+// R19 fallback: the parked stage's flagged dots recomputed exactly (superaccumulators,
+// all-gathered across ranks and summed as integers) and the stage completed.  Returns the
+// stage in *stage (-1: nothing was parked).
+bcgs_status resolve(bcgs_ctx c, int* stage)
+{
+    *stage = -1;
+    int32_t* h = (int32_t*)c->h_pinned;
+    CUDA_OK(c, cudaMemcpyAsync(h, &c->st->pend_stage, 2 * sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, c->s));
+    TRY(sync_stream(c));
+    const int stg = h[0], mask = h[1];
+    if (!mask) return BCGS_OK;
+    const int64_t XL = xdot::XL, per_rank = 6 * XL;
+    CUDA_OK(c, cudaMemsetAsync(c->limbs, 0, sizeof(long long) * per_rank, c->s));
+    for (int d = 0; d < 5; ++d)
+        if (mask & (1 << d)) {
+            const double* a = c->src[stg][2 * d];
+            const double* b = c->src[stg][2 * d + 1];
+            if (!a || !b) return fail(c, BCGS_E_STATE, "exact dot: no operands for stage %d", stg);
+            xdot::k_exact_dot<<<kEwBlocks, 256, 0, c->s>>>(a, b, npts(c), c->limbs + d * XL,
+                                                           c->limbs + 5 * XL);
+        }
+    CUDA_OK(c, cudaGetLastError());
+    const long long* L = c->limbs;
+    if (c->p2p) {
+        p2p::k_limbs_p2p<<<1, 256, 0, c->s>>>(c->peers, c->limbs, c->glimbs, c->st);
+        L = c->glimbs;
+    } else if (c->nranks > 1) {
+        TRY(allgather_bytes(c, c->limbs, c->glimbs, sizeof(long long) * per_rank));
+        L = c->glimbs;
+    }
+    k_resolve<<<1, 1, 0, c->s>>>(c->st, L, c->nranks, per_rank, c->hist, c->scal);
+    CUDA_OK(c, cudaGetLastError());
+    *stage = stg;
     return BCGS_OK;
 }
 
@@ -313,6 +469,7 @@ bcgs_status halo_deep(bcgs_ctx c, const double* q, double* E, int k)
     const size_t pl = (size_t)c->lay.plane;
     const int64_t L = c->lay.L, KG = BCGS_MAX_DEGREE;
     Prof pf(c, KC_HALO, 0.0);
+    if (c->p2p) return p2p_halo(c, q, E + (KG - k) * pl, E + (KG + L) * pl, k, c->s, 1);
     if (c->lg) {
         const ptrdiff_t off = (const char*)q - c->ws;
         TRY(local_exchange_begin(c, c->s));
@@ -356,14 +513,15 @@ bcgs_status precond_g(bcgs_ctx c, const double* q, double* out, const DevState* 
     double* E = c->ext[0];
     double* A = c->ext[1];
     double* B = c->ext[2];
-    CUDA_OK(c, cudaMemcpyAsync(E + KG * pl, q, sizeof(double) * L * pl, cudaMemcpyDeviceToDevice,
-                               c->s));
+    // every write below is guarded by the device state (a parked solve, R19, leaves the
+    // fields the resumed iteration still needs untouched)
+    ref::k_copy<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(q, E + KG * pl, L * pl, st);
     TRY(halo_deep(c, q, E, k));
     const int v0 = (int)(c->rank == 0 ? KG : KG - k);
     const int v1 = (int)(c->rank == c->nranks - 1 ? KG + L : KG + L + k);
     if (c->kernels == 1 && k <= fused::KMAX_TB) {   // all k sweeps in one HBM pass
         Prof pf(c, KC_PRECOND, 16.0 * npts(c));
-        return fused::precond_g_tb(c, E, out, v0, v1);
+        return fused::precond_g_tb(c, E, out, v0, v1, st);
     }
     const int nx = (int)c->lay.nx, ny = (int)c->lay.ny;
     const dim3 blk(ref::BX, ref::BY);
@@ -386,8 +544,7 @@ bcgs_status precond_g(bcgs_ctx c, const double* q, double* out, const DevState* 
         xm2 = xm1;
         xm1 = dst;
     }
-    CUDA_OK(c, cudaMemcpyAsync(out, xm1 + KG * pl, sizeof(double) * L * pl,
-                               cudaMemcpyDeviceToDevice, c->s));
+    ref::k_copy<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(xm1 + KG * pl, out, L * pl, st);
     CUDA_OK(c, cudaGetLastError());
     return BCGS_OK;
 }
@@ -442,13 +599,18 @@ bcgs_status precond_ref(bcgs_ctx c, const double* q, double* out, const DevState
 }
 
 // ------------------------------------------------------------------ one outer iteration
-bcgs_status iteration_ref(bcgs_ctx c)
+// `from` >= 0: the remainder of an iteration whose reduction stage `from` was parked and has
+// been resolved (R19 fallback): only the steps after that stage are enqueued.
+bcgs_status iteration_ref(bcgs_ctx c, int from)
 {
     const int64_t n = npts(c);
     DevState* st = c->st;
     ref::Grid g = ref_grid(c, (int)c->lay.L);
     dim3 sg = stencil_grid(c), sb(ref::BX, ref::BY);
     const int nsb = (int)(sg.x * sg.y * sg.z);
+    if (from == STAGE_RHO) goto a14;
+    if (from == STAGE_OMEGA) goto a11;
+    if (from == STAGE_ALPHA) goto a6;
     // a2: p̂ = M^-1 p
     TRY(precond_ref(c, F(c, V_P), F(c, V_PH), st));
     // a3: halo p̂
@@ -460,8 +622,8 @@ bcgs_status iteration_ref(bcgs_ctx c)
                                                   c->part, st);
     }
     // a5: α
-    TRY(reduce<1>(c, nsb, STAGE_ALPHA));
-    // a6: s = r - α w
+    TRY(reduce<1>(c, nsb, STAGE_ALPHA, kStencilDepth, 1, {F(c, V_RT), F(c, V_W)}));
+a6:  // a6: s = r - α w
     {
         Prof pf(c, KC_AXPY, 24.0 * n);
         ref::k_axpy_s<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(F(c, V_R), F(c, V_W), n, st);
@@ -477,16 +639,18 @@ bcgs_status iteration_ref(bcgs_ctx c)
                                                   c->part, st);
     }
     // a10: ω
-    TRY(reduce<2>(c, nsb, STAGE_OMEGA));
-    // a11 + a12: x, r, r~ᵀr, rᵀr
+    TRY(reduce<2>(c, nsb, STAGE_OMEGA, kStencilDepth, 0,
+                  {F(c, V_T), F(c, V_R), F(c, V_T), F(c, V_T)}));   // s = r in place
+a11:  // a11 + a12: x, r, r~ᵀr, rᵀr
     {
         Prof pf(c, KC_UPDATE_XR, 64.0 * n);
         ref::k_update_xr<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(
             F(c, V_X), F(c, V_PH), F(c, V_RH), F(c, V_R), F(c, V_T), F(c, V_RT), n, c->part, st);
     }
     // a13: test, ρ, β
-    TRY(reduce<2>(c, kEwBlocks, STAGE_RHO));
-    // a14: p = r + β (p - ω w)
+    TRY(reduce<2>(c, kEwBlocks, STAGE_RHO, ew_depth(n), 1, {F(c, V_RT), F(c, V_R), F(c, V_R),
+                                                         F(c, V_R)}));
+a14:  // a14: p = r + β (p - ω w)
     {
         Prof pf(c, KC_UPDATE_P, 32.0 * n);
         ref::k_update_p<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(F(c, V_P), F(c, V_R), F(c, V_W),
@@ -496,14 +660,14 @@ bcgs_status iteration_ref(bcgs_ctx c)
     return BCGS_OK;
 }
 
-bcgs_status iteration(bcgs_ctx c)
+bcgs_status iteration(bcgs_ctx c, int from)
 {
-    if (c->pc == BCGS_PC_CHEB_G && c->nranks > 1) return iteration_ref(c);   // k-deep halos
+    if (c->pc == BCGS_PC_CHEB_G && c->nranks > 1) return iteration_ref(c, from);   // k-deep halos
     if (c->kernels == 1 && fused::supported(c, c->degree, c->pc != BCGS_PC_NONE))
-        return fused::iteration(c);
+        return fused::iteration(c, from);
     if (c->kernels == 1 && c->pc == BCGS_PC_NONE && c->lay.nx % 2 == 0)
-        return fused::iteration_none(c);
-    return iteration_ref(c);
+        return fused::iteration_none(c, from);
+    return iteration_ref(c, from);
 }
 
 bcgs_status enqueue_iterations(bcgs_ctx c, int n)
@@ -511,11 +675,13 @@ bcgs_status enqueue_iterations(bcgs_ctx c, int n)
     // graphs: single rank only (multi-rank runs launch directly; NCCL inside captured graphs
     // is supported but not exercised in round 1)
     // (inner-Krylov preconditioners synchronise the host inside an iteration: no graph)
-    if (c->use_graph && !c->profile && !c->lg && c->nranks == 1 && !inner_pc(c)) {
+    // graphs: one rank, or the p2p transport (kernels only); NCCL with BCGS_OPT_GRAPH = 2
+    const bool graph_ok = c->nranks == 1 || c->p2p || (c->comm && c->use_graph == 2);
+    if (c->use_graph && graph_ok && !c->profile && !c->lg && !inner_pc(c)) {
         if (!c->gexec) {
             cudaGraph_t graph;
             CUDA_OK(c, cudaStreamBeginCapture(c->s, cudaStreamCaptureModeThreadLocal));
-            bcgs_status st = iteration(c);
+            bcgs_status st = iteration(c, -1);
             cudaError_t e = cudaStreamEndCapture(c->s, &graph);
             if (st != BCGS_OK) return st;
             CUDA_OK(c, e);
@@ -525,7 +691,7 @@ bcgs_status enqueue_iterations(bcgs_ctx c, int n)
         for (int i = 0; i < n; ++i) CUDA_OK(c, cudaGraphLaunch(c->gexec, c->s));
         return BCGS_OK;
     }
-    for (int i = 0; i < n; ++i) TRY(iteration(c));
+    for (int i = 0; i < n; ++i) TRY(iteration(c, -1));
     return BCGS_OK;
 }
 
@@ -628,6 +794,7 @@ const char* bcgs_status_string(bcgs_status s)
     case BCGS_NOT_CONVERGED: return "not converged";
     case BCGS_BREAKDOWN: return "breakdown";
     case BCGS_E_STATE: return "call out of order";
+    case BCGS_E_COMM: return "peer transport error (timeout)";
     }
     return "unknown";
 }
@@ -666,11 +833,12 @@ bcgs_status bcgs_nccl_unique_id(void* out128)
 static bcgs_status create_ctx(const bcgs_grid_desc* grid, int32_t rank, int32_t nranks,
                               const void* nccl_unique_id, LocalGroup* lg, int32_t cuda_device,
                               void* d_workspace, size_t ws_bytes, void* cuda_stream,
-                              bcgs_ctx* out)
+                              bcgs_ctx* out, int p2p = 0)
 {
     if (!grid || !out || nranks < 1 || rank < 0 || rank >= nranks) return BCGS_E_INVALID;
     if (!(grid->h > 0.0)) return BCGS_E_INVALID;
-    if (nranks > 1 && !nccl_unique_id && !lg) return BCGS_E_INVALID;
+    if (nranks > 1 && !nccl_unique_id && !lg && !p2p) return BCGS_E_INVALID;
+    if (p2p && (nranks < 2 || nranks > p2p::MAXR)) return BCGS_E_INVALID;
     if (!bc_ok(grid)) return BCGS_E_CONFIG;
     Layout lay;
     if (!make_layout(grid, nranks, &lay)) return BCGS_E_CONFIG;
@@ -718,6 +886,22 @@ static bcgs_status create_ctx(const bcgs_grid_desc* grid, int32_t rank, int32_t 
     c->part = (dd*)(c->ws + lay.off_part);
     c->rank_out = (dd*)(c->ws + lay.off_rank);
     c->gath = (dd*)(c->ws + lay.off_gath);
+    c->limbs = (long long*)(c->ws + lay.off_limb);
+    c->glimbs = (long long*)(c->ws + lay.off_glimb);
+    if (p2p) {   // mailbox + landing zones (face halos; G(CI) k-deep halos up to `cap` planes)
+        c->p2p = 1;
+        c->peers.rank = rank;
+        c->peers.nranks = nranks;
+        c->peers.plane = lay.plane;
+        c->peers.cap = std::min<int64_t>(lay.L, 16);
+        c->peers.timeout_ns = 60ull * 1000000000ull;
+        c->mailbox_bytes = p2p::land_offset() +
+                           sizeof(double) * 4 * (size_t)c->peers.cap * (size_t)lay.plane;
+        CUDA_OK(c, cudaMalloc(&c->mailbox, c->mailbox_bytes));
+        CUDA_OK(c, cudaMemset(c->mailbox, 0, c->mailbox_bytes));
+        c->peers.mb[rank] = (p2p::Mailbox*)c->mailbox;
+        c->peers.land[rank] = (double*)(c->mailbox + p2p::land_offset());
+    }
     TRY(enter(c));
     CUDA_OK(c, cudaMemsetAsync(c->ws, 0, lay.total, c->s));   // zero ghost planes + state
     if (nranks > 1 && !lg) {
@@ -736,6 +920,82 @@ bcgs_status bcgs_create(const bcgs_grid_desc* grid, int32_t rank, int32_t nranks
 {
     return create_ctx(grid, rank, nranks, nccl_unique_id, nullptr, cuda_device, d_workspace,
                       ws_bytes, cuda_stream, out);
+}
+
+bcgs_status bcgs_create_p2p(const bcgs_grid_desc* grid, int32_t rank, int32_t nranks,
+                            int32_t cuda_device, void* d_workspace, size_t ws_bytes,
+                            void* cuda_stream, bcgs_ctx* out)
+{
+    return create_ctx(grid, rank, nranks, nullptr, nullptr, cuda_device, d_workspace, ws_bytes,
+                      cuda_stream, out, 1);
+}
+
+// 128-byte record: [0, 64) cudaIpcMemHandle_t of the mailbox, then magic, rank, nranks, pid,
+// mailbox bytes (int64 each)
+bcgs_status bcgs_p2p_handle(bcgs_ctx c, void* out128)
+{
+    if (!c || !out128 || !c->p2p) return BCGS_E_INVALID;
+    CUDA_OK(c, cudaSetDevice(c->device));
+    cudaIpcMemHandle_t h;
+    CUDA_OK(c, cudaIpcGetMemHandle(&h, c->mailbox));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
+    char* o = (char*)out128;
+    memset(o, 0, 128);
+    memcpy(o, &h, 64);
+    const int64_t rec[5] = {0x6263677332703270ll, c->rank, c->nranks, (int64_t)getpid(),
+                            (int64_t)c->mailbox_bytes};
+    memcpy(o + 64, rec, sizeof rec);
+    return BCGS_OK;
+}
+
+bcgs_status bcgs_p2p_connect(bcgs_ctx c, const void* all_handles)
+{
+    if (!c || !all_handles || !c->p2p) return BCGS_E_INVALID;
+    if (c->p2p_ready) return fail(c, BCGS_E_STATE, "p2p transport already connected");
+    CUDA_OK(c, cudaSetDevice(c->device));
+    const char* in = (const char*)all_handles;
+    for (int r = 0; r < c->nranks; ++r) {
+        int64_t rec[5];
+        memcpy(rec, in + 128 * r + 64, sizeof rec);
+        if (rec[0] != 0x6263677332703270ll || rec[1] != r || rec[2] != c->nranks ||
+            rec[4] != (int64_t)c->mailbox_bytes)
+            return fail(c, BCGS_E_INVALID, "p2p handle %d: wrong record (rank %lld of %lld)", r,
+                        (long long)rec[1], (long long)rec[2]);
+        if (r == c->rank) continue;
+        if (rec[3] == (int64_t)getpid())
+            return fail(c, BCGS_E_CONFIG, "p2p peer %d is in this process: use "
+                        "bcgs_create_local_p2p", r);
+        cudaIpcMemHandle_t h;
+        memcpy(&h, in + 128 * r, 64);
+        void* p = nullptr;
+        CUDA_OK(c, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_opened.push_back(p);
+        c->peers.mb[r] = (p2p::Mailbox*)p;
+        c->peers.land[r] = (double*)((char*)p + p2p::land_offset());
+    }
+    c->p2p_ready = 1;
+    return BCGS_OK;
+}
+
+bcgs_status bcgs_create_local_p2p(const bcgs_grid_desc* grid, int32_t nranks,
+                                  int32_t cuda_device, void* const* d_workspaces,
+                                  size_t ws_bytes, void* cuda_stream, bcgs_ctx* outs)
+{
+    if (!grid || !outs || !d_workspaces || nranks < 2 || nranks > p2p::MAXR)
+        return BCGS_E_INVALID;
+    for (int r = 0; r < nranks; ++r) {
+        bcgs_status st = create_ctx(grid, r, nranks, nullptr, nullptr, cuda_device,
+                                    d_workspaces[r], ws_bytes, cuda_stream, &outs[r], 1);
+        if (st != BCGS_OK) return st;
+    }
+    for (int r = 0; r < nranks; ++r) {   // same process: the peers' pointers directly
+        for (int q = 0; q < nranks; ++q) {
+            outs[r]->peers.mb[q] = outs[q]->peers.mb[q];
+            outs[r]->peers.land[q] = outs[q]->peers.land[q];
+        }
+        outs[r]->p2p_ready = 1;
+    }
+    return BCGS_OK;
 }
 
 bcgs_status bcgs_create_local(const bcgs_grid_desc* grid, int32_t nranks, int32_t cuda_device,
@@ -766,6 +1026,8 @@ void bcgs_destroy(bcgs_ctx c)
     drop_graph(c);
     for (auto e : c->free_ev) cudaEventDestroy(e);
     if (c->comm) ncclCommDestroy(c->comm);
+    for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+    if (c->mailbox) cudaFree(c->mailbox);
     if (c->ev_ready) cudaEventDestroy(c->ev_ready);
     if (c->ev_pre) cudaEventDestroy(c->ev_pre);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
@@ -804,6 +1066,11 @@ bcgs_status bcgs_set_option(bcgs_ctx c, int32_t option, int64_t value)
     case BCGS_OPT_MULTIPASS: c->mp_min = std::max<int>(4, (int)value); break;
     case BCGS_OPT_ABLATE: c->ablate = (int)(value & 3); break;
     case BCGS_OPT_SYNC2: c->sync2_opt = (int)value; drop_graph(c); break;
+    case BCGS_OPT_EXACT_DOT: c->exact_opt = value ? 1 : 0; break;
+    case BCGS_OPT_COMM_TIMEOUT:   // NCCL host waits; p2p device waits (default 60 s)
+        c->comm_timeout_s = value > 0 ? (double)value : 300.0;
+        c->peers.timeout_ns = (value > 0 ? (unsigned long long)value : 60ull) * 1000000000ull;
+        break;
     default: return fail(c, BCGS_E_INVALID, "unknown option %d", option);
     }
     drop_graph(c);
@@ -904,6 +1171,27 @@ bcgs_status bcgs_set_inner_solver(bcgs_ctx c, double rel_tol, int32_t max_iter)
 
 int64_t bcgs_inner_iterations(bcgs_ctx c) { return c ? c->in_iters : -1; }
 
+bcgs_status bcgs_certification_info(bcgs_ctx c, double* out9)
+{
+    if (!c || !out9) return BCGS_E_INVALID;
+    CUDA_OK(c, cudaStreamSynchronize(c->s));
+    CUDA_OK(c, cudaMemcpy(out9, c->st->cert_last, 9 * sizeof(double), cudaMemcpyDeviceToHost));
+    int32_t nref = 0;
+    CUDA_OK(c, cudaMemcpy(&nref, &c->st->n_refused, sizeof nref, cudaMemcpyDeviceToHost));
+    out9[9] = nref;
+    return BCGS_OK;
+}
+
+int32_t bcgs_exact_dots(bcgs_ctx c)
+{
+    if (!c) return -1;
+    int32_t v = -1;
+    if (cudaStreamSynchronize(c->s) != cudaSuccess ||
+        cudaMemcpy(&v, &c->st->n_exact, sizeof v, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return -1;
+    return v;
+}
+
 bcgs_status bcgs_set_eigen_bounds(bcgs_ctx c, double a, double b)
 {
     if (!c) return BCGS_E_INVALID;
@@ -933,7 +1221,7 @@ bcgs_status bcgs_begin(bcgs_ctx c, double rel_tol, int32_t max_iter, int32_t fix
     c->t0 = std::chrono::steady_clock::now();
     const int64_t n = npts(c);
     const size_t bytes = sizeof(double) * (size_t)n;
-    k_init_state<<<1, 1, 0, c->s>>>(c->st, rel_tol, max_iter, fixed_iters);
+    k_init_state<<<1, 1, 0, c->s>>>(c->st, rel_tol, max_iter, fixed_iters, c->exact_opt);
     c->in_iters = 0;
     c->sync2 = c->sync2_opt ? 1 : 0;
     // Alg. 3 l.1-4: r0 = b - A x0; r~ = r0; p0 = r0; ρ0 = r~ᵀr0.  The initial
@@ -942,7 +1230,7 @@ bcgs_status bcgs_begin(bcgs_ctx c, double rel_tol, int32_t max_iter, int32_t fix
     const bool x0 = c->have_x0;
     c->have_x0 = 0;
     if (x0) {
-        TRY(halo(c, F(c, V_X)));
+        TRY(halo_api(c, F(c, V_X)));
         ref::k_stencil_dot<0><<<stencil_grid(c), dim3(ref::BX, ref::BY), 0, c->s>>>(
             F(c, V_X), nullptr, F(c, V_R), ref_grid(c, (int)c->lay.L), 0, nullptr, nullptr);
         ref::k_residual0<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(F(c, V_B), F(c, V_R), n);
@@ -955,7 +1243,8 @@ bcgs_status bcgs_begin(bcgs_ctx c, double rel_tol, int32_t max_iter, int32_t fix
     ref::k_dot2<2><<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(F(c, V_B), F(c, V_B), F(c, V_RT),
                                                            F(c, V_R), n, c->part);
     CUDA_OK(c, cudaGetLastError());
-    TRY(reduce<2>(c, kEwBlocks, STAGE_SETUP));
+    TRY(reduce<2>(c, kEwBlocks, STAGE_SETUP, ew_depth(n), 3,
+                  {F(c, V_B), F(c, V_B), F(c, V_RT), F(c, V_R)}));
     c->begun = 1;
     c->launched = 0;
     c->fixed = fixed_iters;
@@ -980,13 +1269,36 @@ bcgs_status bcgs_join(bcgs_ctx c)
     return leave(c);
 }
 
-static bcgs_status poll_state(bcgs_ctx c, int32_t* done, int32_t* iter)
+static bcgs_status read_state(bcgs_ctx c, int32_t* done, int32_t* iter)
 {
     CUDA_OK(c, cudaMemcpyAsync(c->h_pinned, &c->st->iter, 2 * sizeof(int32_t),
                                cudaMemcpyDeviceToHost, c->s));
-    CUDA_OK(c, cudaStreamSynchronize(c->s));
+    TRY(sync_stream(c));
     *iter = ((int32_t*)c->h_pinned)[0];
     *done = ((int32_t*)c->h_pinned)[1];
+    if (*done == DONE_COMM_ERROR)
+        return fail(c, BCGS_E_COMM, "p2p transport: a peer did not answer within the timeout");
+    return BCGS_OK;
+}
+
+// Poll the device state; a parked reduction (DONE_PENDING, R19) is resolved exactly, the
+// interrupted iteration completed and the iterations enqueued after it (device no-ops while
+// parked) enqueued again.  Every rank sees the same parked stage (the certification runs
+// on identical combined values), so the collectives of the resolution match across ranks.
+static bcgs_status poll_state(bcgs_ctx c, int32_t* done, int32_t* iter)
+{
+    TRY(read_state(c, done, iter));
+    while (*done == DONE_PENDING) {
+        int stage;
+        TRY(resolve(c, &stage));
+        if (stage < 0) return fail(c, BCGS_E_STATE, "parked solve without a parked stage");
+        if (stage != STAGE_SETUP) TRY(iteration(c, stage));
+        TRY(read_state(c, done, iter));
+        if (*done == DONE_RUNNING && c->launched > *iter) {
+            TRY(enqueue_iterations(c, c->launched - *iter));
+            TRY(read_state(c, done, iter));
+        }
+    }
     return BCGS_OK;
 }
 
@@ -999,13 +1311,15 @@ bcgs_status bcgs_finish(bcgs_ctx c, bcgs_report* out)
     // true residual (R22): ||b - A x|| / ||b||, once
     double true_rel = NAN, rel = NAN;
     {
-        TRY(halo(c, F(c, V_X)));
+        TRY(halo_api(c, F(c, V_X)));
         ref::k_stencil_dot<0><<<stencil_grid(c), dim3(ref::BX, ref::BY), 0, c->s>>>(
             F(c, V_X), nullptr, F(c, V_IO), ref_grid(c, (int)c->lay.L), 0, nullptr, nullptr);
         ref::k_residual0<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(F(c, V_B), F(c, V_IO), npts(c));
         ref::k_dot2<1><<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(F(c, V_IO), F(c, V_IO), nullptr,
                                                                nullptr, npts(c), c->part);
-        TRY(reduce<1>(c, kEwBlocks, STAGE_DOT));
+        TRY(reduce<1>(c, kEwBlocks, STAGE_DOT, ew_depth(npts(c)), 1, {F(c, V_IO), F(c, V_IO)}));
+        int stg;
+        TRY(resolve(c, &stg));
         double h[2];
         CUDA_OK(c, cudaMemcpyAsync(h, c->st->scratch, sizeof h, cudaMemcpyDeviceToHost, c->s));
         double nbv;
@@ -1097,7 +1411,7 @@ bcgs_status bcgs_apply_operator(bcgs_ctx c, const double* d_in, double* d_out,
     const size_t bytes = sizeof(double) * (size_t)npts(c);
     double* io = F(c, V_IO);
     CUDA_OK(c, cudaMemcpyAsync(io, d_in, bytes, cudaMemcpyDeviceToDevice, c->s));
-    if (!block_local) TRY(halo(c, io));
+    if (!block_local) TRY(halo_api(c, io));
     else {
         CUDA_OK(c, cudaMemsetAsync(io - c->lay.plane, 0, sizeof(double) * c->lay.plane, c->s));
         CUDA_OK(c, cudaMemsetAsync(io + npts(c), 0, sizeof(double) * c->lay.plane, c->s));
@@ -1131,10 +1445,13 @@ bcgs_status bcgs_dot(bcgs_ctx c, const double* d_a, const double* d_b, double* h
 {
     if (!c || !d_a || !d_b || !host_out) return BCGS_E_INVALID;
     TRY(enter(c));
+    k_set_exact<<<1, 1, 0, c->s>>>(c->st, c->exact_opt);
     ref::k_dot2<1><<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(d_a, d_b, nullptr, nullptr, npts(c),
                                                            c->part);
     CUDA_OK(c, cudaGetLastError());
-    TRY(reduce<1>(c, kEwBlocks, STAGE_DOT));
+    TRY(reduce<1>(c, kEwBlocks, STAGE_DOT, ew_depth(npts(c)), 1, {d_a, d_b}));
+    int stg;
+    TRY(resolve(c, &stg));
     CUDA_OK(c, cudaMemcpyAsync(c->h_pinned, c->st->scratch, sizeof(double),
                                cudaMemcpyDeviceToHost, c->s));
     CUDA_OK(c, cudaStreamSynchronize(c->s));

@@ -14,13 +14,17 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
+
+#include <unistd.h>
 
 #include "../../include/bcgs.h"
 #include "dd.cuh"
 #include "state.cuh"
 #include "ref_shapes.cuh"
 #include "k_fused.cuh"
+#include "p2p.cuh"
 
 constexpr int kNumSMs = 148;
 constexpr int kEwBlocks = kNumSMs * 8;   // element-wise grid: fixed -> deterministic partials
@@ -45,7 +49,7 @@ struct Layout {
     size_t off_vec[V_COUNT_MAX];
     int64_t ext_elems;
     size_t off_ext[3];
-    size_t off_state, off_hist, off_scal, off_part, off_rank, off_gath, total;
+    size_t off_state, off_hist, off_scal, off_part, off_rank, off_gath, off_limb, off_glimb, total;
 };
 
 constexpr int V_X = 0, V_R = 1, V_RT = 2, V_P = 3, V_PH = 4, V_RH = 5, V_W = 6, V_T = 7,
@@ -89,6 +93,9 @@ inline bool make_layout(const bcgs_grid_desc* g, int32_t nranks, Layout* lay)
     lay->off_part = off;  off = align_up(off + sizeof(dd) * 5 * (size_t)lay->n_part);
     lay->off_rank = off;  off = align_up(off + sizeof(dd) * 5);
     lay->off_gath = off;  off = align_up(off + sizeof(dd) * 5 * (size_t)nranks);
+    // R19 exact path: this rank's superaccumulators [5 dots + flag][XL] and all ranks' copies
+    lay->off_limb = off;  off = align_up(off + sizeof(long long) * 6 * xdot::XL);
+    lay->off_glimb = off; off = align_up(off + sizeof(long long) * 6 * xdot::XL * (size_t)nranks);
     lay->total = off;
     return true;
 }
@@ -142,6 +149,9 @@ struct bcgs_ctx_s {
     DevState* st = nullptr;
     double *hist = nullptr, *scal = nullptr;
     dd *part = nullptr, *rank_out = nullptr, *gath = nullptr;
+    long long *limbs = nullptr, *glimbs = nullptr;   // R19 exact path (xdot.cuh)
+    const double* src[6][10] = {};   // operand pairs of each reduction stage (exact path)
+    int exact_opt = 0;               // BCGS_OPT_EXACT_DOT
     double* h_pinned = nullptr;    // small pinned buffer for flag polls
     // options
     int kernels = 1, use_graph = 1, profile = 0, poll = 8, tb_variant = 7;
@@ -178,6 +188,14 @@ struct bcgs_ctx_s {
     cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
     cudaStream_t s_comm = nullptr;              // halo stream (nranks > 1), overlapped
     cudaEvent_t ev_pre = nullptr, ev_halo = nullptr;
+    // peer-memory transport (p2p.cuh): own mailbox (+ landing zones), the peers' mapped
+    // mailboxes, and which of them were opened through CUDA IPC (closed at destroy)
+    int p2p = 0, p2p_ready = 0;
+    p2p::Peers peers{};
+    char* mailbox = nullptr;
+    size_t mailbox_bytes = 0;
+    std::vector<void*> ipc_opened;
+    double comm_timeout_s = 300.0;              // NCCL: host-side wait limit before abort
     std::string err;
 };
 

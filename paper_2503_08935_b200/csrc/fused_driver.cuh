@@ -22,16 +22,16 @@ __global__ void k_update_xr_s(double* __restrict__ x, const double* __restrict__
 {
     if (st->done) return;
     const double alpha = st->alpha, omega = st->omega;
-    double p[2] = {0.0, 0.0}, q[2] = {0.0, 0.0};
+    double p[2] = {0.0, 0.0}, m[2] = {0.0, 0.0}, q[2] = {0.0, 0.0}, ab[2] = {0.0, 0.0};
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
          c += (int64_t)gridDim.x * blockDim.x) {
         x[c] = upd_x(x[c], ph[c], rh[c], alpha, omega);
         const double rn = upd_r(s[c], t[c], omega);
         r[c] = rn;
-        dot2_acc(p[0], q[0], rt[c], rn);
-        dot2_acc(p[1], q[1], rn, rn);
+        dot3_acc(p[0], m[0], q[0], ab[0], rt[c], rn);
+        dot2_acc_self(p[1], q[1], rn);
     }
-    block_reduce_dd<2>(p, q, part + (int64_t)blockIdx.x * 2);
+    block_reduce_dd<2>(p, m, q, ab, part + (int64_t)blockIdx.x * 2);
 }
 
 // 2-sync (R31): apply the stop decided at the ω stage once x and r are updated
@@ -112,13 +112,14 @@ bcgs_status launch_tb(bcgs_ctx c, TbArgs& a)
 
 // G(CI) on P > 1 ranks through the temporally blocked kernel: input = the extended slab
 // (k-deep halos already exchanged), zero ghosts outside [v0, v1), outputs planes [KG, KG+L).
-bcgs_status precond_g_tb(bcgs_ctx c, const double* E, double* out, int v0, int v1)
+bcgs_status precond_g_tb(bcgs_ctx c, const double* E, double* out, int v0, int v1,
+                         const DevState* st)
 {
     TbArgs a{};
     const int64_t KG = BCGS_MAX_DEGREE;
     a.q = E;
     a.out = out - KG * c->lay.plane;
-    a.st = nullptr;
+    a.st = st;
     a.ext = 1;
     a.zv0 = v0;
     a.zv1 = v1;
@@ -181,13 +182,18 @@ bcgs_status halo_stencil(bcgs_ctx c, double* v, const double* a, double* out, in
 // Unpreconditioned iteration (M = I: BiCGS, Table II row 1; config C1) on the streaming
 // kernels: no copies for p̂ = p and r̂ = s.  168 B/pt: w = A p + r~ᵀw (24), s (24),
 // t = A s + tᵀs, tᵀt (24), x / r + r~ᵀr, rᵀr (64), p (32).
-bcgs_status iteration_none(bcgs_ctx c)
+// from >= 0: resume after the resolved stage `from` (R19 fallback, bcgs_api.cu resolve).
+bcgs_status iteration_none(bcgs_ctx c, int from)
 {
     const int64_t n = npts(c);
     DevState* st = c->st;
     int np1 = 0, np2 = 0;
+    if (from == STAGE_RHO) goto a14;
+    if (from == STAGE_OMEGA) goto a11;
+    if (from == STAGE_ALPHA) goto a6;
     TRY(halo_stencil<1>(c, F(c, V_P), F(c, V_RT), F(c, V_W), KC_STENCIL1, &np1));
-    TRY(reduce<1>(c, np1, STAGE_ALPHA));
+    TRY(reduce<1>(c, np1, STAGE_ALPHA, kStencilDepth, 1, {F(c, V_RT), F(c, V_W)}));
+a6:
     {
         Prof pf(c, KC_AXPY, 24.0 * n);
         stream::k_axpy_s2<<<kEwBlocks, 256, 0, c->s>>>((double2*)F(c, V_S),
@@ -195,7 +201,9 @@ bcgs_status iteration_none(bcgs_ctx c)
                                                        (const double2*)F(c, V_W), n / 2, st);
     }
     TRY(halo_stencil<2>(c, F(c, V_S), F(c, V_S), F(c, V_T), KC_STENCIL2, &np2));
-    TRY(reduce<2>(c, np2, STAGE_OMEGA));
+    TRY(reduce<2>(c, np2, STAGE_OMEGA, kStencilDepth, 0,
+                  {F(c, V_T), F(c, V_S), F(c, V_T), F(c, V_T)}));
+a11:
     {
         Prof pf(c, KC_FUSED_XR, 64.0 * n);
         stream::k_update_xr2<2><<<kEwBlocks, 256, 0, c->s>>>(
@@ -203,7 +211,9 @@ bcgs_status iteration_none(bcgs_ctx c)
             (const double2*)F(c, V_S), (double2*)F(c, V_R), (const double2*)F(c, V_T),
             (const double2*)F(c, V_RT), n / 2, c->part, st);
     }
-    TRY(reduce<2>(c, kEwBlocks, STAGE_RHO));
+    TRY(reduce<2>(c, kEwBlocks, STAGE_RHO, ew_depth(n), 1,
+                  {F(c, V_RT), F(c, V_R), F(c, V_R), F(c, V_R)}));
+a14:
     {
         Prof pf(c, KC_UPDATE_P, 32.0 * n);
         stream::k_update_p2<<<kEwBlocks, 256, 0, c->s>>>((double2*)F(c, V_P),
@@ -214,7 +224,7 @@ bcgs_status iteration_none(bcgs_ctx c)
     return BCGS_OK;
 }
 
-bcgs_status iteration(bcgs_ctx c)
+bcgs_status iteration(bcgs_ctx c, int from)
 {
     const int64_t n = npts(c);
     DevState* st = c->st;
@@ -222,6 +232,12 @@ bcgs_status iteration(bcgs_ctx c)
     ref::Grid g = ref_grid(c, (int)c->lay.L);
     dim3 sg = stencil_grid(c), sb(ref::BX, ref::BY);
     const int nsb = (int)(sg.x * sg.y * sg.z);
+    const bool vec = (c->lay.nx % 2) == 0;   // 16-byte rows: vectorised streaming kernels
+    int np1 = nsb, np2 = nsb;
+    if (from == STAGE_RHO) return BCGS_OK;   // a14 is folded into the next iteration's K1
+    if (from == STAGE_OMEGA2) goto a11_sync2;
+    if (from == STAGE_OMEGA) goto a11;
+    if (from == STAGE_ALPHA) goto k2;
     {   // K1: a14 (previous iteration) + a2
         TbArgs a{};
         a.r = F(c, V_R);
@@ -235,8 +251,6 @@ bcgs_status iteration(bcgs_ctx c)
         Prof pf(c, KC_FUSED_P1, 40.0 * n);
         TRY(launch_tb<MODE_P>(c, a));
     }
-    const bool vec = (c->lay.nx % 2) == 0;   // 16-byte rows: vectorised streaming kernels
-    int np1 = nsb, np2 = nsb;
     if (vec) {
         TRY(halo_stencil<1>(c, ph, F(c, V_RT), F(c, V_W), KC_STENCIL1, &np1));
     } else {
@@ -245,7 +259,8 @@ bcgs_status iteration(bcgs_ctx c)
         ref::k_stencil_dot<1><<<sg, sb, 0, c->s>>>(ph, F(c, V_RT), F(c, V_W), g, 0,
                                                   c->part, st);
     }
-    TRY(reduce<1>(c, np1, STAGE_ALPHA));
+    TRY(reduce<1>(c, np1, STAGE_ALPHA, kStencilDepth, 1, {F(c, V_RT), F(c, V_W)}));
+k2:
     {   // K2: a6 + a7
         TbArgs a{};
         a.r = F(c, V_R);
@@ -267,7 +282,12 @@ bcgs_status iteration(bcgs_ctx c)
                                                   c->part, st);
     }
     if (c->sync2) {   // ω, ρ_new, ||r||², test, β now; the stop applies after a11 + a12
-        TRY(reduce<5>(c, np2, STAGE_OMEGA2));
+        TRY(reduce<5>(c, np2, STAGE_OMEGA2, kStencilDepth, 12,
+                      {F(c, V_T), F(c, V_S), F(c, V_T), F(c, V_T), F(c, V_RT), F(c, V_S),
+                       F(c, V_RT), F(c, V_T), F(c, V_S), F(c, V_S)}));
+    }
+a11_sync2:
+    if (c->sync2) {
         Prof pf(c, KC_FUSED_XR, 56.0 * n);
         stream::k_update_xr2<0><<<kEwBlocks, 256, 0, c->s>>>(
             (double2*)F(c, V_X), (const double2*)F(c, V_PH), (const double2*)F(c, V_RH),
@@ -277,7 +297,9 @@ bcgs_status iteration(bcgs_ctx c)
         CUDA_OK(c, cudaGetLastError());
         return BCGS_OK;
     }
-    TRY(reduce<2>(c, np2, STAGE_OMEGA));
+    TRY(reduce<2>(c, np2, STAGE_OMEGA, kStencilDepth, 0,
+                  {F(c, V_T), F(c, V_S), F(c, V_T), F(c, V_T)}));
+a11:
     {
         Prof pf(c, KC_FUSED_XR, 64.0 * n);
         if (vec)
@@ -290,7 +312,8 @@ bcgs_status iteration(bcgs_ctx c)
                 F(c, V_X), F(c, V_PH), F(c, V_RH), F(c, V_S), F(c, V_R), F(c, V_T), F(c, V_RT),
                 n, c->part, st);
     }
-    TRY(reduce<2>(c, kEwBlocks, STAGE_RHO));
+    TRY(reduce<2>(c, kEwBlocks, STAGE_RHO, ew_depth(n), 1,
+                  {F(c, V_RT), F(c, V_R), F(c, V_R), F(c, V_R)}));
     CUDA_OK(c, cudaGetLastError());
     return BCGS_OK;
 }

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(BX * BY) k_stencil_dot(const double* __restric
     const int i = blockIdx.x * BX + threadIdx.x, j = blockIdx.y * BY + threadIdx.y;
     const int k0 = blockIdx.z * ZC, k1 = min(g.L, k0 + ZC);
     constexpr int NDA = (ND > 0) ? ND : 1;
-    double p[NDA] = {}, s[NDA] = {};
+    double p[NDA] = {}, m[NDA] = {}, s[NDA] = {}, ab[NDA] = {};
     if (i < g.nx && j < g.ny) {
         const int64_t plane = (int64_t)g.nx * g.ny;
         int64_t c = i + (int64_t)g.nx * j + plane * k0;
@@ -93,15 +93,16 @@ __global__ void __launch_bounds__(BX * BY) k_stencil_dot(const double* __restric
                               : (block_local && (k % g.Lb) == g.Lb - 1) ? 0.0 : vzp;
             const double o = stencil_at(in, c, i, j, g.nx, g.ny, zm, zp, g.h2inv, g.bc.m);
             out[c] = o;
-            if (ND >= 1) dot2_acc(p[0], s[0], a[c], o);
-            if (ND >= 2) dot2_acc(p[ND - 1], s[ND - 1], o, o);
+            if (ND == 1) dot3_acc(p[0], m[0], s[0], ab[0], a[c], o);   // r~ᵀw: Dot3
+            if (ND == 2) dot2_acc(p[0], s[0], ab[0], a[c], o);         // tᵀs: Dot2
+            if (ND >= 2) dot2_acc_self(p[ND - 1], s[ND - 1], o);
             vzm = vc;
             vc = vzp;
         }
     }
     if (ND > 0) {
         const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-        block_reduce_dd<NDA>(p, s, part + (int64_t)bid * ND);
+        block_reduce_dd<NDA>(p, m, s, ab, part + (int64_t)bid * ND);
     }
 }
 
@@ -214,13 +215,13 @@ __global__ void k_dot2(const double* __restrict__ a0, const double* __restrict__
                        const double* __restrict__ a1, const double* __restrict__ b1, int64_t n,
                        dd* __restrict__ part)
 {
-    double p[ND] = {}, s[ND] = {};
+    double p[ND] = {}, m[ND] = {}, s[ND] = {}, ab[ND] = {};
     EW_LOOP(n)
     {
-        dot2_acc(p[0], s[0], a0[c], b0[c]);
-        if (ND > 1) dot2_acc(p[ND - 1], s[ND - 1], a1[c], b1[c]);
+        dot3_acc(p[0], m[0], s[0], ab[0], a0[c], b0[c]);
+        if (ND > 1) dot3_acc(p[ND - 1], m[ND - 1], s[ND - 1], ab[ND - 1], a1[c], b1[c]);
     }
-    block_reduce_dd<ND>(p, s, part + (int64_t)blockIdx.x * ND);
+    block_reduce_dd<ND>(p, m, s, ab, part + (int64_t)blockIdx.x * ND);
 }
 
 // a6, KernelBiCGS2: s = r - α w  (in place on r)
@@ -241,16 +242,16 @@ __global__ void k_update_xr(double* __restrict__ x, const double* __restrict__ p
 {
     if (st->done) return;
     const double alpha = st->alpha, omega = st->omega;
-    double p[2] = {0.0, 0.0}, s[2] = {0.0, 0.0};
+    double p[2] = {0.0, 0.0}, m[2] = {0.0, 0.0}, s[2] = {0.0, 0.0}, ab[2] = {0.0, 0.0};
     EW_LOOP(n)
     {
         x[c] = upd_x(x[c], ph[c], rh[c], alpha, omega);
         const double rn = upd_r(r[c], t[c], omega);
         r[c] = rn;
-        dot2_acc(p[0], s[0], rt[c], rn);
-        dot2_acc(p[1], s[1], rn, rn);
+        dot3_acc(p[0], m[0], s[0], ab[0], rt[c], rn);
+        dot2_acc_self(p[1], s[1], rn);
     }
-    block_reduce_dd<2>(p, s, part + (int64_t)blockIdx.x * 2);
+    block_reduce_dd<2>(p, m, s, ab, part + (int64_t)blockIdx.x * 2);
 }
 
 // a14, KernelBiCGS6: p = r + β (p - ω w)
@@ -267,68 +268,60 @@ __global__ void k_update_p(double* __restrict__ p, const double* __restrict__ r,
 
 // ------------------------------------------------------------------- reduction finalize
 // One CTA combines `nparts` block partials (fixed order: contiguous chunks per thread,
-// then the deterministic block tree) into this rank's (hi, lo) pairs.  nranks == 1: the
-// global value is formed immediately and the stage's scalar update runs.  nranks > 1:
-// the pairs go to `rank_out` for the NCCL all-gather; k_scalars finishes.
+// then the deterministic block tree) into this rank's (hi, lo, ab) triples.  nranks == 1:
+// the stage is completed (certified, or parked for the exact path: finish_stage).
+// nranks > 1: the triples go to `rank_out` for the all-gather; k_scalars finishes.
+// depth = 2 x the longest per-thread product chain of the producer kernel; the bound D
+// adds the block, finalize and rank trees (dd.cuh, DESIGN.md §4 "Reductions").
+__host__ __device__ inline int reduce_depth(int depth, int nparts, int nranks)
+{
+    return depth + 2 * ((nparts + 1023) / 1024) + 48 + 2 * nranks;
+}
+
 template <int ND>
 __global__ void __launch_bounds__(1024) k_finalize(const dd* __restrict__ part, int nparts,
                                                    int stage, DevState* st, double* hist,
-                                                   double* scal, dd* rank_out, int nranks)
+                                                   double* scal, dd* rank_out, int nranks,
+                                                   int depth, double nprod, int self_mask,
+                                                   int k3_mask)
 {
     if (stage != STAGE_SETUP && stage != STAGE_DOT && st->done) return;
-    double p[ND], s[ND];
-#pragma unroll
-    for (int d = 0; d < ND; ++d) { p[d] = 0.0; s[d] = 0.0; }
-    // thread t combines partials t, t + T, t + 2T, ... (coalesced; 8 loads in flight)
-    const int T = blockDim.x;
-    int b = threadIdx.x;
-    for (; b + 7 * T < nparts; b += 8 * T) {
-        dd v[8][ND];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-#pragma unroll
-            for (int d = 0; d < ND; ++d) v[u][d] = part[(int64_t)(b + u * T) * ND + d];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-#pragma unroll
-            for (int d = 0; d < ND; ++d) dd_add(p[d], s[d], v[u][d].hi, v[u][d].lo);
-    }
-    for (; b < nparts; b += T)
-#pragma unroll
-        for (int d = 0; d < ND; ++d) dd_add(p[d], s[d], part[(int64_t)b * ND + d].hi,
-                                            part[(int64_t)b * ND + d].lo);
     __shared__ dd res[ND];
-    block_reduce_dd<ND>(p, s, res);
-    __syncthreads();
+    combine_partials<ND>(part, nparts, res);
     if (threadIdx.x == 0) {
         if (nranks > 1) {
 #pragma unroll
             for (int d = 0; d < ND; ++d) rank_out[d] = res[d];
         } else {
-            double v[ND > 2 ? ND : 2] = {};
+            dd comb[ND];
 #pragma unroll
             for (int d = 0; d < ND; ++d) {
-                double P = 0.0, S = 0.0;
-                dd_add(P, S, res[d].hi, res[d].lo);
-                v[d] = P + S;
+                comb[d] = dd{0.0, 0.0, 0.0, 0.0};
+                dd_add(comb[d].hi, comb[d].mid, comb[d].lo, comb[d].ab, res[d].hi, res[d].mid,
+                       res[d].lo, res[d].ab);
             }
-            stage_update(st, stage, v, hist, scal);
+            finish_stage(st, stage, ND, comb, reduce_depth(depth, nparts, 1), nprod, self_mask,
+                         k3_mask, hist, scal);
         }
     }
 }
 
-// nranks > 1: combine the gathered per-rank pairs in ascending rank order (R19).
+// nranks > 1: combine the gathered per-rank triples in ascending rank order (R19).
 template <int ND>
 __global__ void k_scalars(const dd* __restrict__ gathered, int nranks, int stage,
-                          DevState* st, double* hist, double* scal)
+                          DevState* st, double* hist, double* scal, int depth, int nparts,
+                          double nprod, int self_mask, int k3_mask)
 {
     if (stage != STAGE_SETUP && stage != STAGE_DOT && st->done) return;
-    double v[ND > 2 ? ND : 2] = {};
+    dd comb[ND];
     for (int d = 0; d < ND; ++d) {
-        double P = 0.0, S = 0.0;
-        for (int r = 0; r < nranks; ++r) dd_add(P, S, gathered[r * ND + d].hi,
-                                                gathered[r * ND + d].lo);
-        v[d] = P + S;
+        comb[d] = dd{0.0, 0.0, 0.0, 0.0};
+        for (int r = 0; r < nranks; ++r) {
+            const dd g = gathered[r * ND + d];
+            dd_add(comb[d].hi, comb[d].mid, comb[d].lo, comb[d].ab, g.hi, g.mid, g.lo, g.ab);
+        }
     }
-    stage_update(st, stage, v, hist, scal);
+    finish_stage(st, stage, ND, comb, reduce_depth(depth, nparts, nranks), nprod, self_mask,
+                 k3_mask, hist, scal);
 }
+

@@ -13,16 +13,18 @@
 
 namespace stream {
 
-constexpr int SBX = 32, SBY = 8, SZC = 8;   // threads (x pairs) x rows, planes per thread
+// threads (x pairs) x rows, planes per thread: 16 planes keep the partial count per launch
+// (one per CTA) at 16 K for 512^3 -- the finalize reads them all
+constexpr int SBX = 32, SBY = 8, SZC = 16;
 
 // w = A v (global operator; ghost planes hold halo data or zeros) and Dot2 partials of
 // a·w (ND >= 1) and w·w (ND == 2).  Each thread owns 2 adjacent x points of one row and
 // marches SZC planes; requires nx even (16-byte aligned rows).
 // ND == 5 (2-sync, R31): a = s, rt = r~: partials tᵀs, tᵀt, r~ᵀs, r~ᵀt, sᵀs.
 template <int ND, int SBX, int SBY, int SZC>
-// occupancy targets (registers): ND <= 1: 6 x 256 threads (<= 40), ND = 2: 4 (<= 64),
-// ND = 5: 3 (<= 80, no spills) -- the kernel is latency-bound (long scoreboard)
-__global__ void __launch_bounds__(SBX * SBY, (ND == 5 ? 768 : ND == 2 ? 1024 : 1536) / (SBX * SBY))
+// occupancy targets (registers): ND = 0: 6 x 256 threads (<= 40), ND = 1, 2: 4 (<= 64),
+// ND = 5: 2 (<= 128) -- no spills; the kernel is latency-bound (long scoreboard)
+__global__ void __launch_bounds__(SBX * SBY, (ND == 5 ? 512 : ND >= 1 ? 1024 : 1536) / (SBX * SBY))
 k_stencil2_dot(const double* __restrict__ v,
                                                             const double* __restrict__ a,
                                                             const double* __restrict__ rt,
@@ -36,11 +38,10 @@ k_stencil2_dot(const double* __restrict__ v,
     const int i = (blockIdx.x * SBX + threadIdx.x) * 2, j = blockIdx.y * SBY + threadIdx.y;
     const int k0 = kb + blockIdx.z * SZC, k1 = min(ke, k0 + SZC);
     constexpr int NDA = (ND > 0) ? ND : 1;
-    double p[NDA] = {}, s[NDA] = {};
-    // ND == 2: second accumulator pair per dot for the odd x point -- two independent Dot2
-    // chains (ILP, 0.70 -> 0.67 ms at 512^3); merged before the block reduction (Dot2 is
-    // order-insensitive, R19)
-    double p2[2] = {}, s2[2] = {};
+    double p[NDA] = {}, m[NDA] = {}, s[NDA] = {}, ab[NDA] = {};
+    // second accumulators per dot for the odd x point -- two independent chains (ILP);
+    // merged before the block reduction (the certified result is order-free, R19)
+    double p2[2] = {}, m2[2] = {}, s2[2] = {};
     if (i < nx && j < ny) {
         const int64_t plane = (int64_t)nx * ny;
         int64_t c = i + (int64_t)nx * j + plane * k0;
@@ -64,23 +65,25 @@ k_stencil2_dot(const double* __restrict__ v,
             o.x = stencil_row(zc.x, xm, zc.y, ym.x, yp.x, zmk.x, zpk.x, h2inv);
             o.y = stencil_row(zc.y, zc.x, xp, ym.y, yp.y, zmk.y, zpk.y, h2inv);
             *reinterpret_cast<double2*>(out + c) = o;
-            if (ND >= 1) {   // ND == 1: one chain measured faster (0.53 vs 0.58 ms at 512^3)
-                dot2_acc(p[0], s[0], av.x, o.x);
-                if (ND >= 2) dot2_acc(p2[0], s2[0], av.y, o.y);
-                else dot2_acc(p[0], s[0], av.y, o.y);
+            if (ND >= 2) {          // tᵀs: Dot2, two chains
+                dot2_acc(p[0], s[0], ab[0], av.x, o.x);
+                dot2_acc(p2[0], s2[0], ab[0], av.y, o.y);
+            } else if (ND == 1) {   // r~ᵀw: Dot3, two chains
+                dot3_acc(p[0], m[0], s[0], ab[0], av.x, o.x);
+                dot3_acc(p2[0], m2[0], s2[0], ab[0], av.y, o.y);
             }
             if (ND == 2 || ND == 5) {
-                dot2_acc(p[1], s[1], o.x, o.x);
-                dot2_acc(p2[1], s2[1], o.y, o.y);
+                dot2_acc_self(p[1], s[1], o.x);
+                dot2_acc_self(p2[1], s2[1], o.y);
             }
             if (ND == 5) {   // one chain per extra dot: registers for occupancy (latency)
                 const double2 rv = __ldg(reinterpret_cast<const double2*>(rt + c));
-                dot2_acc(p[2], s[2], rv.x, av.x);
-                dot2_acc(p[2], s[2], rv.y, av.y);
-                dot2_acc(p[3], s[3], rv.x, o.x);
-                dot2_acc(p[3], s[3], rv.y, o.y);
-                dot2_acc(p[4], s[4], av.x, av.x);
-                dot2_acc(p[4], s[4], av.y, av.y);
+                dot3_acc(p[2], m[2], s[2], ab[2], rv.x, av.x);   // r~ᵀs, r~ᵀt: Dot3
+                dot3_acc(p[2], m[2], s[2], ab[2], rv.y, av.y);
+                dot3_acc(p[3], m[3], s[3], ab[3], rv.x, o.x);
+                dot3_acc(p[3], m[3], s[3], ab[3], rv.y, o.y);
+                dot2_acc_self(p[4], s[4], av.x);
+                dot2_acc_self(p[4], s[4], av.y);
             }
             zm = zc;
             zc = zp;
@@ -88,9 +91,10 @@ k_stencil2_dot(const double* __restrict__ v,
     }
     if (ND > 0) {
 #pragma unroll
-        for (int d = 0; d < (ND >= 2 ? 2 : 0); ++d) dd_add(p[d], s[d], p2[d], s2[d]);
+        for (int d = 0; d < (ND >= 2 ? 2 : ND); ++d)   // ab: one shared sum per dot
+            dd_add(p[d], m[d], s[d], ab[d], p2[d], m2[d], s2[d], 0.0);
         const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-        block_reduce_dd<NDA>(p, s, part + (int64_t)bid * ND);
+        block_reduce_dd<NDA>(p, m, s, ab, part + (int64_t)bid * ND);
     }
 }
 
@@ -117,7 +121,7 @@ __global__ void __launch_bounds__(256) k_update_xr2(double2* __restrict__ x,
 {
     if (st->done) return;
     const double alpha = st->alpha, omega = st->omega;
-    double p[2] = {0.0, 0.0}, q[2] = {0.0, 0.0};
+    double p[2] = {0.0, 0.0}, m[2] = {0.0, 0.0}, q[2] = {0.0, 0.0}, ab[2] = {0.0, 0.0};
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     for (; c + (XR_UNR - 1) * stride < n2; c += XR_UNR * stride) {
@@ -143,10 +147,10 @@ __global__ void __launch_bounds__(256) k_update_xr2(double2* __restrict__ x,
             x[e] = xn;
             r[e] = rn;
             if (ND) {
-                dot2_acc(p[0], q[0], vrt[u].x, rn.x);
-                dot2_acc(p[0], q[0], vrt[u].y, rn.y);
-                dot2_acc(p[1], q[1], rn.x, rn.x);
-                dot2_acc(p[1], q[1], rn.y, rn.y);
+                dot3_acc(p[0], m[0], q[0], ab[0], vrt[u].x, rn.x);
+                dot3_acc(p[0], m[0], q[0], ab[0], vrt[u].y, rn.y);
+                dot2_acc_self(p[1], q[1], rn.x);
+                dot2_acc_self(p[1], q[1], rn.y);
             }
         }
     }
@@ -161,13 +165,13 @@ __global__ void __launch_bounds__(256) k_update_xr2(double2* __restrict__ x,
         x[c] = xn;
         r[c] = rn;
         if (ND) {
-            dot2_acc(p[0], q[0], vrt.x, rn.x);
-            dot2_acc(p[0], q[0], vrt.y, rn.y);
-            dot2_acc(p[1], q[1], rn.x, rn.x);
-            dot2_acc(p[1], q[1], rn.y, rn.y);
+            dot3_acc(p[0], m[0], q[0], ab[0], vrt.x, rn.x);
+            dot3_acc(p[0], m[0], q[0], ab[0], vrt.y, rn.y);
+            dot2_acc_self(p[1], q[1], rn.x);
+            dot2_acc_self(p[1], q[1], rn.y);
         }
     }
-    if (ND) block_reduce_dd<2>(p, q, part + (int64_t)blockIdx.x * 2);
+    if (ND) block_reduce_dd<2>(p, m, q, ab, part + (int64_t)blockIdx.x * 2);
 }
 
 // M = I (plain Bi-CGSTAB, P:145-174 / Alg. 3 with p̂ = p, r̂ = s): a6 s = fma(-α, w, r) into

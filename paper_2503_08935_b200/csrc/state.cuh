@@ -6,8 +6,13 @@
 #include <stdint.h>
 
 #include "dd.cuh"
+#include "xdot.cuh"
 
-enum : int32_t { DONE_RUNNING = 0, DONE_OK = 1, DONE_BREAKDOWN = 2, DONE_MAXIT = 3 };
+// DONE_PENDING: a reduction could not be certified (R19); every later kernel of the solve
+// is a no-op until the host has recomputed the flagged dots exactly and resumed (resolve).
+// DONE_COMM_ERROR: a peer-transport wait timed out (p2p.cuh); the host returns BCGS_E_COMM.
+enum : int32_t { DONE_RUNNING = 0, DONE_OK = 1, DONE_BREAKDOWN = 2, DONE_MAXIT = 3,
+                 DONE_PENDING = 4, DONE_COMM_ERROR = 5 };
 
 struct DevState {
     double rho, alpha, omega, beta, nb;
@@ -19,6 +24,18 @@ struct DevState {
     int32_t max_iter;
     double scratch[8];    // results of stand-alone dot calls
     int32_t pend;         // 2-sync (R31): stop decided at the ω stage, applied after a11/a12
+    // R19 certification fallback
+    int32_t pend_stage;   // stage whose reduction is parked (valid while pend_mask != 0)
+    int32_t pend_mask;    // bit d: dot d of that stage needs the exact recomputation
+    double pend_v[5];     // the stage's values (certified ones final, the others replaced)
+    int32_t exact_mode;   // BCGS_OPT_EXACT_DOT = 1: every dot through the exact path
+    int32_t n_exact;      // dots recomputed exactly since bcgs_begin
+    // peer transport (p2p.cuh): exchange sequence numbers, monotone over the context's life
+    unsigned long long halo_sent, halo_recv, red_seq;
+    int32_t comm_err;
+    // the last refused certification: stage, dot, D, r, e, E, |r| gap up, gap down, Hc
+    double cert_last[9];
+    int32_t n_refused;    // certifications refused since bcgs_create
 };
 
 // Reduction stages (one per MPI_Allreduce site of Alg. 3).
@@ -158,3 +175,43 @@ __device__ __forceinline__ void stage_update(DevState* st, int stage, const doub
     }
     }
 }
+
+// Completion of a reduction stage from the combined Dot2 triples (one thread): certified
+// values go straight to the stage's scalar update; otherwise the stage is parked
+// (DONE_PENDING, or pend_mask alone for the stand-alone STAGE_DOT) for the exact path.
+// D = depth bound of the summation chains, nprod = number of products per dot (R19).
+// self_mask bit d: dot d is a·a (no Σ|h| accumulated): its terms are >= 0, so
+// Σ|a_i a_i| = Σ a_i a_i <= |hi + mid + lo| + E, and the bound holds with 1.001 |...|.
+// k3_mask bit d: dot d was accumulated with Dot3 chains (dd.cuh).
+__device__ __forceinline__ void finish_stage(DevState* st, int stage, int nd, const dd* comb,
+                                             int D, double nprod, int self_mask, int k3_mask,
+                                             double* hist, double* scal)
+{
+    double v[5] = {0, 0, 0, 0, 0};
+    int mask = 0;
+    for (int d = 0; d < nd; ++d) {
+        const dd& c = comb[d];
+        const double ab = (self_mask >> d) & 1 ? fabs((c.hi + c.mid) + c.lo) * 1.001 : c.ab;
+        double r, o, E;
+        const bool ok = dd_certify(c, ab, D, nprod, (k3_mask >> d) & 1, &v[d], &r, &o, &E);
+        if (!ok) {
+            const double ar = fabs(r);
+            const long long bits = __double_as_longlong(ar);
+            const double cl[9] = {(double)stage, (double)d, (double)D, r, o, E,
+                                  __longlong_as_double(bits + 1) - ar,
+                                  bits > 0 ? ar - __longlong_as_double(bits - 1) : 0.0, ab};
+            for (int i = 0; i < 9; ++i) st->cert_last[i] = cl[i];
+            st->n_refused += 1;
+        }
+        if (!ok || st->exact_mode) mask |= 1 << d;
+    }
+    if (mask) {
+        st->pend_stage = stage;
+        st->pend_mask = mask;
+        for (int d = 0; d < 5; ++d) st->pend_v[d] = v[d];
+        if (stage != STAGE_DOT) st->done = DONE_PENDING;
+        return;
+    }
+    stage_update(st, stage, v, hist, scal);
+}
+

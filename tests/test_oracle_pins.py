@@ -169,17 +169,56 @@ def _exact_dot(a, b):
                      Fraction(0)))
 
 
-@pytest.mark.parametrize("case", range(6))
-def test_dot2_is_correctly_rounded(orc, case):
-    """R19: Dot2 returns the correctly rounded dot on these inputs (exact rational check)."""
+@pytest.mark.parametrize("case", range(8))
+def test_dot_is_correctly_rounded(orc, case):
+    """R19: the dot product is RN(Σ a_i b_i) -- checked against exact rational arithmetic
+    (Python's Fraction; float(Fraction) rounds to nearest, ties to even), including heavy
+    cancellation and a 10^±150 dynamic range where a compensated (Dot2) sum is not exact."""
     r = rng(10 + case)
-    n = [1, 7, 100, 1000, 4096, 999][case]
+    n = [1, 7, 100, 1000, 4096, 999, 300, 2000][case]
     a = r.standard_normal(n) * 10.0 ** r.integers(-8, 8, n)
     b = r.standard_normal(n)
     if case >= 3:          # heavy cancellation
         a = np.concatenate([a, -a[: n // 2]])
         b = np.concatenate([b, b[: n // 2] * (1 + 1e-13)])
+    if case >= 6:          # huge dynamic range + exact cancellation of the large terms
+        big = r.standard_normal(n) * 10.0 ** r.integers(100, 150, n)
+        a = np.concatenate([big, a, -big])
+        b = np.concatenate([np.ones(n), b, np.ones(n)])
     assert orc.dot(a, b) == _exact_dot(a, b)
+
+
+def test_dot_is_order_independent(orc):
+    r = rng(21)
+    a = r.standard_normal(5000) * 10.0 ** r.integers(-20, 20, 5000)
+    b = r.standard_normal(5000)
+    p = r.permutation(5000)
+    assert orc.dot(a, b) == orc.dot(a[p], b[p]) == _exact_dot(a, b)
+
+
+def test_dot_ties_round_to_even(orc):
+    # 1 + 2^-53 is the midpoint of 1 and 1 + 2^-52: ties-to-even gives 1
+    assert orc.dot(np.array([1.0, 2.0 ** -53]), np.ones(2)) == 1.0
+    # (1 + 2^-52) + 2^-53 is the midpoint of 1 + 2^-52 and 1 + 2^-51: even is 1 + 2^-51
+    assert orc.dot(np.array([1.0 + 2.0 ** -52, 2.0 ** -53]), np.ones(2)) == 1.0 + 2.0 ** -51
+    # just above the midpoint rounds up
+    assert orc.dot(np.array([1.0, 2.0 ** -53, 2.0 ** -200]), np.ones(3)) == 1.0 + 2.0 ** -52
+
+
+def test_dot_subnormal_overflow_and_nonfinite(orc):
+    # each product 2^-1080 underflows to 0 in floating point; their exact sum is 2^-1074
+    a = np.full(64, 2.0 ** -540)
+    assert _exact_dot(a, a) == 2.0 ** -1074
+    assert orc.dot(a, a) == 2.0 ** -1074
+    # 3 * 2^-1076 = 0.75 * 2^-1074 rounds to the nearest subnormal 2^-1074
+    a = np.full(3, 2.0 ** -538)
+    assert orc.dot(a, a) == _exact_dot(a, a) == 2.0 ** -1074
+    a = np.array([2.0 ** -537, 2.0 ** -537, 3.0 * 2.0 ** -540])
+    assert orc.dot(a, np.ones(3) * 2.0 ** -537) == _exact_dot(a, np.ones(3) * 2.0 ** -537)
+    assert orc.dot(np.array([1e300, 1e300]), np.array([1e300, 1e300])) == np.inf
+    assert np.isnan(orc.dot(np.array([1.0, np.inf]), np.array([1.0, 1.0])))
+    assert np.isnan(orc.dot(np.array([1.0, 2.0]), np.array([np.nan, 1.0])))
+    assert orc.dot(np.zeros(10), np.ones(10)) == 0.0
 
 
 def test_dot2_cancellation_example(orc):
