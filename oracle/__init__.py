@@ -253,11 +253,14 @@ def bicgstab(b: np.ndarray, h: float, *, pc: str = "none", k: int = 4, nslab: in
              c_min: float = 10.0, c_max: float = 1.0 - 1e-4, bounds_override=None,
              x0: np.ndarray | None = None, tol: float = 1e-8, max_it: int = 5000,
              fixed_it: int = 0, bc=None, inner_tol: float | None = None,
-             inner_max: int | None = None, sync2: bool = False) -> Result:
+             inner_max: int | None = None, sync2: bool = False,
+             pipelined: bool = False) -> Result:
     """Alg. 3 (P:264-308) with M = I, GNoComm(CI), BJ(CI), G(CI) on `nslab` z-slabs, or the
     inner-Krylov BJ(BiCGS) / G(BiCGS) (inner_tol / inner_max default to P:393-394's values;
     Result.extra["inner_iterations"] = total inner iterations).  sync2: the 2-sync rewrite
-    (R31): ρ_new and ||r||² from the a9 reduction, no MPI5."""
+    (R31): ρ_new and ||r||² from the a9 reduction, no MPI5.  pipelined: the pipelined
+    (communication-hiding) Bi-CGSTAB of bcgs_oracle.c's pbicgstab, two reductions per
+    iteration (linear preconditioners only)."""
     dt, dm = INNER_DEFAULT.get(pc, (0.0, 0))
     inner_tol = dt if inner_tol is None else inner_tol
     inner_max = dm if inner_max is None else inner_max
@@ -276,7 +279,8 @@ def bicgstab(b: np.ndarray, h: float, *, pc: str = "none", k: int = 4, nslab: in
         x0 = np.ascontiguousarray(x0, np.float64)
         x0p = _ptr(x0)
     st = lib().orc_bicgstab_ex(nx, ny, nz, h, nslab, bc_mask(bc), PC[pc], k, c_min, c_max,
-                               lmin, lmax, inner_tol, inner_max, 1 if sync2 else 0,
+                               lmin, lmax, inner_tol, inner_max,
+                               (1 if sync2 else 0) | (2 if pipelined else 0),
                                _ptr(b), x0p, tol, max_it, fixed_it, _ptr(x), _ptr(hist),
                                _ptr(scal), ctypes.byref(it), ctypes.byref(tr),
                                ctypes.byref(tot))

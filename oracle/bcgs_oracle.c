@@ -583,6 +583,148 @@ static void apply_inner_bicgs(int64_t nx, int64_t ny, int64_t nz, double h, int6
  * *iters_out = number of completed iterations (each appended one entry to hist); a
  * breakdown at r~ᵀw ends the run before iteration i appends anything (iters = i-1).
  * ---------------------------------------------------------------------------------------- */
+/* ------------------------------------------------------------------------------------------
+ * Pipelined Bi-CGSTAB (flags bit 1, the paper's "communication-
+ * avoiding/reducing algorithms" future work): the communication-hiding p-BiCGStab of
+ * Cools & Vanroose (2017) for the right-preconditioned operator B = A M^-1, written out from
+ * Alg. 3 by the recurrences below; in exact arithmetic it produces the iterates
+ * of Alg. 3.  With S = B p, z = B S, w = B r, t = B w, v = B z, q = r - α S (Alg. 3's s),
+ * y = B q (Alg. 3's t), and hats = M^-1 (p̂ = M^-1 p, ...):
+ *   p = r + β(p - ω S)        p̂ = r̂ + β(p̂ - ω Ŝ)
+ *   S = w + β(S - ω z)        Ŝ = ŵ + β(Ŝ - ω ẑ)
+ *   z = t + β(z - ω v)        ẑ = M^-1 z        v = A ẑ          (2nd stencil overlaps R1)
+ *   q = r - α S      q̂ = r̂ - α Ŝ      y = w - α z
+ *   R1: (q, y), (y, y) -> ω = (q, y)/(y, y)
+ *   x += α p̂ + ω q̂     r = q - ω y     r̂ = q̂ - ω(ŵ - α ẑ)     w = y - ω(t - α v)
+ *   ŵ = M^-1 w        t = A ŵ                                  (1st stencil overlaps R2)
+ *   R2: (r~, r), (r~, w), (r~, S), (r~, z), (r, r)
+ *   β = (ρ_new/ρ)(α/ω);   α = ρ_new / (β((r~, S) - ω (r~, z)) + (r~, w))
+ * Two reductions per iteration (three in Alg. 3), each independent of the stencil +
+ * preconditioner application that follows it.  Start: w = A r̂0, ŵ = M^-1 w, t = A ŵ,
+ * α0 = ρ0/(r~, w0), β = ω = 0 (so p0 = r0, S0 = w0, z0 = t0).  Linear preconditioners only
+ * (the recurrences for the hatted vectors need M^-1 fixed).  Expression trees (contract
+ * R20 style): every update is the nested fma written above, a + β(b - ω c) =
+ * fma(β, fma(-ω, c, b), a).  Scalars per iteration: (r~,w)-combination, α, (q,y), (y,y), ω,
+ * ρ_new, (r,r), β.  Stopping and breakdown as R4 / R6 / R7.
+ * ---------------------------------------------------------------------------------------- */
+static int pbicgstab(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab_pc, int bcm,
+                     int pc, int k, double a_iv, double b_iv, const double* b, const double* x0,
+                     double tol, int max_run, int fixed_it, double* x, double* hist,
+                     double* scal, int* iters_out, double* true_rel)
+{
+    int64_t n = nx * ny * nz, pl = nx * ny;
+    double* V[18];
+    for (int i = 0; i < 18; ++i) V[i] = (double*)calloc((size_t)n, sizeof(double));
+    double *r = V[0], *rh = V[1], *w = V[2], *wh = V[3], *t = V[4], *p = V[5], *ph = V[6],
+           *S = V[7], *Sh = V[8], *z = V[9], *zh = V[10], *q = V[11], *qh = V[12], *y = V[13],
+           *v = V[14], *rt = V[15], *tmp = V[16];
+#define APPLY_M(in, out)                                                                    \
+    do {                                                                                    \
+        if (pc == 0) memcpy((out), (in), sizeof(double) * (size_t)n);                       \
+        else orc_apply_cheb_bc(nx, ny, nz, h, nslab_pc, bcm, k, a_iv, b_iv, (in), (out));   \
+    } while (0)
+    if (x0) {
+        memcpy(x, x0, sizeof(double) * (size_t)n);
+        orc_apply_A_bc(nx, ny, nz, h, 1, bcm, x, tmp);
+        for (int64_t c = 0; c < n; ++c) r[c] = b[c] - tmp[c];
+    } else {
+        memset(x, 0, sizeof(double) * (size_t)n);
+        memcpy(r, b, sizeof(double) * (size_t)n);
+    }
+    memcpy(rt, r, sizeof(double) * (size_t)n);
+    double rho = orc_dot(pl, nz, rt, r);
+    double nb = sqrt(orc_dot(pl, nz, b, b));
+    int status = 6, it = 0;
+    if (nb == 0.0) {
+        hist[0] = 0.0;
+        status = 0;
+        goto done;
+    }
+    hist[0] = sqrt(rho) / nb;
+    if (fixed_it <= 0 && hist[0] < tol) {
+        status = 0;
+        goto done;
+    }
+    /* start: r̂ = M^-1 r, w = A r̂, ŵ = M^-1 w, t = A ŵ, α0 = ρ0 / (r~, w0) */
+    APPLY_M(r, rh);
+    orc_apply_A_bc(nx, ny, nz, h, 1, bcm, rh, w);
+    APPLY_M(w, wh);
+    orc_apply_A_bc(nx, ny, nz, h, 1, bcm, wh, t);
+    double den = orc_dot(pl, nz, rt, w);
+    if (den == 0.0 || !isfinite(den)) { status = 7; goto done; }
+    double alpha = rho / den, beta = 0.0, omega = 0.0;
+    for (int i = 1; i <= max_run; ++i) {
+        it = i;
+        double* sc = scal ? scal + 8 * (i - 1) : NULL;
+        if (sc) { sc[0] = den; sc[1] = alpha; }
+#pragma omp parallel for schedule(static)
+        for (int64_t c = 0; c < n; ++c) {
+            p[c] = fma(beta, fma(-omega, S[c], p[c]), r[c]);
+            ph[c] = fma(beta, fma(-omega, Sh[c], ph[c]), rh[c]);
+            S[c] = fma(beta, fma(-omega, z[c], S[c]), w[c]);
+            Sh[c] = fma(beta, fma(-omega, zh[c], Sh[c]), wh[c]);
+            z[c] = fma(beta, fma(-omega, v[c], z[c]), t[c]);
+        }
+        APPLY_M(z, zh);
+        orc_apply_A_bc(nx, ny, nz, h, 1, bcm, zh, v);
+#pragma omp parallel for schedule(static)
+        for (int64_t c = 0; c < n; ++c) {
+            q[c] = fma(-alpha, S[c], r[c]);
+            qh[c] = fma(-alpha, Sh[c], rh[c]);
+            y[c] = fma(-alpha, z[c], w[c]);
+        }
+        double qy = orc_dot(pl, nz, q, y);                        /* R1 */
+        double yy = orc_dot(pl, nz, y, y);
+        omega = (yy == 0.0) ? 0.0 : qy / yy;                       /* R6 */
+        if (sc) { sc[2] = qy; sc[3] = yy; sc[4] = omega; }
+#pragma omp parallel for schedule(static)
+        for (int64_t c = 0; c < n; ++c) {
+            x[c] = fma(omega, qh[c], fma(alpha, ph[c], x[c]));
+            r[c] = fma(-omega, y[c], q[c]);
+            rh[c] = fma(-omega, fma(-alpha, zh[c], wh[c]), qh[c]);
+            w[c] = fma(-omega, fma(-alpha, v[c], t[c]), y[c]);
+        }
+        APPLY_M(w, wh);
+        orc_apply_A_bc(nx, ny, nz, h, 1, bcm, wh, t);
+        double rho_new = orc_dot(pl, nz, rt, r);                  /* R2 */
+        double rw = orc_dot(pl, nz, rt, w);
+        double rS = orc_dot(pl, nz, rt, S);
+        double rz = orc_dot(pl, nz, rt, z);
+        double rr = orc_dot(pl, nz, r, r);
+        double rel = sqrt(rr) / nb;
+        hist[i] = rel;
+        if (sc) { sc[5] = rho_new; sc[6] = rr; sc[7] = 0.0; }
+        if (fixed_it > 0) {
+            if (i == fixed_it) { status = 0; break; }
+        } else if (rel < tol) {
+            status = 0;
+            break;
+        }
+        if (omega == 0.0 || rho_new == 0.0 || !isfinite(rho_new) || !isfinite(rr) ||
+            !isfinite(omega)) {
+            status = 7;
+            break;
+        }
+        beta = (rho_new / rho) * (alpha / omega);                  /* R20 form */
+        rho = rho_new;
+        if (sc) sc[7] = beta;
+        den = fma(beta, fma(-omega, rz, rS), rw);
+        if (den == 0.0 || !isfinite(den)) { status = 7; break; }
+        alpha = rho_new / den;
+        if (fixed_it <= 0 && i == max_run) status = 6;
+    }
+#undef APPLY_M
+done:
+    if (iters_out) *iters_out = it;
+    if (true_rel) {
+        orc_apply_A_bc(nx, ny, nz, h, 1, bcm, x, tmp);
+        for (int64_t c = 0; c < n; ++c) tmp[c] = b[c] - tmp[c];
+        *true_rel = nb == 0.0 ? 0.0 : sqrt(orc_dot(pl, nz, tmp, tmp)) / nb;
+    }
+    for (int i = 0; i < 18; ++i) free(V[i]);
+    return status;
+}
+
 int orc_bicgstab_ex(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab, int bcm,
                     int pc, int k, double c_min, double c_max, double lmin_ov, double lmax_ov,
                     double tol_in, int max_in, int flags, const double* b, const double* x0,
@@ -616,6 +758,11 @@ int orc_bicgstab_ex(int64_t nx, int64_t ny, int64_t nz, double h, int64_t nslab,
     /* pc 5 = G(BiCGS): one inner solve over the whole domain (no block cuts) */
     const int64_t nslab_in = (pc == 5) ? 1 : nslab;
     int max_run = fixed_it > 0 ? fixed_it : max_it;
+    if (flags & 2) {   /* pipelined Bi-CGSTAB: linear preconditioners only */
+        if (pc >= 4 || (flags & 1)) return 1;
+        return pbicgstab(nx, ny, nz, h, nslab_pc, bcm, pc, k, a_iv, b_iv, b, x0, tol, max_run,
+                         fixed_it, x, hist, scal, iters_out, true_rel);
+    }
 
     double* r = (double*)calloc((size_t)n, sizeof(double));
     double* rt = (double*)calloc((size_t)n, sizeof(double));
