@@ -117,10 +117,16 @@ typedef enum {
                                /* path (R19 fallback) instead of certified   */
                                /* Dot2; the results are the same (correctly rounded) --   */
                                /* for testing the fallback.  0 = certified Dot2 (default) */
-    BCGS_OPT_COMM_TIMEOUT = 12 /* seconds a transport wait may take: NCCL host waits abort  */
+    BCGS_OPT_COMM_TIMEOUT = 12,/* seconds a transport wait may take: NCCL host waits abort  */
                                /* the communicator after it (default 300; async errors    */
                                /* abort at once); p2p device waits give up (default 60).  */
                                /* Both end the solve with an error status, never a hang.  */
+    BCGS_OPT_PIPELINED = 13    /* 1 = pipelined (communication-hiding) Bi-CGSTAB for      */
+                               /* B = A M^-1 (NEXT-4; R32): 2 reductions  */
+                               /* per iteration, each independent of the preconditioner + */
+                               /* stencil that follows it; linear preconditioners only;   */
+                               /* six more fields (library-owned).  Same iterates as Alg. 3 */
+                               /* in exact arithmetic; the oracle implements the same flag */
 } bcgs_option;
 
 /* Boundary condition kind of a physical face (Eq. 4 / Eq. 5). */

@@ -8,6 +8,7 @@
 #include "ctx.cuh"
 #include "k_ref.cuh"
 #include "k_stream.cuh"
+#include "pipe.cuh"
 
 namespace {
 
@@ -300,6 +301,16 @@ bcgs_status p2p_halo(bcgs_ctx c, const double* v, double* gl, double* gh, int k,
     return BCGS_OK;
 }
 
+// The peer context's copy of my field pointer v (same layout on every rank): the workspace,
+// or the library-owned pipelined fields
+const double* peer_field(bcgs_ctx c, bcgs_ctx p, const void* v)
+{
+    const char* cv = (const char*)v;
+    if (c->pipe_mem && cv >= c->pipe_mem && cv < c->pipe_mem + c->pipe_bytes && p->pipe_mem)
+        return (const double*)(p->pipe_mem + (cv - c->pipe_mem));
+    return (const double*)(p->ws + (cv - c->ws));
+}
+
 bcgs_status halo_on(bcgs_ctx c, double* v, cudaStream_t hs, int guarded = 1)
 {
     if (c->nranks == 1 || (c->ablate & 1)) return BCGS_OK;   // ablation: timing only
@@ -307,13 +318,12 @@ bcgs_status halo_on(bcgs_ctx c, double* v, cudaStream_t hs, int guarded = 1)
     const size_t pl = (size_t)c->lay.plane;
     if (c->p2p) return p2p_halo(c, v, v - pl, v + c->lay.L * pl, 1, hs, guarded);
     if (c->lg) {
-        const ptrdiff_t off = (char*)v - c->ws;   // same layout on every rank
         TRY(local_exchange_begin(c, hs));
         for (int d = -1; d <= 1; d += 2) {
             const int nb = c->rank + d;
             if (nb < 0 || nb >= c->nranks) continue;
             bcgs_ctx p = c->lg->ctxs[nb];
-            const double* pv = (const double*)(p->ws + off);
+            const double* pv = peer_field(c, p, v);
             CUDA_OK(c, cudaStreamWaitEvent(hs, p->ev_ready, 0));
             // from rank-1: its plane L-1 -> my ghost -1; from rank+1: its plane 0 -> ghost L
             const double* src = d < 0 ? pv + (c->lay.L - 1) * pl : pv;
@@ -471,13 +481,12 @@ bcgs_status halo_deep(bcgs_ctx c, const double* q, double* E, int k)
     Prof pf(c, KC_HALO, 0.0);
     if (c->p2p) return p2p_halo(c, q, E + (KG - k) * pl, E + (KG + L) * pl, k, c->s, 1);
     if (c->lg) {
-        const ptrdiff_t off = (const char*)q - c->ws;
         TRY(local_exchange_begin(c, c->s));
         for (int d = -1; d <= 1; d += 2) {
             const int nb = c->rank + d;
             if (nb < 0 || nb >= c->nranks) continue;
             bcgs_ctx p = c->lg->ctxs[nb];
-            const double* pq = (const double*)(p->ws + off);
+            const double* pq = peer_field(c, p, q);
             CUDA_OK(c, cudaStreamWaitEvent(c->s, p->ev_ready, 0));
             const double* src = d < 0 ? pq + (L - k) * pl : pq;
             double* dst = d < 0 ? E + (KG - k) * pl : E + (KG + L) * pl;
@@ -660,8 +669,91 @@ a14:  // a14: p = r + β (p - ω w)
     return BCGS_OK;
 }
 
+// ------------------------------------------------------------------ pipelined Bi-CGSTAB
+// BCGS_OPT_PIPELINED (pipe.cuh; NEXT-4): library-owned fields z, ẑ, q, q̂, y, v; the
+// rest reuse the workspace: p = V_P, p̂ = V_PH, S = V_S, Ŝ = V_P2, r̂ = V_RH, w = V_W,
+// ŵ = V_W2, t = V_T.
+enum { PZ = 0, PZH = 1, PQ = 2, PQH = 3, PY = 4, PV = 5 };
+
+bcgs_status pipe_alloc(bcgs_ctx c)
+{
+    if (c->pipe_mem) return BCGS_OK;
+    const size_t one = align_up(sizeof(double) * (size_t)c->lay.vec_elems);
+    c->pipe_bytes = 6 * one;
+    CUDA_OK(c, cudaMalloc(&c->pipe_mem, 6 * one));
+    CUDA_OK(c, cudaMemset(c->pipe_mem, 0, 6 * one));   // ghost planes: zero (Dirichlet)
+    for (int i = 0; i < 6; ++i) c->pipe[i] = (double*)(c->pipe_mem + i * one) + c->lay.plane;
+    return BCGS_OK;
+}
+
+bcgs_status pipe_precond(bcgs_ctx c, const double* in, double* out)
+{
+    if (c->kernels == 1 && fused::precond_supported(c) &&
+        !(c->pc == BCGS_PC_CHEB_G && c->nranks > 1))
+        return fused::precond_apply(c, in, out, c->st);
+    return precond_ref(c, in, out, c->st);
+}
+
+bcgs_status pipe_stencil(bcgs_ctx c, double* in, double* out)
+{
+    TRY(halo(c, in));
+    Prof pf(c, KC_STENCIL1, 16.0 * npts(c));
+    ref::k_stencil_dot<0><<<stencil_grid(c), dim3(ref::BX, ref::BY), 0, c->s>>>(
+        in, nullptr, out, ref_grid(c, (int)c->lay.L), 0, nullptr, c->st);
+    CUDA_OK(c, cudaGetLastError());
+    return BCGS_OK;
+}
+
+// after the setup stage: r̂ = M^-1 r, w = A r̂, ŵ = M^-1 w, t = A ŵ, α0 = ρ0 / r~ᵀw
+bcgs_status pipe_start(bcgs_ctx c)
+{
+    TRY(pipe_precond(c, F(c, V_R), F(c, V_RH)));
+    TRY(pipe_stencil(c, F(c, V_RH), F(c, V_W)));
+    TRY(pipe_precond(c, F(c, V_W), F(c, V_W2)));
+    TRY(pipe_stencil(c, F(c, V_W2), F(c, V_T)));
+    const int64_t n = npts(c);
+    ref::k_dot2<1><<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(F(c, V_RT), F(c, V_W), nullptr,
+                                                           nullptr, n, c->part);
+    CUDA_OK(c, cudaGetLastError());
+    return reduce<1>(c, kEwBlocks, STAGE_PIPE_INIT, ew_depth(n), 1, {F(c, V_RT), F(c, V_W)});
+}
+
+bcgs_status iteration_pipe(bcgs_ctx c, int from)
+{
+    const int64_t n = npts(c);
+    DevState* st = c->st;
+    double** P = c->pipe;
+    if (from == STAGE_PIPE_RHO) return BCGS_OK;
+    if (from == STAGE_PIPE_OMEGA) goto after_r1;
+    {
+        Prof pf(c, KC_UPDATE_P, 160.0 * n);
+        pbcg::k_pipe_a<<<kEwBlocks, 256, 0, c->s>>>(
+            F(c, V_P), F(c, V_PH), F(c, V_S), F(c, V_P2), P[PZ], P[PZH], P[PV], F(c, V_R),
+            F(c, V_RH), F(c, V_W), F(c, V_W2), F(c, V_T), P[PQ], P[PQH], P[PY], n, c->part, st);
+    }
+    CUDA_OK(c, cudaGetLastError());
+    TRY(reduce<2>(c, kEwBlocks, STAGE_PIPE_OMEGA, ew_depth(n), 0,
+                  {P[PQ], P[PY], P[PY], P[PY]}));   // R1
+after_r1:
+    TRY(pipe_precond(c, P[PZ], P[PZH]));
+    TRY(pipe_stencil(c, P[PZH], P[PV]));
+    {
+        Prof pf(c, KC_UPDATE_XR, 128.0 * n);
+        pbcg::k_pipe_b<<<kEwBlocks, 256, 0, c->s>>>(
+            F(c, V_X), F(c, V_R), F(c, V_RH), F(c, V_W), F(c, V_PH), P[PQH], P[PQ], P[PY],
+            P[PZH], F(c, V_W2), F(c, V_T), P[PV], F(c, V_RT), F(c, V_S), P[PZ], n, c->part, st);
+    }
+    CUDA_OK(c, cudaGetLastError());
+    TRY(pipe_precond(c, F(c, V_W), F(c, V_W2)));
+    TRY(pipe_stencil(c, F(c, V_W2), F(c, V_T)));
+    return reduce<5>(c, kEwBlocks, STAGE_PIPE_RHO, ew_depth(n), 15,
+                     {F(c, V_RT), F(c, V_R), F(c, V_RT), F(c, V_W), F(c, V_RT), F(c, V_S),
+                      F(c, V_RT), P[PZ], F(c, V_R), F(c, V_R)});   // R2
+}
+
 bcgs_status iteration(bcgs_ctx c, int from)
 {
+    if (c->pipelined) return iteration_pipe(c, from);
     if (c->pc == BCGS_PC_CHEB_G && c->nranks > 1) return iteration_ref(c, from);   // k-deep halos
     if (c->kernels == 1 && fused::supported(c, c->degree, c->pc != BCGS_PC_NONE))
         return fused::iteration(c, from);
@@ -833,11 +925,14 @@ bcgs_status bcgs_nccl_unique_id(void* out128)
 static bcgs_status create_ctx(const bcgs_grid_desc* grid, int32_t rank, int32_t nranks,
                               const void* nccl_unique_id, LocalGroup* lg, int32_t cuda_device,
                               void* d_workspace, size_t ws_bytes, void* cuda_stream,
-                              bcgs_ctx* out, int p2p = 0)
+                              bcgs_ctx* out, int p2p = 0, bcgs_ctx share = nullptr)
 {
+    // share: a context over the same ranks that uses `share`'s transport (the NCCL
+    // communicator, or the p2p mailboxes with their sequence numbers) -- the global inner
+    // solver of G(BiCGS) on nranks > 1
     if (!grid || !out || nranks < 1 || rank < 0 || rank >= nranks) return BCGS_E_INVALID;
     if (!(grid->h > 0.0)) return BCGS_E_INVALID;
-    if (nranks > 1 && !nccl_unique_id && !lg && !p2p) return BCGS_E_INVALID;
+    if (nranks > 1 && !nccl_unique_id && !lg && !p2p && !share) return BCGS_E_INVALID;
     if (p2p && (nranks < 2 || nranks > p2p::MAXR)) return BCGS_E_INVALID;
     if (!bc_ok(grid)) return BCGS_E_CONFIG;
     Layout lay;
@@ -888,7 +983,13 @@ static bcgs_status create_ctx(const bcgs_grid_desc* grid, int32_t rank, int32_t 
     c->gath = (dd*)(c->ws + lay.off_gath);
     c->limbs = (long long*)(c->ws + lay.off_limb);
     c->glimbs = (long long*)(c->ws + lay.off_glimb);
-    if (p2p) {   // mailbox + landing zones (face halos; G(CI) k-deep halos up to `cap` planes)
+    if (share) {
+        c->comm = share->comm;
+        c->comm_borrowed = 1;
+        c->p2p = share->p2p;
+        c->p2p_ready = share->p2p_ready;
+        c->peers = share->peers;
+    } else if (p2p) {   // mailbox + landing zones (face halos; G(CI) k-deep halos <= `cap`)
         c->p2p = 1;
         c->peers.rank = rank;
         c->peers.nranks = nranks;
@@ -904,7 +1005,7 @@ static bcgs_status create_ctx(const bcgs_grid_desc* grid, int32_t rank, int32_t 
     }
     TRY(enter(c));
     CUDA_OK(c, cudaMemsetAsync(c->ws, 0, lay.total, c->s));   // zero ghost planes + state
-    if (nranks > 1 && !lg) {
+    if (nranks > 1 && !lg && !p2p && !share) {
         ncclUniqueId id;
         memcpy(&id, nccl_unique_id, sizeof id);
         NCCL_OK(c, ncclCommInitRank(&c->comm, nranks, id, rank));
@@ -1025,9 +1126,10 @@ void bcgs_destroy(bcgs_ctx c)
     harvest(c);
     drop_graph(c);
     for (auto e : c->free_ev) cudaEventDestroy(e);
-    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->comm && !c->comm_borrowed) ncclCommDestroy(c->comm);
     for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
     if (c->mailbox) cudaFree(c->mailbox);
+    if (c->pipe_mem) cudaFree(c->pipe_mem);
     if (c->ev_ready) cudaEventDestroy(c->ev_ready);
     if (c->ev_pre) cudaEventDestroy(c->ev_pre);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
@@ -1067,6 +1169,7 @@ bcgs_status bcgs_set_option(bcgs_ctx c, int32_t option, int64_t value)
     case BCGS_OPT_ABLATE: c->ablate = (int)(value & 3); break;
     case BCGS_OPT_SYNC2: c->sync2_opt = (int)value; drop_graph(c); break;
     case BCGS_OPT_EXACT_DOT: c->exact_opt = value ? 1 : 0; break;
+    case BCGS_OPT_PIPELINED: c->pipelined_opt = value ? 1 : 0; break;
     case BCGS_OPT_COMM_TIMEOUT:   // NCCL host waits; p2p device waits (default 60 s)
         c->comm_timeout_s = value > 0 ? (double)value : 300.0;
         c->peers.timeout_ns = (value > 0 ? (unsigned long long)value : 60ull) * 1000000000ull;
@@ -1129,8 +1232,9 @@ bcgs_status bcgs_set_preconditioner(bcgs_ctx c, bcgs_pc pc, int32_t degree, doub
         return fail(c, BCGS_E_INVALID, "unknown preconditioner %d", (int)pc);
     drop_inner(c);
     if (pc == BCGS_PC_BJ_BICGS || pc == BCGS_PC_G_BICGS) {   // P:393-394 defaults
-        if (pc == BCGS_PC_G_BICGS && (c->nranks > 1 || c->lg))
-            return fail(c, BCGS_E_CONFIG, "G(BiCGS) spans ranks: not built (nranks must be 1)");
+        if (pc == BCGS_PC_G_BICGS && c->lg)
+            return fail(c, BCGS_E_CONFIG, "G(BiCGS) across ranks needs the NCCL or p2p "
+                        "transport (not the in-process copy transport)");
         degree = 0;
         c->in_tol = pc == BCGS_PC_G_BICGS ? 1e-2 : 1e-6;
         c->in_max = 500;
@@ -1217,6 +1321,10 @@ bcgs_status bcgs_begin(bcgs_ctx c, double rel_tol, int32_t max_iter, int32_t fix
           c->lay.nx % 2 == 0 && !(c->pc == BCGS_PC_CHEB_G && c->nranks > 1)))
         return fail(c, BCGS_E_CONFIG, "BCGS_OPT_SYNC2 needs the fused path (kernels = 1, a "
                     "Chebyshev preconditioner, even nx)");
+    if (c->pipelined_opt && (inner_pc(c) || c->sync2_opt))
+        return fail(c, BCGS_E_CONFIG, "BCGS_OPT_PIPELINED needs a linear preconditioner "
+                    "(none / Chebyshev) and excludes BCGS_OPT_SYNC2");
+    if (c->pipelined_opt) TRY(pipe_alloc(c));
     TRY(enter(c));
     c->t0 = std::chrono::steady_clock::now();
     const int64_t n = npts(c);
@@ -1224,6 +1332,8 @@ bcgs_status bcgs_begin(bcgs_ctx c, double rel_tol, int32_t max_iter, int32_t fix
     k_init_state<<<1, 1, 0, c->s>>>(c->st, rel_tol, max_iter, fixed_iters, c->exact_opt);
     c->in_iters = 0;
     c->sync2 = c->sync2_opt ? 1 : 0;
+    c->pipelined = c->pipelined_opt;
+    drop_graph(c);   // the captured iteration depends on the algorithm variant
     // Alg. 3 l.1-4: r0 = b - A x0; r~ = r0; p0 = r0; ρ0 = r~ᵀr0.  The initial
     // guess set by bcgs_set_initial_guess applies to this solve only (V_X then holds the
     // iterate); later solves start from x0 = 0 unless a new guess is set (R21).
@@ -1245,6 +1355,12 @@ bcgs_status bcgs_begin(bcgs_ctx c, double rel_tol, int32_t max_iter, int32_t fix
     CUDA_OK(c, cudaGetLastError());
     TRY(reduce<2>(c, kEwBlocks, STAGE_SETUP, ew_depth(n), 3,
                   {F(c, V_B), F(c, V_B), F(c, V_RT), F(c, V_R)}));
+    if (c->pipelined) {   // recurrence vectors start at 0 (β = ω = 0: p0 = r0, S0 = w0, ...)
+        const size_t vb = sizeof(double) * (size_t)n;
+        for (int v : {V_P, V_PH, V_S, V_P2}) CUDA_OK(c, cudaMemsetAsync(F(c, v), 0, vb, c->s));
+        for (int i : {PZ, PZH, PV}) CUDA_OK(c, cudaMemsetAsync(c->pipe[i], 0, vb, c->s));
+        TRY(pipe_start(c));
+    }
     c->begun = 1;
     c->launched = 0;
     c->fixed = fixed_iters;
@@ -1292,7 +1408,8 @@ static bcgs_status poll_state(bcgs_ctx c, int32_t* done, int32_t* iter)
         int stage;
         TRY(resolve(c, &stage));
         if (stage < 0) return fail(c, BCGS_E_STATE, "parked solve without a parked stage");
-        if (stage != STAGE_SETUP) TRY(iteration(c, stage));
+        if (stage == STAGE_SETUP && c->pipelined) TRY(pipe_start(c));
+        else if (stage != STAGE_SETUP && stage != STAGE_PIPE_INIT) TRY(iteration(c, stage));
         TRY(read_state(c, done, iter));
         if (*done == DONE_RUNNING && c->launched > *iter) {
             TRY(enqueue_iterations(c, c->launched - *iter));
@@ -1514,20 +1631,27 @@ bcgs_status inner_ctx(bcgs_ctx c, int s, int key, bcgs_ctx* out)
     }
     if (!c->inner[s]) {
         const int nb = c->pc == BCGS_PC_G_BICGS ? 1 : c->bpr;
+        // G(BiCGS) on nranks > 1: ONE inner solve over the whole domain, spread over the
+        // same ranks -- a multi-rank context sharing the outer transport
+        const bool global = c->pc == BCGS_PC_G_BICGS && c->nranks > 1;
         bcgs_grid_desc g{};
         g.n[0] = c->lay.nx;
         g.n[1] = c->lay.ny;
-        g.n[2] = c->lay.L / nb;
+        g.n[2] = global ? c->lay.nz : c->lay.L / nb;
         g.h = c->h;
         for (int f = 0; f < 4; ++f) g.bc[f] = c->bc[f];
         g.bc[4] = (key & 1) ? BCGS_BC_NEUMANN : BCGS_BC_DIRICHLET;
         g.bc[5] = (key & 2) ? BCGS_BC_NEUMANN : BCGS_BC_DIRICHLET;
-        const size_t bytes = bcgs_workspace_bytes(&g, 1);
+        const int inr = global ? c->nranks : 1;
+        const size_t bytes = bcgs_workspace_bytes(&g, inr);
         if (!bytes) return fail(c, BCGS_E_CONFIG, "inner solver: invalid block grid");
         void* ws = nullptr;
         CUDA_OK(c, cudaMalloc(&ws, bytes));
         bcgs_ctx ic = nullptr;
-        bcgs_status st = create_ctx(&g, 0, 1, nullptr, nullptr, c->device, ws, bytes, c->s, &ic);
+        bcgs_status st = global ? create_ctx(&g, c->rank, c->nranks, nullptr, nullptr, c->device,
+                                             ws, bytes, c->s, &ic, 0, c)
+                                : create_ctx(&g, 0, 1, nullptr, nullptr, c->device, ws, bytes,
+                                             c->s, &ic);
         if (st != BCGS_OK) {
             std::string e = ic ? ic->err : "";
             if (ic) bcgs_destroy(ic);
@@ -1557,7 +1681,9 @@ bcgs_status precond_inner(bcgs_ctx c, const double* q, double* out, const DevSta
     // start every block's solve (bcgs_solve split into begin / iterate / poll / finish)
     for (int s = 0; s < nb; ++s) {
         const int gb = c->rank * nb + s;
-        const int key = ((c->bc[4] && gb == 0) ? 1 : 0) | ((c->bc[5] && gb == total - 1) ? 2 : 0);
+        int key = ((c->bc[4] && gb == 0) ? 1 : 0) | ((c->bc[5] && gb == total - 1) ? 2 : 0);
+        if (c->pc == BCGS_PC_G_BICGS && c->nranks > 1)   // the global problem's own faces
+            key = (c->bc[4] ? 1 : 0) | (c->bc[5] ? 2 : 0);
         TRY(inner_ctx(c, s, key, &ics[s]));
         bcgs_ctx ic = ics[s];
         bcgs_status e = bcgs_set_rhs(ic, q + s * blk, BCGS_MEM_DEVICE);

@@ -150,8 +150,12 @@ struct bcgs_ctx_s {
     double *hist = nullptr, *scal = nullptr;
     dd *part = nullptr, *rank_out = nullptr, *gath = nullptr;
     long long *limbs = nullptr, *glimbs = nullptr;   // R19 exact path (xdot.cuh)
-    const double* src[6][10] = {};   // operand pairs of each reduction stage (exact path)
+    const double* src[9][10] = {};   // operand pairs of each reduction stage (exact path)
     int exact_opt = 0;               // BCGS_OPT_EXACT_DOT
+    int pipelined_opt = 0, pipelined = 0;   // BCGS_OPT_PIPELINED (option / active solve)
+    char* pipe_mem = nullptr;        // pipelined: z, ẑ, q, q̂, y, v (library-owned fields)
+    size_t pipe_bytes = 0;
+    double* pipe[6] = {};
     double* h_pinned = nullptr;    // small pinned buffer for flag polls
     // options
     int kernels = 1, use_graph = 1, profile = 0, poll = 8, tb_variant = 7;
@@ -191,6 +195,7 @@ struct bcgs_ctx_s {
     // peer-memory transport (p2p.cuh): own mailbox (+ landing zones), the peers' mapped
     // mailboxes, and which of them were opened through CUDA IPC (closed at destroy)
     int p2p = 0, p2p_ready = 0;
+    int comm_borrowed = 0;           // G(BiCGS) inner context: the outer one's NCCL comm
     p2p::Peers peers{};
     char* mailbox = nullptr;
     size_t mailbox_bytes = 0;

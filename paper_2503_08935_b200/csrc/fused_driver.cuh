@@ -134,12 +134,12 @@ bool precond_supported(bcgs_ctx c)
     return supported(c, c->degree, c->pc != BCGS_PC_NONE);
 }
 
-bcgs_status precond_apply(bcgs_ctx c, const double* q, double* out)
+bcgs_status precond_apply(bcgs_ctx c, const double* q, double* out, const DevState* st)
 {
     TbArgs a{};
     a.q = q;
     a.out = out;
-    a.st = nullptr;
+    a.st = st;   // nullptr for the API call; the pipelined iteration passes its state
     Prof pf(c, KC_FUSED_P1, 16.0 * npts(c));
     return launch_tb<MODE_PLAIN>(c, a);
 }

@@ -281,7 +281,8 @@ inline bool supported(bcgs_ctx c, int degree, bool has_pc)
 bcgs_status iteration(bcgs_ctx c, int from);
 bcgs_status iteration_none(bcgs_ctx c, int from);
 bool precond_supported(bcgs_ctx c);
-bcgs_status precond_apply(bcgs_ctx c, const double* q, double* out);
+bcgs_status precond_apply(bcgs_ctx c, const double* q, double* out,
+                          const DevState* st = nullptr);
 bcgs_status precond_g_tb(bcgs_ctx c, const double* E, double* out, int v0, int v1,
                          const DevState* st);
 

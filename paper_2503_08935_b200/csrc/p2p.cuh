@@ -5,8 +5,8 @@
 // sequence-numbered flags -- no host involvement, so a multi-rank iteration is one CUDA graph.
 //
 // Every rank owns a Mailbox (library cudaMalloc; peers map it with CUDA IPC, or use the
-// pointer directly inside one process).  Sequence numbers live in DevState and advance on
-// the device, identically on every rank (bulk-synchronous: every rank performs the same
+// pointer directly inside one process).  Sequence numbers live in the own mailbox and advance
+// on the device, identically on every rank (bulk-synchronous: every rank performs the same
 // exchanges in the same order; a parked or finished solve skips them on every rank alike).
 //   halo seq q (sender):  wait until the receiver acknowledged q - 2 (same landing slot),
 //                         copy planes into its landing slot q & 1, fence, flag = q
@@ -35,7 +35,10 @@ struct Mailbox {
     unsigned long long halo_ack[2];       // halo seq the lower (0) / upper (1) rank consumed
     unsigned long long red_flag[MAXR];    // per source rank: reduction seq of its data
     unsigned ctr_send, ctr_land;          // block-completion counters (own rank only)
-    unsigned long long pad[9];
+    // this rank's exchange sequence numbers (own rank only; shared by every context that
+    // uses the mailbox, e.g. the inner solver of G(BiCGS))
+    unsigned long long seq_halo_sent, seq_halo_recv, seq_red;
+    unsigned long long pad[6];
     dd red[2][MAXR][5];                   // reduction triples [seq & 1][source rank][dot]
     long long limbs[2][MAXR][6 * xdot::XL];   // exact-path superaccumulators
     // landing zones follow at land_offset(): [dir][slot][cap planes][plane]
@@ -98,7 +101,7 @@ __device__ __forceinline__ double* land_slot(double* land, int dir, unsigned lon
 
 // Sender: planes [z0, z0 + k) of field v to the lower neighbour (dir 1 of its landing) and
 // planes [L - k, L) to the upper neighbour (dir 0 of its landing).  Grid-stride copy; the
-// last block to finish publishes the flags.  seq = st->halo_sent + 1.
+// last block to finish publishes the flags.  seq = seq_halo_sent + 1.
 // guarded != 0 (inside an iteration): skipped once the solve is done or parked, on every
 // rank alike; API calls (apply_operator, the x halo of begin / finish) pass 0.
 static __global__ void k_halo_send(Peers P, const double* __restrict__ v, int64_t L, int k,
@@ -106,7 +109,7 @@ static __global__ void k_halo_send(Peers P, const double* __restrict__ v, int64_
 {
     if (guarded && st->done) return;
     __shared__ int ok_s;
-    const unsigned long long seq = st->halo_sent + 1;
+    const unsigned long long seq = P.mb[P.rank]->seq_halo_sent + 1;
     const int r = P.rank;
     const bool lo = r > 0, hi = r < P.nranks - 1;
     Mailbox* me = P.mb[r];
@@ -143,16 +146,16 @@ static __global__ void k_halo_send(Peers P, const double* __restrict__ v, int64_
             if (lo) st_release(&P.mb[r - 1]->halo_flag[1], seq);
             if (hi) st_release(&P.mb[r + 1]->halo_flag[0], seq);
             *done_ctr = 0;
-            st->halo_sent = seq;
+            me->seq_halo_sent = seq;
         }
     }
 }
 
-// Receiver, part 1 (one warp): wait for the neighbours' data of seq = st->halo_recv + 1
+// Receiver, part 1 (one warp): wait for the neighbours' data of seq = seq_halo_recv + 1
 static __global__ void k_halo_wait(Peers P, DevState* st, int guarded)
 {
     if ((guarded && st->done) || threadIdx.x) return;
-    const unsigned long long seq = st->halo_recv + 1;
+    const unsigned long long seq = P.mb[P.rank]->seq_halo_recv + 1;
     const int r = P.rank;
     Mailbox* me = P.mb[r];
     bool ok = true;
@@ -167,7 +170,7 @@ static __global__ void k_halo_land(Peers P, double* gl, double* gh, int k, DevSt
 {
     if ((guarded && st->done) || st->comm_err) return;
     unsigned* done_ctr = &P.mb[P.rank]->ctr_land;
-    const unsigned long long seq = st->halo_recv + 1;
+    const unsigned long long seq = P.mb[P.rank]->seq_halo_recv + 1;
     const int r = P.rank;
     const int64_t n = (int64_t)k * P.plane;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -189,7 +192,7 @@ static __global__ void k_halo_land(Peers P, double* gl, double* gh, int k, DevSt
             if (r > 0) st_release(&P.mb[r - 1]->halo_ack[1], seq);
             if (r < P.nranks - 1) st_release(&P.mb[r + 1]->halo_ack[0], seq);
             *done_ctr = 0;
-            st->halo_recv = seq;
+            P.mb[r]->seq_halo_recv = seq;
         }
     }
 }
@@ -229,7 +232,7 @@ __global__ void __launch_bounds__(1024) k_reduce_p2p(Peers P, const dd* __restri
                    res[d].lo, res[d].ab);
         }
     } else {
-        const unsigned long long seq = st->red_seq + 1;
+        const unsigned long long seq = P.mb[me]->seq_red + 1;
         const int slot = (int)(seq & 1);
         for (int r = 0; r < P.nranks; ++r)
             for (int d = 0; d < ND; ++d) P.mb[r]->red[slot][me][d] = res[d];
@@ -237,7 +240,7 @@ __global__ void __launch_bounds__(1024) k_reduce_p2p(Peers P, const dd* __restri
             comm_error(st);
             return;
         }
-        st->red_seq = seq;
+        P.mb[me]->seq_red = seq;
         Mailbox* my = P.mb[me];
         for (int d = 0; d < ND; ++d) {
             comb[d] = dd{0.0, 0.0, 0.0, 0.0};
@@ -261,7 +264,7 @@ static __global__ void k_limbs_p2p(Peers P, const long long* __restrict__ mine, 
     __shared__ int ok_s;
     const int me = P.rank;
     const int64_t per = 6 * xdot::XL;
-    if (threadIdx.x == 0) seq_s = st->red_seq + 1;
+    if (threadIdx.x == 0) seq_s = P.mb[me]->seq_red + 1;
     __syncthreads();
     const int slot = (int)(seq_s & 1);
     for (int r = 0; r < P.nranks; ++r)
@@ -270,7 +273,7 @@ static __global__ void k_limbs_p2p(Peers P, const long long* __restrict__ mine, 
     __syncthreads();
     if (threadIdx.x == 0) {
         ok_s = exchange(P, st, seq_s) ? 1 : 0;
-        if (ok_s) st->red_seq = seq_s;
+        if (ok_s) P.mb[me]->seq_red = seq_s;
         else comm_error(st);
     }
     __syncthreads();

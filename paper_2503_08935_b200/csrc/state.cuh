@@ -16,6 +16,7 @@ enum : int32_t { DONE_RUNNING = 0, DONE_OK = 1, DONE_BREAKDOWN = 2, DONE_MAXIT =
 
 struct DevState {
     double rho, alpha, omega, beta, nb;
+    double den;           // pipelined: the α denominator r~ᵀw + β (r~ᵀS - ω r~ᵀz)
     double rw, ts, tt, rho_new, rr, rel;
     double tol;
     int32_t iter;         // completed outer iterations
@@ -30,9 +31,7 @@ struct DevState {
     double pend_v[5];     // the stage's values (certified ones final, the others replaced)
     int32_t exact_mode;   // BCGS_OPT_EXACT_DOT = 1: every dot through the exact path
     int32_t n_exact;      // dots recomputed exactly since bcgs_begin
-    // peer transport (p2p.cuh): exchange sequence numbers, monotone over the context's life
-    unsigned long long halo_sent, halo_recv, red_seq;
-    int32_t comm_err;
+    int32_t comm_err;     // peer transport (p2p.cuh): a wait timed out
     // the last refused certification: stage, dot, D, r, e, E, |r| gap up, gap down, Hc
     double cert_last[9];
     int32_t n_refused;    // certifications refused since bcgs_create
@@ -45,7 +44,11 @@ enum : int32_t {
     STAGE_OMEGA = 2,   // {tᵀs, tᵀt}           MPI4 + ω
     STAGE_RHO = 3,     // {r~ᵀr, rᵀr}          MPI5 + test + ρ, β
     STAGE_DOT = 4,     // stand-alone dot -> scratch
-    STAGE_OMEGA2 = 5   // 2-sync (R31): {tᵀs, tᵀt, r~ᵀs, r~ᵀt, sᵀs} -> ω, ρ_new, ||r||², test
+    STAGE_OMEGA2 = 5,  // 2-sync (R31): {tᵀs, tᵀt, r~ᵀs, r~ᵀt, sᵀs} -> ω, ρ_new, ||r||², test
+    // pipelined Bi-CGSTAB (pipe.cuh; NEXT-4): two reductions per iteration
+    STAGE_PIPE_INIT = 6,    // {r~ᵀw0} -> α0
+    STAGE_PIPE_OMEGA = 7,   // R1 {qᵀy, yᵀy} -> ω
+    STAGE_PIPE_RHO = 8      // R2 {r~ᵀr, r~ᵀw, r~ᵀS, r~ᵀz, rᵀr} -> test, β, α
 };
 
 // Executed by a single thread once the global Dot2 values are known.
@@ -121,6 +124,69 @@ __device__ __forceinline__ void stage_update(DevState* st, int stage, const doub
         st->beta = beta;
         st->rho = rho_new;
         sc[7] = beta;
+        if (st->fixed_iters <= 0 && i >= st->max_iter) st->done = DONE_MAXIT;
+        break;
+    }
+    case STAGE_PIPE_INIT: {
+        st->den = v[0];
+        st->beta = 0.0;
+        st->omega = 0.0;
+        if (v[0] == 0.0 || !isfinite(v[0])) {    // R7
+            st->done = DONE_BREAKDOWN;
+            break;
+        }
+        st->alpha = st->rho / v[0];
+        break;
+    }
+    case STAGE_PIPE_OMEGA: {
+        const int i = st->iter + 1;
+        double* sc = scal + 8 * (i - 1);
+        sc[0] = st->den;
+        sc[1] = st->alpha;
+        st->ts = v[0];
+        st->tt = v[1];
+        st->omega = (v[1] == 0.0) ? 0.0 : v[0] / v[1];   // R6
+        sc[2] = v[0];
+        sc[3] = v[1];
+        sc[4] = st->omega;
+        break;
+    }
+    case STAGE_PIPE_RHO: {
+        const int i = st->iter + 1;
+        double* sc = scal + 8 * (i - 1);
+        const double rho_new = v[0], rw = v[1], rS = v[2], rz = v[3], rr = v[4];
+        st->rho_new = rho_new;
+        st->rr = rr;
+        const double rel = sqrt(rr) / st->nb;    // R4
+        st->rel = rel;
+        st->iter = i;
+        hist[i] = rel;
+        sc[5] = rho_new;
+        sc[6] = rr;
+        sc[7] = 0.0;
+        if (st->fixed_iters > 0) {
+            if (i == st->fixed_iters) { st->done = DONE_OK; break; }
+        } else if (rel < st->tol) {
+            st->done = DONE_OK;
+            break;
+        }
+        const double omega = st->omega;
+        if (omega == 0.0 || rho_new == 0.0 || !isfinite(rho_new) || !isfinite(rr) ||
+            !isfinite(omega)) {
+            st->done = DONE_BREAKDOWN;
+            break;
+        }
+        const double beta = (rho_new / st->rho) * (st->alpha / omega);   // R20
+        st->beta = beta;
+        st->rho = rho_new;
+        sc[7] = beta;
+        const double den = fma(beta, fma(-omega, rz, rS), rw);
+        st->den = den;
+        if (den == 0.0 || !isfinite(den)) {
+            st->done = DONE_BREAKDOWN;
+            break;
+        }
+        st->alpha = rho_new / den;
         if (st->fixed_iters <= 0 && i >= st->max_iter) st->done = DONE_MAXIT;
         break;
     }
