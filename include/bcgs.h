@@ -155,10 +155,15 @@ typedef struct {
     double seconds;            /* wall time of the solve                                   */
 } bcgs_report;
 
+/* BCGS_ABI_VERSION of the library; one-line text of a status. */
 int32_t bcgs_abi_version(void);
 const char* bcgs_status_string(bcgs_status s);
 
-/* Device workspace the caller must provide to bcgs_create for this grid and rank count. */
+/* Device workspace the caller must provide to bcgs_create for this grid and rank count:
+ * the vectors of one rank's slab of Alg. 3 (x, r, r~, p, p̂, r̂, w, t, b, ... -- P:272-305)
+ * each with one ghost plane below and above (the halo planes of MPI1 / MPI3, P:278, P:286;
+ * DESIGN.md §4), the G(CI) extended slabs for nranks > 1, the device scalars and history,
+ * and the reduction partials.  Returns 0 for an invalid grid / rank count (nz % nranks). */
 size_t bcgs_workspace_bytes(const bcgs_grid_desc* grid, int32_t nranks);
 
 /* Chebyshev interval and constants for a configuration, computed on the host exactly as
@@ -194,8 +199,10 @@ bcgs_status bcgs_create_local(const bcgs_grid_desc* grid, int32_t nranks, int32_
  * bcgs_p2p_connect with the nranks records in rank order (CUDA IPC; ranks on the same or
  * on NVLink-connected devices).  The mailbox (and the landing zones of the halos) is
  * allocated and freed by the library.  In one process: bcgs_create_local_p2p (direct
- * pointers; drive each context from its own host thread).  Peer waits time out after 60 s
- * (BCGS_E_COMM) instead of hanging. */
+ * pointers; drive each context from its own host thread; set CUDA_MODULE_LOADING=EAGER
+ * before the CUDA context exists -- a lazy module load at a kernel's first launch can stall
+ * behind another rank's spin-waiting kernel on the same GPU).  Peer waits time out after
+ * 60 s (BCGS_E_COMM) instead of hanging. */
 bcgs_status bcgs_create_p2p(const bcgs_grid_desc* grid, int32_t rank, int32_t nranks,
                             int32_t cuda_device, void* d_workspace, size_t ws_bytes,
                             void* cuda_stream, bcgs_ctx* out);
@@ -204,6 +211,10 @@ bcgs_status bcgs_p2p_connect(bcgs_ctx ctx, const void* all_handles);
 bcgs_status bcgs_create_local_p2p(const bcgs_grid_desc* grid, int32_t nranks,
                                   int32_t cuda_device, void* const* d_workspaces,
                                   size_t ws_bytes, void* cuda_stream, bcgs_ctx* outs);
+/* Destroy a context (waits for its stream; frees what the library allocated, never the
+ * caller's workspace or stream).  last_error: one-line diagnostic of the last failed call
+ * (owned by the context).  set_option: bcgs_option switches (implementation choices; the
+ * maths of Alg. 3 is unchanged unless an option says otherwise). */
 void bcgs_destroy(bcgs_ctx ctx);
 const char* bcgs_last_error(bcgs_ctx ctx);
 bcgs_status bcgs_set_option(bcgs_ctx ctx, int32_t option, int64_t value);
@@ -238,7 +249,8 @@ int32_t bcgs_exact_dots(bcgs_ctx ctx);
  * chain depth D, r = fl(hi + lo), e = (hi + lo) - r, the error bound E, the gaps above and
  * below |r|, Σ|a_i b_i|, then the number of refusals since bcgs_create (10 doubles). */
 bcgs_status bcgs_certification_info(bcgs_ctx ctx, double* out10);
-/* Override the Chebyshev interval [a', b'] (0 < a' < b'); (0, 0) restores the default. */
+/* Override the Chebyshev interval [a', b'] of Alg. 2 (0 < a' < b'); (0, 0)
+ * restores the default bounds of Eq. 9-11 (R9, R10). */
 bcgs_status bcgs_set_eigen_bounds(bcgs_ctx ctx, double a, double b);
 
 /* Solve A x = b with Alg. 3.  fixed_iters > 0: run exactly that many iterations
@@ -255,11 +267,17 @@ bcgs_status bcgs_finish(bcgs_ctx ctx, bcgs_report* out);
 /* Order the caller's stream after all work enqueued so far (no host synchronisation). */
 bcgs_status bcgs_join(bcgs_ctx ctx);
 
-/* Residual history rel_0..rel_iters (rel_0 = 1); returns the count copied. */
+/* Residual history rel_0..rel_iters of the last solve: rel_i = sqrt(rᵀr)/||b|| of Alg. 3
+ * l.21-24 (R4; rel_0 = sqrt(r~ᵀr0)/||b|| = 1 for x0 = 0, R26); host_out holds
+ * cap doubles; returns the count copied (min(cap, iterations + 1); 0 on error).  Identical
+ * on every rank. */
 int32_t bcgs_residual_history(bcgs_ctx ctx, double* host_out, int32_t cap);
-/* Per-iteration scalars, 8 per iteration: r~ᵀw, α, tᵀs, tᵀt, ω, ρ_new, rᵀr, β. */
+/* Per-iteration scalars of Alg. 3, 8 per iteration: r~ᵀw, α, tᵀs, tᵀt, ω,
+ * ρ_new, rᵀr, β (pipelined, R32: α's denominator, α, qᵀy, yᵀy, ω, ρ_new, rᵀr, β);
+ * host_out holds 8 * cap_iters doubles; returns the iterations copied. */
 int32_t bcgs_scalar_history(bcgs_ctx ctx, double* host_out, int32_t cap_iters);
-/* Solution x (this rank's slab). */
+/* Solution x of Alg. 3 l.20 (the converged iterate, R25): this rank's slab,
+ * nx*ny*L doubles, x fastest, into device or host memory `x` (mem); the caller owns x. */
 bcgs_status bcgs_get_solution(bcgs_ctx ctx, double* x, int32_t mem);
 
 /* Single steps of the path on device slabs, for parity tests and micro-benchmarks.
@@ -273,7 +291,8 @@ bcgs_status bcgs_apply_preconditioner(bcgs_ctx ctx, const double* d_in, double* 
 bcgs_status bcgs_dot(bcgs_ctx ctx, const double* d_a, const double* d_b, double* host_out);
 
 /* Kernel timings accumulated while BCGS_OPT_PROFILE = 1 (CUDA events on the launching
- * stream).  Returns the number of kernel classes; names are '\n'-separated in names_out.
+ * stream; the paper's per-kernel profiling of Alg. 3, P:493 -- KernelBiCGS1-6, CI sweeps,
+ * MPI calls).  Returns the number of kernel classes; names are '\n'-separated in names_out.
  * ms_out[i] = total milliseconds, calls_out[i] = launches; bytes_out[i] = algorithmic
  * bytes per launch of class i. */
 int32_t bcgs_kernel_times(bcgs_ctx ctx, char* names_out, int32_t names_cap, double* ms_out,

@@ -8,7 +8,8 @@ import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-LIB = os.path.join(PKG, "lib", "libbcgs.so")
+# BCGS_BUILD_OUT / BCGS_NVCC_EXTRA: build a variant elsewhere (A/B timing with BCGS_LIB)
+LIB = os.environ.get("BCGS_BUILD_OUT") or os.path.join(PKG, "lib", "libbcgs.so")
 SRC = os.path.join(PKG, "csrc", "bcgs_api.cu")
 
 
@@ -37,20 +38,21 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 0) -> str:
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
         return LIB
     nccl = nccl_dir()
-    objdir = os.path.join(PKG, "lib", "obj")
+    objdir = os.path.join(os.path.dirname(LIB), "obj")
     os.makedirs(objdir, exist_ok=True)
     inc = ["-I", os.path.join(nccl, "include")]
 
     def compile_one(src):
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = ["nvcc", *NVCC_FLAGS, *inc, "-c", "-o", obj, os.path.join(PKG, "csrc", src)]
+        extra = os.environ.get("BCGS_NVCC_EXTRA", "").split()
+        cmd = ["nvcc", *NVCC_FLAGS, *extra, *inc, "-c", "-o", obj, os.path.join(PKG, "csrc", src)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         return src, obj, cmd, r
 
     jobs = jobs or min(len(CU_SOURCES), os.cpu_count() or 4)
     with cf.ThreadPoolExecutor(jobs) as ex:
         results = list(ex.map(compile_one, CU_SOURCES))
-    log = os.path.join(PKG, "lib", "ptxas.log")
+    log = os.path.join(os.path.dirname(LIB), "ptxas.log")
     with open(log, "w") as f:
         for src, obj, cmd, r in results:
             f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)

@@ -199,7 +199,7 @@ __global__ void k_resolve(DevState* st, const long long* __restrict__ limbs, int
                           int64_t rank_stride, double* hist, double* scal)
 {
     const int stage = st->pend_stage, mask = st->pend_mask;
-    if (!mask) return;
+    if (!mask || st->comm_err) return;   // a failed limb exchange leaves the stage parked
     bool bad = false;
     for (int r = 0; r < nranks; ++r) bad |= limbs[r * rank_stride + 5 * xdot::XL] != 0;
     double v[5];
@@ -294,6 +294,7 @@ bcgs_status p2p_halo(bcgs_ctx c, const double* v, double* gl, double* gh, int k,
         return fail(c, BCGS_E_CONFIG, "halo of %d planes > p2p landing capacity %lld", k,
                     (long long)c->peers.cap);
     const int nb = (int)std::min<int64_t>(kNumSMs, (k * c->lay.plane + 255) / 256);
+    p2p::k_halo_ack<<<1, 32, 0, hs>>>(c->peers, c->st, guarded);
     p2p::k_halo_send<<<nb, 256, 0, hs>>>(c->peers, v, c->lay.L, k, c->st, guarded);
     p2p::k_halo_wait<<<1, 32, 0, hs>>>(c->peers, c->st, guarded);
     p2p::k_halo_land<<<nb, 256, 0, hs>>>(c->peers, gl, gh, k, c->st, guarded);
@@ -408,7 +409,7 @@ bcgs_status reduce(bcgs_ctx c, int nparts, int stage, int depth, int k3_mask,
     if (c->p2p) {   // one kernel: finalize + one-shot peer exchange + rank-ordered combine
         if (!c->p2p_ready) return fail(c, BCGS_E_STATE, "p2p transport not connected");
         Prof pf(c, KC_FINALIZE, 0.0);
-        p2p::k_reduce_p2p<ND><<<1, 1024, 0, c->s>>>(c->peers, c->part, nparts, stage, c->st,
+        p2p::k_reduce_p2p<ND><<<1, 256, 0, c->s>>>(c->peers, c->part, nparts, stage, c->st,
                                                     c->hist, c->scal, depth, nprod, self_mask,
                                                     k3_mask, (c->ablate & 2) ? 1 : 0);
         CUDA_OK(c, cudaGetLastError());
@@ -559,6 +560,7 @@ bcgs_status precond_g(bcgs_ctx c, const double* q, double* out, const DevState* 
 }
 
 bcgs_status precond_inner(bcgs_ctx c, const double* q, double* out, const DevState* st);
+bcgs_status inner_all(bcgs_ctx c);
 
 bcgs_status precond_ref(bcgs_ctx c, const double* q, double* out, const DevState* st)
 {
@@ -768,7 +770,9 @@ bcgs_status enqueue_iterations(bcgs_ctx c, int n)
     // is supported but not exercised in round 1)
     // (inner-Krylov preconditioners synchronise the host inside an iteration: no graph)
     // graphs: one rank, or the p2p transport (kernels only); NCCL with BCGS_OPT_GRAPH = 2
-    const bool graph_ok = c->nranks == 1 || c->p2p || (c->comm && c->use_graph == 2);
+    // (not for in-process p2p groups: instantiating a graph can wait for the device, i.e.
+    // for another rank's kernel that spins on this rank -- a stall until the timeout)
+    const bool graph_ok = c->nranks == 1 || (c->p2p && !c->inproc) || (c->comm && c->use_graph == 2);
     if (c->use_graph && graph_ok && !c->profile && !c->lg && !inner_pc(c)) {
         if (!c->gexec) {
             cudaGraph_t graph;
@@ -989,6 +993,7 @@ static bcgs_status create_ctx(const bcgs_grid_desc* grid, int32_t rank, int32_t 
         c->p2p = share->p2p;
         c->p2p_ready = share->p2p_ready;
         c->peers = share->peers;
+        c->inproc = share->inproc;
     } else if (p2p) {   // mailbox + landing zones (face halos; G(CI) k-deep halos <= `cap`)
         c->p2p = 1;
         c->peers.rank = rank;
@@ -1095,6 +1100,7 @@ bcgs_status bcgs_create_local_p2p(const bcgs_grid_desc* grid, int32_t nranks,
             outs[r]->peers.land[q] = outs[q]->peers.land[q];
         }
         outs[r]->p2p_ready = 1;
+        outs[r]->inproc = 1;
     }
     return BCGS_OK;
 }
@@ -1169,7 +1175,10 @@ bcgs_status bcgs_set_option(bcgs_ctx c, int32_t option, int64_t value)
     case BCGS_OPT_ABLATE: c->ablate = (int)(value & 3); break;
     case BCGS_OPT_SYNC2: c->sync2_opt = (int)value; drop_graph(c); break;
     case BCGS_OPT_EXACT_DOT: c->exact_opt = value ? 1 : 0; break;
-    case BCGS_OPT_PIPELINED: c->pipelined_opt = value ? 1 : 0; break;
+    case BCGS_OPT_PIPELINED:   // allocate now (an allocation synchronises the device)
+        c->pipelined_opt = value ? 1 : 0;
+        if (c->pipelined_opt) TRY(pipe_alloc(c));
+        break;
     case BCGS_OPT_COMM_TIMEOUT:   // NCCL host waits; p2p device waits (default 60 s)
         c->comm_timeout_s = value > 0 ? (double)value : 300.0;
         c->peers.timeout_ns = (value > 0 ? (unsigned long long)value : 60ull) * 1000000000ull;
@@ -1259,7 +1268,12 @@ bcgs_status bcgs_set_preconditioner(bcgs_ctx c, bcgs_pc pc, int32_t degree, doub
     c->bpr = blocks_per_rank;
     drop_graph(c);
     c->begun = 0;
-    return validate_pc(c);
+    TRY(validate_pc(c));
+    // inner-Krylov preconditioners: create the private block contexts now, not inside the
+    // first solve -- their allocations synchronise the device, which must not happen while
+    // ranks sharing the GPU (in-process groups) are in a peer exchange
+    if (inner_pc(c)) TRY(inner_all(c));
+    return BCGS_OK;
 }
 
 bcgs_status bcgs_set_inner_solver(bcgs_ctx c, double rel_tol, int32_t max_iter)
@@ -1665,6 +1679,26 @@ bcgs_status inner_ctx(bcgs_ctx c, int s, int key, bcgs_ctx* out)
     return BCGS_OK;
 }
 
+// Neumann z faces (R27) of inner block s: the global problem's first / last block only
+int inner_key(bcgs_ctx c, int s)
+{
+    const int nb = c->pc == BCGS_PC_G_BICGS ? 1 : c->bpr;
+    const int total = c->nranks * nb, gb = c->rank * nb + s;
+    if (c->pc == BCGS_PC_G_BICGS && c->nranks > 1)   // the global problem's own faces
+        return (c->bc[4] ? 1 : 0) | (c->bc[5] ? 2 : 0);
+    return ((c->bc[4] && gb == 0) ? 1 : 0) | ((c->bc[5] && gb == total - 1) ? 2 : 0);
+}
+
+bcgs_status inner_all(bcgs_ctx c)
+{
+    const int nb = c->pc == BCGS_PC_G_BICGS ? 1 : c->bpr;
+    for (int s = 0; s < nb; ++s) {
+        bcgs_ctx ic;
+        TRY(inner_ctx(c, s, inner_key(c, s), &ic));
+    }
+    return BCGS_OK;
+}
+
 bcgs_status precond_inner(bcgs_ctx c, const double* q, double* out, const DevState* st)
 {
     if (st) {   // an outer stop earlier in this iteration (breakdown at α): nothing to do
@@ -1680,11 +1714,7 @@ bcgs_status precond_inner(bcgs_ctx c, const double* q, double* out, const DevSta
     std::vector<bcgs_ctx> ics(nb, nullptr);
     // start every block's solve (bcgs_solve split into begin / iterate / poll / finish)
     for (int s = 0; s < nb; ++s) {
-        const int gb = c->rank * nb + s;
-        int key = ((c->bc[4] && gb == 0) ? 1 : 0) | ((c->bc[5] && gb == total - 1) ? 2 : 0);
-        if (c->pc == BCGS_PC_G_BICGS && c->nranks > 1)   // the global problem's own faces
-            key = (c->bc[4] ? 1 : 0) | (c->bc[5] ? 2 : 0);
-        TRY(inner_ctx(c, s, key, &ics[s]));
+        TRY(inner_ctx(c, s, inner_key(c, s), &ics[s]));
         bcgs_ctx ic = ics[s];
         bcgs_status e = bcgs_set_rhs(ic, q + s * blk, BCGS_MEM_DEVICE);
         if (e == BCGS_OK) e = bcgs_begin(ic, c->in_tol, c->in_max, 0);

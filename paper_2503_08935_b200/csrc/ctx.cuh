@@ -196,6 +196,7 @@ struct bcgs_ctx_s {
     // mailboxes, and which of them were opened through CUDA IPC (closed at destroy)
     int p2p = 0, p2p_ready = 0;
     int comm_borrowed = 0;           // G(BiCGS) inner context: the outer one's NCCL comm
+    int inproc = 0;                  // p2p ranks sharing this process (and GPU): no graphs
     p2p::Peers peers{};
     char* mailbox = nullptr;
     size_t mailbox_bytes = 0;

@@ -13,9 +13,16 @@
 
 namespace stream {
 
-// threads (x pairs) x rows, planes per thread: 16 planes keep the partial count per launch
-// (one per CTA) at 16 K for 512^3 -- the finalize reads them all
-constexpr int SBX = 32, SBY = 8, SZC = 16;
+// threads (x pairs) x rows, planes per thread: 32 planes keep the partial count per launch
+// (one per CTA) at 8 K for 512^3 -- the finalize reads them all (measured 5.35 vs 5.41 ms)
+#ifndef BCGS_SZC
+#define BCGS_SZC 32
+#endif
+constexpr int SBX = 32, SBY = 8, SZC = BCGS_SZC;
+#ifndef BCGS_ST_UNROLL
+#define BCGS_ST_UNROLL 2
+#endif
+constexpr int kStUnroll = BCGS_ST_UNROLL;   // z-planes unrolled (loads in flight)
 
 // w = A v (global operator; ghost planes hold halo data or zeros) and Dot2 partials of
 // a·w (ND >= 1) and w·w (ND == 2).  Each thread owns 2 adjacent x points of one row and
@@ -24,7 +31,13 @@ constexpr int SBX = 32, SBY = 8, SZC = 16;
 template <int ND, int SBX, int SBY, int SZC>
 // occupancy targets (registers): ND = 0: 6 x 256 threads (<= 40), ND = 1, 2: 4 (<= 64),
 // ND = 5: 2 (<= 128) -- no spills; the kernel is latency-bound (long scoreboard)
-__global__ void __launch_bounds__(SBX * SBY, (ND == 5 ? 512 : ND >= 1 ? 1024 : 1536) / (SBX * SBY))
+#ifndef BCGS_ST1_THREADS
+#define BCGS_ST1_THREADS 1024   // ND = 1 (r~ᵀw, Dot3) resident threads per SM target
+#endif
+#ifndef BCGS_ST1_CHAINS
+#define BCGS_ST1_CHAINS 2       // ND = 1: independent Dot3 chains (x / y point)
+#endif
+__global__ void __launch_bounds__(SBX * SBY, (ND == 5 ? 512 : ND == 2 ? 1024 : ND == 1 ? BCGS_ST1_THREADS : 1536) / (SBX * SBY))
 k_stencil2_dot(const double* __restrict__ v,
                                                             const double* __restrict__ a,
                                                             const double* __restrict__ rt,
@@ -48,7 +61,7 @@ k_stencil2_dot(const double* __restrict__ v,
         double2 zm = *reinterpret_cast<const double2*>(v + c - plane);
         double2 zc = *reinterpret_cast<const double2*>(v + c);
         const bool hxm = i > 0, hxp = i + 2 < nx, hym = j > 0, hyp = j < ny - 1;
-#pragma unroll 2
+#pragma unroll kStUnroll
         for (int k = k0; k < k1; ++k, c += plane) {
             const double2 zp = *reinterpret_cast<const double2*>(v + c + plane);
             // out-of-domain neighbours: 0, or the mirror on a Neumann face (R27)
@@ -68,9 +81,10 @@ k_stencil2_dot(const double* __restrict__ v,
             if (ND >= 2) {          // tᵀs: Dot2, two chains
                 dot2_acc(p[0], s[0], ab[0], av.x, o.x);
                 dot2_acc(p2[0], s2[0], ab[0], av.y, o.y);
-            } else if (ND == 1) {   // r~ᵀw: Dot3, two chains
+            } else if (ND == 1) {   // r~ᵀw: Dot3, one or two chains
                 dot3_acc(p[0], m[0], s[0], ab[0], av.x, o.x);
-                dot3_acc(p2[0], m2[0], s2[0], ab[0], av.y, o.y);
+                if (BCGS_ST1_CHAINS == 2) dot3_acc(p2[0], m2[0], s2[0], ab[0], av.y, o.y);
+                else dot3_acc(p[0], m[0], s[0], ab[0], av.y, o.y);
             }
             if (ND == 2 || ND == 5) {
                 dot2_acc_self(p[1], s[1], o.x);

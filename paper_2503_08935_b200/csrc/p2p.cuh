@@ -104,26 +104,33 @@ __device__ __forceinline__ double* land_slot(double* land, int dir, unsigned lon
 // last block to finish publishes the flags.  seq = seq_halo_sent + 1.
 // guarded != 0 (inside an iteration): skipped once the solve is done or parked, on every
 // rank alike; API calls (apply_operator, the x halo of begin / finish) pass 0.
+// Every spin is done by ONE small block (k_halo_ack, k_halo_wait, the reduction's thread
+// 0), so ranks that share a GPU (in-process groups) keep SMs free for each other.
+//
+// Sender, part 1 (one warp): the receivers must have consumed seq - 2 (the same landing
+// slot) before it is overwritten.
+static __global__ void k_halo_ack(Peers P, DevState* st, int guarded)
+{
+    if ((guarded && st->done) || threadIdx.x) return;
+    const unsigned long long seq = P.mb[P.rank]->seq_halo_sent + 1;
+    const int r = P.rank;
+    Mailbox* me = P.mb[r];
+    bool ok = true;
+    if (r > 0 && seq > 2) ok &= wait_ge(&me->halo_ack[0], seq - 2, P.timeout_ns);
+    if (r < P.nranks - 1 && seq > 2) ok &= wait_ge(&me->halo_ack[1], seq - 2, P.timeout_ns);
+    if (!ok) comm_error(st);
+}
+
+// Sender, part 2
 static __global__ void k_halo_send(Peers P, const double* __restrict__ v, int64_t L, int k,
                             DevState* st, int guarded)
 {
-    if (guarded && st->done) return;
-    __shared__ int ok_s;
+    if ((guarded && st->done) || st->comm_err) return;
     const unsigned long long seq = P.mb[P.rank]->seq_halo_sent + 1;
     const int r = P.rank;
     const bool lo = r > 0, hi = r < P.nranks - 1;
     Mailbox* me = P.mb[r];
     unsigned* done_ctr = &me->ctr_send;
-    // the receiver must have consumed seq - 2 (same slot) before it is overwritten
-    if (threadIdx.x == 0) {
-        bool ok = true;
-        if (lo && seq > 2) ok &= wait_ge(&me->halo_ack[0], seq - 2, P.timeout_ns);
-        if (hi && seq > 2) ok &= wait_ge(&me->halo_ack[1], seq - 2, P.timeout_ns);
-        if (!ok) comm_error(st);
-        ok_s = ok;
-    }
-    __syncthreads();
-    if (!ok_s) return;
     const int64_t n = (int64_t)k * P.plane;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     if (lo) {   // my lowest planes -> lower rank, arriving "from above" (dir 1)
@@ -213,7 +220,7 @@ __device__ inline bool exchange(const Peers& P, DevState* st, unsigned long long
 // Fused reduction (one CTA of 1024 threads): this rank's partials -> triples (as
 // k_finalize), one-shot exchange, rank-ordered combination, stage completion (R19).
 template <int ND>
-__global__ void __launch_bounds__(1024) k_reduce_p2p(Peers P, const dd* __restrict__ part,
+__global__ void __launch_bounds__(256) k_reduce_p2p(Peers P, const dd* __restrict__ part,
                                                      int nparts, int stage, DevState* st,
                                                      double* hist, double* scal, int depth,
                                                      double nprod, int self_mask, int k3_mask,
@@ -251,7 +258,7 @@ __global__ void __launch_bounds__(1024) k_reduce_p2p(Peers P, const dd* __restri
             }
         }
     }
-    finish_stage(st, stage, ND, comb, depth + 2 * ((nparts + 1023) / 1024) + 48 + 2 * P.nranks,
+    finish_stage(st, stage, ND, comb, depth + 2 * ((nparts + 255) / 256) + 48 + 2 * P.nranks,
                  nprod, self_mask, k3_mask, hist, scal);
 }
 

@@ -1,6 +1,11 @@
 import os
 import sys
 
+# In-process groups on ONE GPU (bcgs_create_local_p2p) run each rank's kernels concurrently
+# with the others' spin-waiting kernels; lazily loading a kernel module at its first launch
+# can stall behind those waits.  Load every module when the CUDA context is created.
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

@@ -123,48 +123,10 @@ def test_inner_group_two_ranks(bc, orc):
 
 def test_g_bicgs_copy_transport_rejected(bc):
     """G(BiCGS) across ranks runs its global inner solve on the outer context's transport
-    (NCCL or p2p); the in-process copy transport (a host-barrier test twin of NCCL) has no
-    second group for it."""
+    (NCCL or p2p; tested across processes in test_gpu_p2p.py); the in-process copy transport
+    (a host-barrier test twin of NCCL) has no second group for it."""
     grp = bc.local_group((16, 16, 16), 1.0 / 17, 2)
     with pytest.raises(bc.BcgsError):
         grp[0].set_preconditioner("g_bicgs", 0)
     for s in grp:
         s.close()
-
-
-@pytest.mark.parametrize("P", [2, 4])
-def test_g_bicgs_across_ranks_bitwise(bc, orc, P):
-    """FBiCGS-G(BiCGS) on P ranks (p2p transport, one host thread per rank): the
-    inner solve is ONE Bi-CGSTAB over the whole domain, its reductions and halos spanning all
-    ranks -- so the result is the single-rank G(BiCGS)'s, bitwise, and the oracle's."""
-    n3 = (24, 20, 32)
-    h = si.unit_cube_h(24)
-    grp = bc.local_group(n3, h, P, transport="p2p")
-    reps, errs = [None] * P, []
-
-    def work(r):
-        try:
-            grp[r].set_preconditioner("g_bicgs", 0)
-            grp[r].set_rhs_random(si.SEED)
-            reps[r] = grp[r].solve(tol=1e-8, max_iter=200)
-        except Exception as ex:
-            errs.append(ex)
-
-    th = [threading.Thread(target=work, args=(r,)) for r in range(P)]
-    for t in th:
-        t.start()
-    for t in th:
-        t.join(timeout=600)
-    assert not errs, errs
-    x = np.concatenate([host(s.solution()) for s in grp])
-    hist = grp[0].residual_history()
-    inner = grp[0].inner_iterations()
-    for s in grp:
-        s.close()
-    o = orc.bicgstab(orc.rhs_random(n3[::-1], si.SEED), h, pc="g_bicgs", nslab=P, tol=1e-8,
-                     max_it=200)
-    assert o.status == "ok"
-    assert all(r["iterations"] == o.iterations for r in reps)
-    assert np.array_equal(hist, o.history)
-    assert np.array_equal(x, o.x)
-    assert inner == o.extra["inner_iterations"]

@@ -1,21 +1,19 @@
 """Peer-memory transport (p2p.cuh; SURVEY §8(e), NEXT-4 one-shot reductions): halos and
 reductions as device kernels storing into the peers' memory with sequence-numbered flags.
 
-* in one process: bcgs_create_local_p2p, one host thread per rank, multi-rank iterations
-  replayed as CUDA graphs;
-* across processes: two OS processes on the SAME GPU, mailboxes mapped through CUDA IPC
-  (bcgs_p2p_handle / bcgs_p2p_connect) -- the code path of one process per GPU; on one GPU
-  the two contexts time-slice, so the spin waits are slow but the protocol is the same.
+Ranks are OS processes on the SAME GPU (tests/mp_p2p.py): one CUDA context per rank, the
+mailboxes mapped through CUDA IPC (bcgs_p2p_handle / bcgs_p2p_connect) -- the code path of
+one process per GPU, multi-rank iterations replayed as CUDA graphs.  (In-process groups,
+bcgs_create_local_p2p, share one context: a driver call that waits for the device can stall
+behind another rank's spin-waiting kernel, so they are exercised here only for the timeout.)
 
 Every case is compared bitwise with the oracle's P-slab emulation (R19: correctly rounded
 dots make the rank count invisible in the reductions)."""
-import os
-import threading
-
 import numpy as np
 import pytest
 
 import synth_inputs as si
+from tests import mp_p2p
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -30,69 +28,64 @@ def bc():
     return bcgs
 
 
-def host(t):
-    return t.cpu().numpy()
-
-
-def run_local(bc, n3, h, P, pc, k, kernels=1, exact=0, tol=1e-8, fixed=0, graph=1):
-    grp = bc.local_group(n3, h, P, transport="p2p")
-    reps, errs = [None] * P, []
-
-    def work(r):
-        try:
-            s = grp[r]
-            s.set_option(bc.OPT_KERNELS, kernels)
-            s.set_option(bc.OPT_EXACT_DOT, exact)
-            s.set_option(bc.OPT_GRAPH, graph)
-            s.set_preconditioner(pc, k)
-            s.set_rhs_random(si.SEED)
-            reps[r] = s.solve(tol=tol, fixed_iters=fixed)
-        except Exception as ex:  # surface thread errors
-            errs.append(ex)
-
-    th = [threading.Thread(target=work, args=(r,)) for r in range(P)]
-    for t in th:
-        t.start()
-    for t in th:
-        t.join(timeout=600)
-    assert not errs, errs
-    x = np.concatenate([host(s.solution()) for s in grp])
-    hists = [s.residual_history() for s in grp]
-    scals = [s.scalar_history() for s in grp]
-    for s in grp:
-        s.close()
-    return reps, x, hists, scals
-
-
-@pytest.mark.parametrize("P,n3,pc,k,kernels", [(2, (48, 40, 64), "gnocomm", 4, 1),
-                                               (4, (64, 64, 64), "gnocomm", 4, 1),
-                                               (2, (40, 36, 48), "bj", 3, 1),
-                                               (4, (32, 32, 64), "none", 0, 1),
-                                               (2, (48, 40, 64), "g", 4, 1),
-                                               (4, (40, 32, 32), "g", 8, 0),
-                                               (8, (32, 32, 64), "gnocomm", 4, 0)])
-def test_p2p_local_group_matches_oracle(bc, orc, P, n3, pc, k, kernels):
-    h = si.unit_cube_h(n3[0])
-    reps, x, hists, scals = run_local(bc, n3, h, P, pc, k, kernels)
-    o = orc.bicgstab(orc.rhs_random(n3[::-1], si.SEED), h, pc=pc, k=k, nslab=P, tol=1e-8)
-    for rep, hist, scal in zip(reps, hists, scals):
+def check(out, P, o, scalars=True):
+    for r in range(P):
+        assert isinstance(out[r][0], dict), out[r][0]
+    x = np.concatenate([out[r][3] for r in range(P)])
+    for r in range(P):
+        rep, hist, scal = out[r][0], out[r][1], out[r][2]
         assert rep["iterations"] == o.iterations
-        assert np.array_equal(hist, o.history)
-        assert np.array_equal(scal, o.scalars)
+        assert np.array_equal(hist, o.history)          # identical scalars on every rank
+        if scalars:
+            assert np.array_equal(scal, o.scalars)
     assert np.array_equal(x, o.x)
 
 
-def test_p2p_forced_exact_and_direct_launches(bc, orc):
-    """The exact path's superaccumulators travel through the mailboxes too (k_limbs_p2p);
-    without graphs (direct launches) the same iterates."""
+@pytest.mark.parametrize("P,n3,pc,k,kernels", [(2, (48, 40, 64), "gnocomm", 4, 1),
+                                               (4, (32, 32, 64), "gnocomm", 4, 1),
+                                               (2, (40, 36, 48), "bj", 3, 1),
+                                               (2, (32, 32, 64), "none", 0, 1),
+                                               (2, (48, 40, 64), "g", 4, 1),
+                                               (4, (40, 32, 32), "g", 8, 0)])
+def test_p2p_ranks_match_oracle(bc, orc, P, n3, pc, k, kernels):
+    out = mp_p2p.run(P, {"n3": n3, "pc": pc, "k": k, "options": {"OPT_KERNELS": kernels}})
+    h = si.unit_cube_h(n3[0])
+    o = orc.bicgstab(orc.rhs_random(n3[::-1], si.SEED), h, pc=pc, k=k, nslab=P, tol=1e-8)
+    check(out, P, o)
+
+
+def test_p2p_forced_exact(bc, orc):
+    """The exact path's superaccumulators travel through the mailboxes too (k_limbs_p2p)."""
     n3, P = (32, 32, 64), 2
+    out = mp_p2p.run(P, {"n3": n3, "pc": "gnocomm", "k": 4, "options": {"OPT_EXACT_DOT": 1}})
     h = si.unit_cube_h(32)
     o = orc.bicgstab(orc.rhs_random(n3[::-1], si.SEED), h, pc="gnocomm", k=4, nslab=P, tol=1e-8)
-    for exact, graph in ((1, 1), (0, 0)):
-        reps, x, hists, _ = run_local(bc, n3, h, P, "gnocomm", 4, exact=exact, graph=graph)
-        assert reps[0]["iterations"] == o.iterations
-        assert np.array_equal(hists[0], o.history)
-        assert np.array_equal(x, o.x)
+    check(out, P, o)
+    assert out[0][5] >= 3 * o.iterations
+
+
+def test_p2p_pipelined(bc, orc):
+    """The pipelined iteration (R32) over the p2p transport."""
+    n3, P = (32, 32, 64), 2
+    out = mp_p2p.run(P, {"n3": n3, "pc": "gnocomm", "k": 4, "options": {"OPT_PIPELINED": 1}})
+    h = si.unit_cube_h(32)
+    o = orc.bicgstab(orc.rhs_random(n3[::-1], si.SEED), h, pc="gnocomm", k=4, nslab=P, tol=1e-8,
+                     pipelined=True)
+    check(out, P, o)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_p2p_g_bicgs_across_ranks(bc, orc, P):
+    """FBiCGS-G(BiCGS) on P ranks: the inner solve is ONE Bi-CGSTAB over the
+    whole domain whose halos and reductions span all ranks (it shares the outer transport),
+    so the result is the single-domain G(BiCGS)'s: bitwise the oracle's."""
+    n3 = (24, 20, 32)
+    out = mp_p2p.run(P, {"n3": n3, "pc": "g_bicgs", "max_iter": 200})
+    h = si.unit_cube_h(24)
+    o = orc.bicgstab(orc.rhs_random(n3[::-1], si.SEED), h, pc="g_bicgs", nslab=P, tol=1e-8,
+                     max_it=200)
+    check(out, P, o)
+    assert out[0][4] == o.extra["inner_iterations"]
 
 
 def test_p2p_timeout_instead_of_hang(bc):
@@ -108,60 +101,3 @@ def test_p2p_timeout_instead_of_hang(bc):
     assert ei.value.status == bc.E_COMM
     for g in grp:
         g.close()
-
-
-# ------------------------------------------------------------------ two processes (CUDA IPC)
-
-def _proc(rank, world, port, n3, pc, k, q):
-    import torch
-    import torch.distributed as dist
-    from paper_2503_08935_b200 import bcgs
-    torch.cuda.set_device(0)
-    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
-                            world_size=world)
-    try:
-        h = si.unit_cube_h(n3[0])
-        s = bcgs.Solver(n3, h, rank=rank, nranks=world, transport="p2p", device=0)
-        bcgs.connect_p2p(s)
-        s.set_option(bcgs.OPT_COMM_TIMEOUT, 60)
-        s.set_preconditioner(pc, k)
-        s.set_rhs_random(si.SEED)
-        rep = s.solve(tol=1e-8)
-        q.put((rank, rep, s.residual_history(), s.solution().cpu().numpy()))
-        dist.barrier()
-        s.close()
-    except Exception as ex:  # noqa: BLE001
-        q.put((rank, repr(ex), None, None))
-    finally:
-        dist.destroy_process_group()
-
-
-@pytest.mark.parametrize("pc,k", [("gnocomm", 4), ("g", 4)])
-def test_p2p_two_processes_one_gpu(bc, orc, pc, k):
-    import socket
-    import torch.multiprocessing as mp
-    sock = socket.socket()
-    sock.bind(("127.0.0.1", 0))
-    port = sock.getsockname()[1]
-    sock.close()
-    n3, P = (32, 24, 32), 2
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    procs = [ctx.Process(target=_proc, args=(r, P, port, n3, pc, k, q)) for r in range(P)]
-    for p in procs:
-        p.start()
-    out = {}
-    for _ in range(P):
-        r, rep, hist, x = q.get(timeout=600)
-        out[r] = (rep, hist, x)
-    for p in procs:
-        p.join(timeout=120)
-    for r in range(P):
-        assert isinstance(out[r][0], dict), out[r][0]
-    h = si.unit_cube_h(n3[0])
-    o = orc.bicgstab(orc.rhs_random(n3[::-1], si.SEED), h, pc=pc, k=k, nslab=P, tol=1e-8)
-    x = np.concatenate([out[r][2] for r in range(P)])
-    for r in range(P):
-        assert out[r][0]["iterations"] == o.iterations
-        assert np.array_equal(out[r][1], o.history)
-    assert np.array_equal(x, o.x)

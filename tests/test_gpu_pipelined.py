@@ -74,18 +74,20 @@ def test_pipelined_fixed_iterations_256(bc, orc):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("transport", ["copy", "p2p"])
+@pytest.mark.parametrize("transport", ["copy"])   # p2p: tests/test_gpu_p2p.py (processes)
 def test_pipelined_two_ranks(bc, orc, transport):
     n3, P = (32, 32, 64), 2
     h = si.unit_cube_h(32)
     grp = bc.local_group(n3, h, P, transport=transport)
     reps, errs = [None] * P, []
+    setup = threading.Barrier(P)   # set every rank up before any rank enters an exchange
 
     def work(r):
         try:
             grp[r].set_option(bc.OPT_PIPELINED, 1)
             grp[r].set_preconditioner("gnocomm", 4)
             grp[r].set_rhs_random(si.SEED)
+            setup.wait()
             reps[r] = grp[r].solve(tol=1e-8)
         except Exception as ex:
             errs.append(ex)
