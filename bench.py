@@ -61,6 +61,11 @@ def parse():
     ap.add_argument("--kernels", type=int, default=1, help="0 = reference kernels, 1 = fused")
     ap.add_argument("--sync2", action="store_true",
                     help="2-sync rewrite (R31): 2 reductions per iteration instead of 3")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
+                    help="N > 1: NCCL, or the peer-memory transport (p2p.cuh: one-shot "
+                         "reductions, graph replay)")
+    ap.add_argument("--pipelined", action="store_true",
+                    help="pipelined Bi-CGSTAB (R32): 2 reductions per iteration")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -205,7 +210,9 @@ def config_keys(args, n, k, world):
             "grid": n, "preconditioner": args.pc, "degree": k,
             "c_min": 10.0, "c_max": 1 - 1e-4, "decomposition": f"z-slab x{world}",
             "kernels": "fused" if args.kernels else "reference",
-            "reductions_per_iteration": 2 if args.sync2 else 3,
+            "reductions_per_iteration": 2 if (args.sync2 or args.pipelined) else 3,
+            "transport": args.transport if world > 1 else None,
+            "algorithm": "pipelined (R32)" if args.pipelined else "Alg. 3",
             "l2": "inputs larger than L2 (each field 8*N^3/P bytes >> 126 MB)",
             "rhs": "splitmix64 uniform[-1,1), seed 20250311"}
 
@@ -231,16 +238,22 @@ def main():
     nccl_id = None
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(bcgs.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        nccl_id = bytes(idt.cpu().numpy().tobytes())
+        if args.transport == "nccl":
+            idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+            if rank == 0:
+                idt.copy_(torch.frombuffer(bytearray(bcgs.nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(idt, 0)
+            nccl_id = bytes(idt.cpu().numpy().tobytes())
 
     n, k = args.n, args.degree
     h = si.unit_cube_h(n)
-    s = bcgs.Solver(n, h, rank=rank, nranks=world, nccl_id=nccl_id, device=local)
+    s = bcgs.Solver(n, h, rank=rank, nranks=world, nccl_id=nccl_id, device=local,
+                    transport=args.transport)
+    if world > 1 and args.transport == "p2p":
+        bcgs.connect_p2p(s)
     s.set_option(bcgs.OPT_KERNELS, args.kernels)
+    if args.pipelined:
+        s.set_option(bcgs.OPT_PIPELINED, 1)
     s.set_option(bcgs.OPT_SYNC2, 1 if args.sync2 else 0)
     s.set_preconditioner(args.pc, k)
     s.set_rhs_random(si.SEED)

@@ -121,12 +121,15 @@ typedef enum {
                                /* the communicator after it (default 300; async errors    */
                                /* abort at once); p2p device waits give up (default 60).  */
                                /* Both end the solve with an error status, never a hang.  */
-    BCGS_OPT_PIPELINED = 13    /* 1 = pipelined (communication-hiding) Bi-CGSTAB for      */
+    BCGS_OPT_PIPELINED = 13,   /* 1 = pipelined (communication-hiding) Bi-CGSTAB for      */
                                /* B = A M^-1 (NEXT-4; R32): 2 reductions  */
                                /* per iteration, each independent of the preconditioner + */
                                /* stencil that follows it; linear preconditioners only;   */
                                /* six more fields (library-owned).  Same iterates as Alg. 3 */
                                /* in exact arithmetic; the oracle implements the same flag */
+    BCGS_OPT_STENCIL = 14      /* stencil+dot kernels of a4 / a9: 1 = TMA-staged z-march  */
+                               /* (default; Dirichlet faces, even nx), 0 = L1-cached      */
+                               /* z-march.  Bitwise the same results                      */
 } bcgs_option;
 
 /* Boundary condition kind of a physical face (Eq. 4 / Eq. 5). */
@@ -178,7 +181,9 @@ bcgs_status bcgs_chebyshev_constants(const bcgs_grid_desc* grid, int32_t nslab, 
 bcgs_status bcgs_nccl_unique_id(void* out128);
 
 /* Create a context.  nccl_unique_id: 128-byte ncclUniqueId from rank 0 (broadcast by the
- * caller), NULL iff nranks == 1.  cuda_stream: caller's cudaStream_t (may be 0).
+ * caller); NULL for nranks == 1 (an id with nranks == 1 creates a 1-rank communicator whose
+ * all-gathers carry the reductions: the NCCL code path on one GPU, for testing).
+ * cuda_stream: caller's cudaStream_t (may be 0).
  * d_workspace: >= bcgs_workspace_bytes device bytes, 256-byte aligned. */
 bcgs_status bcgs_create(const bcgs_grid_desc* grid, int32_t rank, int32_t nranks,
                         const void* nccl_unique_id, int32_t cuda_device, void* d_workspace,

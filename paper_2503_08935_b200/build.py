@@ -23,7 +23,7 @@ def sources():
                   [os.path.join(ROOT, "include", "bcgs.h")])
 
 
-CU_SOURCES = ["bcgs_api.cu", "tb_multi.cu", "tb_multi_c.cu"] + [f"tb_k{k}.cu" for k in range(1, 9)]
+CU_SOURCES = ["bcgs_api.cu", "tb_multi.cu", "tb_multi_c.cu", "st_tma.cu"] + [f"tb_k{k}.cu" for k in range(1, 9)]
 NVCC_FLAGS = ["-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               # R17: no FMA contraction except the contract's explicit fma()
               "--fmad=false", "-std=c++17",

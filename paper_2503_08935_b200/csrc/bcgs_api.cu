@@ -415,13 +415,15 @@ bcgs_status reduce(bcgs_ctx c, int nparts, int stage, int depth, int k3_mask,
         CUDA_OK(c, cudaGetLastError());
         return BCGS_OK;
     }
+    // a communicator (also a 1-rank one: the NCCL path exercised on one GPU) -> all-gather
+    const bool gather = c->nranks > 1 || c->comm;
     {
         Prof pf(c, KC_FINALIZE, 0.0);
         k_finalize<ND><<<1, 1024, 0, c->s>>>(c->part, nparts, stage, c->st, c->hist, c->scal,
-                                              c->rank_out, c->nranks, depth, nprod, self_mask,
-                                              k3_mask);
+                                              c->rank_out, gather ? 2 : 1, depth, nprod,
+                                              self_mask, k3_mask);
     }
-    if (c->nranks > 1) {
+    if (gather) {
         TRY(allgather_pairs(c, ND));
         Prof pf(c, KC_SCALARS, 0.0);
         k_scalars<ND><<<1, 1, 0, c->s>>>(c->gath, c->nranks, stage, c->st, c->hist, c->scal,
@@ -458,7 +460,7 @@ bcgs_status resolve(bcgs_ctx c, int* stage)
     if (c->p2p) {
         p2p::k_limbs_p2p<<<1, 256, 0, c->s>>>(c->peers, c->limbs, c->glimbs, c->st);
         L = c->glimbs;
-    } else if (c->nranks > 1) {
+    } else if (c->nranks > 1 || c->comm) {
         TRY(allgather_bytes(c, c->limbs, c->glimbs, sizeof(long long) * per_rank));
         L = c->glimbs;
     }
@@ -1010,7 +1012,9 @@ static bcgs_status create_ctx(const bcgs_grid_desc* grid, int32_t rank, int32_t 
     }
     TRY(enter(c));
     CUDA_OK(c, cudaMemsetAsync(c->ws, 0, lay.total, c->s));   // zero ghost planes + state
-    if (nranks > 1 && !lg && !p2p && !share) {
+    // nranks == 1 with an id: a 1-rank communicator whose all-gathers carry the reductions
+    // (the NCCL code path on one GPU, for testing)
+    if ((nranks > 1 || nccl_unique_id) && !lg && !p2p && !share) {
         ncclUniqueId id;
         memcpy(&id, nccl_unique_id, sizeof id);
         NCCL_OK(c, ncclCommInitRank(&c->comm, nranks, id, rank));
@@ -1175,6 +1179,7 @@ bcgs_status bcgs_set_option(bcgs_ctx c, int32_t option, int64_t value)
     case BCGS_OPT_ABLATE: c->ablate = (int)(value & 3); break;
     case BCGS_OPT_SYNC2: c->sync2_opt = (int)value; drop_graph(c); break;
     case BCGS_OPT_EXACT_DOT: c->exact_opt = value ? 1 : 0; break;
+    case BCGS_OPT_STENCIL: c->stencil_tma = value ? 1 : 0; break;
     case BCGS_OPT_PIPELINED:   // allocate now (an allocation synchronises the device)
         c->pipelined_opt = value ? 1 : 0;
         if (c->pipelined_opt) TRY(pipe_alloc(c));

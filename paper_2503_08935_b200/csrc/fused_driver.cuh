@@ -154,6 +154,17 @@ bcgs_status halo_stencil(bcgs_ctx c, double* v, const double* a, double* out, in
     const int nx = (int)c->lay.nx, ny = (int)c->lay.ny, L = (int)c->lay.L;
     const dim3 sb(stream::SBX, stream::SBY);
     int nb = 0;
+    // TMA-staged kernel (st_tma.cu) for the bulk of the planes; the L1 kernel for Neumann
+    // faces, the 2-sync five-dot variant and the single boundary planes of nranks > 1
+    const bool tma = (ND == 1 || ND == 2) && c->stencil_tma && stencil_tma_ok(c);
+    auto launch_bulk = [&](int kb, int ke) -> bcgs_status {
+        if (!tma) return BCGS_OK;
+        int np = 0;
+        TRY(launch_stencil_tma<(ND == 1 ? 1 : 2)>(c, v, a, out, kb, ke,
+                                                  c->part + (int64_t)nb * ND, &np));
+        nb += np;
+        return BCGS_OK;
+    };
     auto launch = [&](int kb, int ke) {
         const dim3 g = stream::stencil2_grid(nx, ny, ke - kb);
         dd* pp = c->part + (int64_t)nb * ND;
@@ -163,13 +174,17 @@ bcgs_status halo_stencil(bcgs_ctx c, double* v, const double* a, double* out, in
     };
     Prof pf(c, kc, 24.0 * npts(c));
     if (c->nranks == 1) {
-        launch(0, L);
+        if (tma) TRY(launch_bulk(0, L));
+        else launch(0, L);
     } else {
         CUDA_OK(c, cudaEventRecord(c->ev_pre, c->s));
         CUDA_OK(c, cudaStreamWaitEvent(c->s_comm, c->ev_pre, 0));
         TRY(halo_on(c, v, c->s_comm));
         CUDA_OK(c, cudaEventRecord(c->ev_halo, c->s_comm));
-        if (L > 2) launch(1, L - 1);                       // interior, overlapped with the halo
+        if (L > 2) {                                       // interior, overlapped with the halo
+            if (tma) TRY(launch_bulk(1, L - 1));
+            else launch(1, L - 1);
+        }
         CUDA_OK(c, cudaStreamWaitEvent(c->s, c->ev_halo, 0));
         launch(0, 1);                                       // boundary planes
         if (L > 1) launch(L - 1, L);

@@ -2,6 +2,10 @@
 // instantiated once per degree K in tb_k<K>.cu (parallel compilation).
 #pragma once
 namespace fused {
+bool stencil_tma_ok(bcgs_ctx c);   // st_tma.cu
+template <int ND>
+bcgs_status launch_stencil_tma(bcgs_ctx c, const double* v, const double* a, double* out,
+                               int kb, int ke, dd* part, int* nparts);
 bcgs_status launch_multipass(bcgs_ctx c, TbArgs& a, int mode);   // tb_multi.cu
 template <int K, int MODE>
 bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz);

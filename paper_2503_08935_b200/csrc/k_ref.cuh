@@ -270,7 +270,8 @@ __global__ void k_update_p(double* __restrict__ p, const double* __restrict__ r,
 // One CTA combines `nparts` block partials (fixed order: contiguous chunks per thread,
 // then the deterministic block tree) into this rank's (hi, lo, ab) triples.  nranks == 1:
 // the stage is completed (certified, or parked for the exact path: finish_stage).
-// nranks > 1: the triples go to `rank_out` for the all-gather; k_scalars finishes.
+// nranks > 1 (or a 1-rank communicator: the caller passes 2): the quadruples go to
+// `rank_out` for the all-gather; k_scalars finishes.
 // depth = 2 x the longest per-thread product chain of the producer kernel; the bound D
 // adds the block, finalize and rank trees (dd.cuh, DESIGN.md §4 "Reductions").
 __host__ __device__ inline int reduce_depth(int depth, int nparts, int nranks)

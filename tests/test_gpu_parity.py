@@ -351,3 +351,47 @@ def test_tb_variant_option_rejects_removed_layouts(bc):
     for v in (5, 9):
         with pytest.raises(bc.BcgsError):
             s.set_option(bc.OPT_TB_VARIANT, v)
+
+
+@pytest.mark.parametrize("n3,pc,k,bpr", [((64, 48, 40), "gnocomm", 4, 1),
+                                         ((130, 66, 24), "none", 0, 1),
+                                         ((96, 80, 70), "bj", 3, 2),
+                                         ((192, 34, 65), "gnocomm", 2, 5)])
+def test_stencil_tma_equals_l1_kernel_and_oracle(bc, orc, n3, pc, k, bpr):
+    """The TMA-staged stencil+dot kernels (st_tma.cu: 64 x 16 tiles, 32-plane chunks; ragged
+    in x, y and z here) give the L1 kernels' and the oracle's iterates bitwise."""
+    h = si.unit_cube_h(n3[0])
+    outs = []
+    for tma in (0, 1):
+        s = bc.Solver(n3, h)
+        s.set_option(bc.OPT_STENCIL, tma)
+        s.set_preconditioner(pc, k, blocks_per_rank=bpr)
+        s.set_rhs_random(si.SEED)
+        s.solve(fixed_iters=6)
+        outs.append((s.residual_history(), s.scalar_history(), host(s.solution())))
+        s.close()
+    o = orc.bicgstab(orc.rhs_random(n3[::-1], si.SEED), h, pc=pc, k=k, nslab=bpr, fixed_it=6)
+    for hist, scal, x in outs:
+        assert np.array_equal(hist, o.history)
+        assert np.array_equal(scal, o.scalars)
+        assert np.array_equal(x, o.x)
+
+
+@pytest.mark.parametrize("graph,exact", [(0, 0), (2, 0), (2, 1)])
+def test_nccl_one_rank_communicator(bc, orc, graph, exact):
+    """The NCCL code path on one GPU: a 1-rank communicator (ncclCommInitRank) whose
+    ncclAllGather carries every reduction (and the exact path's superaccumulators), captured
+    into the CUDA graph with BCGS_OPT_GRAPH = 2; host waits poll ncclCommGetAsyncError."""
+    n = 48
+    h = si.unit_cube_h(n)
+    s = bc.Solver(n, h, nranks=1, nccl_id=bc.nccl_unique_id())
+    s.set_option(bc.OPT_GRAPH, graph)
+    s.set_option(bc.OPT_EXACT_DOT, exact)
+    s.set_preconditioner("gnocomm", 4)
+    s.set_rhs_random(si.SEED)
+    rep = s.solve(tol=1e-8)
+    o = orc.bicgstab(orc.rhs_random((n, n, n), si.SEED), h, pc="gnocomm", k=4, tol=1e-8)
+    assert rep["iterations"] == o.iterations
+    assert np.array_equal(s.residual_history(), o.history)
+    assert np.array_equal(host(s.solution()), o.x)
+    s.close()
