@@ -361,9 +361,10 @@ def main():
                 "timing": "average launch duration from CUDA events on the launching stream over "
                           "a second timed pass of K iterations (pass B)"}
         if dom_name in ("fused_p_cheb", "fused_s_cheb"):
-            roof["limiter"] = ("L1/shared-memory throughput (ncu l1tex 77-79 % of peak, DRAM "
-                               "38-46 %, FP64 pipe 41 %: profiles/round1_ncu_k_cheb_tb4_r1i.txt, "
-                               "DESIGN.md §4); the HBM fraction is reported against the kernel's "
+            roof["limiter"] = ("L1/shared-memory throughput (ncu l1tex 79.5 % / 75.2 % of peak "
+                               "for the p / s kernels, FP64 pipe 41 %, 24 warps per SM at the "
+                               "80-register cap: profiles/round2_ncu_full_r2a.txt, DESIGN.md "
+                               "§4); the HBM fraction is reported against the kernel's "
                                "compulsory bytes")
         if dom_name in FLOPS_PER_PT:
             # the temporally blocked Chebyshev kernels are FP64-ALU heavy: report that roof too

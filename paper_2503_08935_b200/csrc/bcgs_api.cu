@@ -755,9 +755,34 @@ after_r1:
                       F(c, V_RT), P[PZ], F(c, V_R), F(c, V_R)});   // R2
 }
 
+// ------------------------------------------------------------------ G(CI) on nranks > 1, fused
+// p and s live in the interiors of the extended slabs ext[0] / ext[1] (KG ghost planes per
+// side), so each application's k-deep halo (NEXT-1, §7) lands directly in the ghost region
+// of the preconditioner's input -- no copy of the input; a14 and a6 run as element-wise
+// kernels before it (the neighbours' planes of p / s must exist before the sweeps).
+bool g_fused(bcgs_ctx c)
+{
+    return c->pc == BCGS_PC_CHEB_G && c->nranks > 1 && c->kernels == 1 &&
+           c->degree >= 1 && c->degree <= fused::KMAX_TB && c->lay.nx % 2 == 0 && !c->sync2;
+}
+
+double* g_interior(bcgs_ctx c, int e) { return c->ext[e] + BCGS_MAX_DEGREE * c->lay.plane; }
+
+bcgs_status g_precond(bcgs_ctx c, int e, double* out)
+{
+    const int k = c->degree;
+    const int64_t L = c->lay.L, KG = BCGS_MAX_DEGREE;
+    TRY(halo_deep(c, g_interior(c, e), c->ext[e], k));
+    const int v0 = (int)(c->rank == 0 ? KG : KG - k);
+    const int v1 = (int)(c->rank == c->nranks - 1 ? KG + L : KG + L + k);
+    Prof pf(c, KC_PRECOND, 16.0 * npts(c));
+    return fused::precond_g_tb(c, c->ext[e], out, v0, v1, c->st);
+}
+
 bcgs_status iteration(bcgs_ctx c, int from)
 {
     if (c->pipelined) return iteration_pipe(c, from);
+    if (g_fused(c)) return fused::iteration_g(c, from);
     if (c->pc == BCGS_PC_CHEB_G && c->nranks > 1) return iteration_ref(c, from);   // k-deep halos
     if (c->kernels == 1 && fused::supported(c, c->degree, c->pc != BCGS_PC_NONE))
         return fused::iteration(c, from);
@@ -1369,6 +1394,9 @@ bcgs_status bcgs_begin(bcgs_ctx c, double rel_tol, int32_t max_iter, int32_t fix
     }
     CUDA_OK(c, cudaMemcpyAsync(F(c, V_RT), F(c, V_R), bytes, cudaMemcpyDeviceToDevice, c->s));
     CUDA_OK(c, cudaMemcpyAsync(F(c, V_P), F(c, V_R), bytes, cudaMemcpyDeviceToDevice, c->s));
+    if (g_fused(c))   // fused G(CI) on nranks > 1: p lives in the extended slab's interior
+        CUDA_OK(c, cudaMemcpyAsync(g_interior(c, 0), F(c, V_R), bytes, cudaMemcpyDeviceToDevice,
+                                   c->s));
     ref::k_dot2<2><<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(F(c, V_B), F(c, V_B), F(c, V_RT),
                                                            F(c, V_R), n, c->part);
     CUDA_OK(c, cudaGetLastError());

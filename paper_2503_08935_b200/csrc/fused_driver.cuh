@@ -333,5 +333,46 @@ a11:
     return BCGS_OK;
 }
 
+// The fused G(CI) iteration on nranks > 1 (bcgs_api.cu g_fused / g_precond).
+bcgs_status iteration_g(bcgs_ctx c, int from)
+{
+    const int64_t n = npts(c);
+    DevState* st = c->st;
+    double* p = g_interior(c, 0);
+    double* s = g_interior(c, 1);
+    int np1 = 0, np2 = 0;
+    if (from == STAGE_RHO) return BCGS_OK;
+    if (from == STAGE_OMEGA) goto a11;
+    if (from == STAGE_ALPHA) goto a6;
+    {
+        Prof pf(c, KC_UPDATE_P, 32.0 * n);
+        stream::k_update_p_lead<<<kEwBlocks, 256, 0, c->s>>>((double2*)p, (const double2*)F(c, V_R),
+                                                           (const double2*)F(c, V_W), n / 2, st);
+    }
+    TRY(g_precond(c, 0, F(c, V_PH)));
+    TRY(halo_stencil<1>(c, F(c, V_PH), F(c, V_RT), F(c, V_W), KC_STENCIL1, &np1));
+    TRY(reduce<1>(c, np1, STAGE_ALPHA, kStencilDepth, 1, {F(c, V_RT), F(c, V_W)}));
+a6:
+    {
+        Prof pf(c, KC_AXPY, 24.0 * n);
+        stream::k_axpy_s2<<<kEwBlocks, 256, 0, c->s>>>((double2*)s, (const double2*)F(c, V_R),
+                                                       (const double2*)F(c, V_W), n / 2, st);
+    }
+    TRY(g_precond(c, 1, F(c, V_RH)));
+    TRY(halo_stencil<2>(c, F(c, V_RH), s, F(c, V_T), KC_STENCIL2, &np2));
+    TRY(reduce<2>(c, np2, STAGE_OMEGA, kStencilDepth, 0, {F(c, V_T), s, F(c, V_T), F(c, V_T)}));
+a11:
+    {
+        Prof pf(c, KC_FUSED_XR, 64.0 * n);
+        stream::k_update_xr2<2><<<kEwBlocks, 256, 0, c->s>>>(
+            (double2*)F(c, V_X), (const double2*)F(c, V_PH), (const double2*)F(c, V_RH),
+            (const double2*)s, (double2*)F(c, V_R), (const double2*)F(c, V_T),
+            (const double2*)F(c, V_RT), n / 2, c->part, st);
+    }
+    CUDA_OK(c, cudaGetLastError());
+    return reduce<2>(c, kEwBlocks, STAGE_RHO, ew_depth(n), 1,
+                     {F(c, V_RT), F(c, V_R), F(c, V_R), F(c, V_R)});
+}
+
 }  // namespace fused
 

@@ -280,6 +280,7 @@ inline bool supported(bcgs_ctx c, int degree, bool has_pc)
 }
 bcgs_status iteration(bcgs_ctx c, int from);
 bcgs_status iteration_none(bcgs_ctx c, int from);
+bcgs_status iteration_g(bcgs_ctx c, int from);
 bool precond_supported(bcgs_ctx c);
 bcgs_status precond_apply(bcgs_ctx c, const double* q, double* out,
                           const DevState* st = nullptr);

@@ -219,4 +219,21 @@ __global__ void __launch_bounds__(256) k_update_p2(double2* __restrict__ p,
     }
 }
 
+// a14 at the START of an iteration (the fused G(CI) multi-rank iteration): p is updated in
+// place, except in iteration 1 (p0 = r0 already there) -- the element-wise twin of MODE_P
+__global__ void __launch_bounds__(256) k_update_p_lead(double2* __restrict__ p,
+                                                       const double2* __restrict__ r,
+                                                       const double2* __restrict__ w, int64_t n2,
+                                                       const DevState* __restrict__ st)
+{
+    if (st->done || st->iter == 0) return;
+    const double beta = st->beta, omega = st->omega;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n2;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const double2 rv = __ldg(r + c), wv = __ldg(w + c), pv = p[c];
+        p[c] = make_double2(upd_p(rv.x, pv.x, wv.x, beta, omega),
+                            upd_p(rv.y, pv.y, wv.y, beta, omega));
+    }
+}
+
 }  // namespace stream

@@ -395,3 +395,25 @@ def test_nccl_one_rank_communicator(bc, orc, graph, exact):
     assert np.array_equal(s.residual_history(), o.history)
     assert np.array_equal(host(s.solution()), o.x)
     s.close()
+
+
+@pytest.mark.parametrize("exact", [0, 1])
+def test_r7_breakdown_on_nonfinite_rw_matches_oracle(bc, orc, exact):
+    """R7: r~ᵀw overflows at iteration 1 (b = 1e300 at one point): BREAKDOWN with 0
+    iterations, x untouched, history [NaN] -- the same on the GPU (certified and exact dot
+    paths: a non-finite Σ|ab| or sum is never certified; the exact path rounds the overflow
+    to +inf) as in the oracle."""
+    n = 16
+    h = si.unit_cube_h(n)
+    b = np.zeros((n, n, n))
+    b[5, 6, 7] = 1e300
+    s, n3, _ = make(bc, n, pc="gnocomm", degree=4)
+    s.set_option(bc.OPT_EXACT_DOT, exact)
+    s.set_rhs(dev(b))
+    rep = s.solve(tol=1e-8)
+    o = orc.bicgstab(b, h, pc="gnocomm", k=4, tol=1e-8)
+    assert o.status == "breakdown" and rep["status_name"] == "breakdown"
+    assert rep["iterations"] == o.iterations == 0
+    assert np.array_equal(s.residual_history(), o.history, equal_nan=True)
+    assert not host(s.solution()).any()
+    s.close()

@@ -486,3 +486,18 @@ def test_gci_is_decomposition_independent_and_beats_gnocomm(orc):
     assert np.array_equal(g1.history, g4.history) and np.array_equal(g1.x, g4.x)
     assert np.array_equal(g1.x, gn1.x)
     assert g4.iterations <= gn4.iterations
+
+
+@pytest.mark.parametrize("pc,k", [("none", 0), ("gnocomm", 4)])
+def test_r7_breakdown_on_nonfinite_rw(orc, pc, k):
+    """R7 (paper silent): a non-finite r~ᵀw stops the solve before any update of that
+    iteration with BREAKDOWN and iterations = i - 1.  Constructed exactly: b = 1e300 at one
+    point makes bᵀb overflow (exact sum beyond the double range -> +inf, R19), so
+    ||b|| = inf, rel_0 = inf/inf = NaN, and r~ᵀw = Σ b_i (A p̂)_i overflows at iteration 1."""
+    n = 16
+    b = np.zeros((n, n, n))
+    b[5, 6, 7] = 1e300
+    r = orc.bicgstab(b, si.unit_cube_h(n), pc=pc, k=k, tol=1e-8)
+    assert r.status == "breakdown" and r.iterations == 0
+    assert len(r.history) == 1 and np.isnan(r.history[0])
+    assert not r.x.any()                      # no update was applied
