@@ -162,20 +162,31 @@ __device__ __forceinline__ void combine_partials(const dd* __restrict__ part, in
 //   Dot2 chains (first-level errors rounded into lo):  |Σ a_i b_i - (hi + mid + lo)|
 //                                                       <= 2 (D+1)^2 u^2 Hc + n 2^-1074
 //   Dot3 chains (first-level errors exact in mid):                <= 2 (D+1)^3 u^3 Hc + n 2^-1074
-// (Du < 0.01; the n 2^-1074 term covers low parts of products that underflow).  With
-// (t, e1) = TwoSum(mid, lo), (r, e2) = TwoSum(hi, t): hi + mid + lo = r + e2 + e1 exactly.
-// If the exact value lies strictly inside r's rounding interval, r is the correctly
-// rounded dot.  The bound is doubled and widened by the rounding of e1 + e2; the half gaps
-// are shrunk by 2^-50.
+// (Du < 0.01; the n 2^-1074 term covers low parts of products that underflow).  The three
+// components are renormalised by three error-free VecSum passes (x2, x1, x0 <- TwoSum
+// cascades from the bottom up; exact, so x0 + x1 + x2 = hi + mid + lo): when hi and
+// mid + lo nearly cancel (dots with a condition number far beyond 1/u, e.g. r~ᵀs late in a
+// 2-sync solve) a single pass would leave a remainder of many ulps of the leading term.
+// With r = x0 and the offset o = x1 + x2: if the exact value lies strictly inside r's
+// rounding interval, r is the correctly rounded dot.  The bound is doubled and widened by
+// the rounding of o; the half gaps are shrunk by 2^-50.
 __device__ __forceinline__ bool dd_certify(const dd& c, double AB, int D, double nprod, bool k3,
                                            double* out, double* r_out = nullptr,
                                            double* o_out = nullptr, double* E_out = nullptr)
 {
-    double t, e1, r, e2;
-    two_sum(c.mid, c.lo, t, e1);
-    two_sum(c.hi, t, r, e2);
+    double x0 = c.hi, x1 = c.mid, x2 = c.lo;
+#pragma unroll
+    for (int pass = 0; pass < 3; ++pass) {
+        double s1, e1, s0, e0;
+        two_sum(x1, x2, s1, e1);
+        two_sum(x0, s1, s0, e0);
+        x0 = s0;
+        x1 = e0;
+        x2 = e1;
+    }
+    const double r = x0;
     *out = r;
-    const double o = e2 + e1;
+    const double o = x1 + x2;
     const double d1 = (double)D + 1.0;
     const double bound = k3 ? 2.0 * (d1 * d1 * d1) * (0x1p-53 * 0x1p-53 * 0x1p-53) * AB
                             : 2.0 * (d1 * d1) * (0x1p-53 * 0x1p-53) * AB;

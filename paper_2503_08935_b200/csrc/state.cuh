@@ -257,7 +257,8 @@ __device__ __forceinline__ void finish_stage(DevState* st, int stage, int nd, co
     int mask = 0;
     for (int d = 0; d < nd; ++d) {
         const dd& c = comb[d];
-        const double ab = (self_mask >> d) & 1 ? fabs((c.hi + c.mid) + c.lo) * 1.001 : c.ab;
+        const double ab = (self_mask >> d) & 1 ? fabs((c.hi + c.mid) + c.lo) * 1.001 + 0x1p-1022
+                                               : c.ab;
         double r, o, E;
         const bool ok = dd_certify(c, ab, D, nprod, (k3_mask >> d) & 1, &v[d], &r, &o, &E);
         if (!ok) {

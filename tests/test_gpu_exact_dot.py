@@ -162,3 +162,25 @@ def test_forced_exact_multirank_bitwise(bc, orc, P, pc, kernels):
     assert all(r["iterations"] == o.iterations for r in reps)
     assert np.array_equal(hist, o.history)
     assert np.array_equal(x, o.x)
+
+
+@pytest.mark.parametrize("sync2,fixed", [(0, 0), (1, 45)])
+def test_certification_holds_deep_into_the_solve(bc, orc, sync2, fixed):
+    """The certified path carries whole solves without the exact fallback: the r~ dots grow
+    ill-conditioned as Bi-CGSTAB converges (r~ᵀs of the 2-sync rewrite reaches
+    Σ|ab|/|Σab| ~ 1e20 after 20-40 iterations), which Dot3 plus a renormalised final sum
+    still certifies.  Results are bitwise the oracle's either way."""
+    n = 64
+    h = si.unit_cube_h(n)
+    s = bc.Solver(n, h)
+    s.set_option(bc.OPT_SYNC2, sync2)
+    s.set_preconditioner("gnocomm", 4)
+    s.set_rhs_random(si.SEED)
+    rep = s.solve(tol=1e-8, fixed_iters=fixed)
+    assert s.exact_dots() == 0, s.certification_info()
+    o = orc.bicgstab(orc.rhs_random((n, n, n), si.SEED), h, pc="gnocomm", k=4, tol=1e-8,
+                     fixed_it=fixed, sync2=bool(sync2))
+    assert rep["iterations"] == o.iterations
+    assert np.array_equal(s.residual_history(), o.history)
+    assert np.array_equal(host(s.solution()), o.x)
+    s.close()

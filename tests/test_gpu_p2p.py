@@ -46,7 +46,8 @@ def check(out, P, o, scalars=True):
                                                (2, (40, 36, 48), "bj", 3, 1),
                                                (2, (32, 32, 64), "none", 0, 1),
                                                (2, (48, 40, 64), "g", 4, 1),
-                                               (4, (40, 32, 32), "g", 8, 0)])
+                                               (4, (40, 32, 32), "g", 8, 0),
+                                               (8, (32, 32, 64), "gnocomm", 4, 1)])
 def test_p2p_ranks_match_oracle(bc, orc, P, n3, pc, k, kernels):
     out = mp_p2p.run(P, {"n3": n3, "pc": pc, "k": k, "options": {"OPT_KERNELS": kernels}})
     h = si.unit_cube_h(n3[0])
