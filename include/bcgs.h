@@ -128,8 +128,10 @@ typedef enum {
                                /* six more fields (library-owned).  Same iterates as Alg. 3 */
                                /* in exact arithmetic; the oracle implements the same flag */
     BCGS_OPT_STENCIL = 14      /* stencil+dot kernels of a4 / a9: 1 = TMA-staged z-march  */
-                               /* (default; Dirichlet faces, even nx), 0 = L1-cached      */
-                               /* z-march.  Bitwise the same results                      */
+                               /* (default; Dirichlet faces, even nx; planes per CTA from */
+                               /* a wave cost model), v >= 2 = TMA with v planes per CTA  */
+                               /* (>= 4; measurement), 0 = L1-cached z-march.  Bitwise the */
+                               /* same results; values outside 0..4096: BCGS_E_INVALID    */
 } bcgs_option;
 
 /* Boundary condition kind of a physical face (Eq. 4 / Eq. 5). */

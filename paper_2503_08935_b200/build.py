@@ -42,10 +42,19 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 0) -> str:
     os.makedirs(objdir, exist_ok=True)
     inc = ["-I", os.path.join(nccl, "include")]
 
+    # headers are shared by every unit: an object is reused only if it is newer than its own
+    # .cu, every header and this script (and not force)
+    hdr = max(os.path.getmtime(p) for p in sources() + [os.path.abspath(__file__)]
+              if not p.endswith(".cu"))
+
     def compile_one(src):
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
         extra = os.environ.get("BCGS_NVCC_EXTRA", "").split()
         cmd = ["nvcc", *NVCC_FLAGS, *extra, *inc, "-c", "-o", obj, os.path.join(PKG, "csrc", src)]
+        cu = os.path.join(PKG, "csrc", src)
+        if (not force and not extra and os.path.exists(obj) and
+                os.path.getmtime(obj) >= max(hdr, os.path.getmtime(cu))):
+            return src, obj, cmd, subprocess.CompletedProcess(cmd, 0, "(up to date)\n", "")
         r = subprocess.run(cmd, capture_output=True, text=True)
         return src, obj, cmd, r
 

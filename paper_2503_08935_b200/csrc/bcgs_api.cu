@@ -1195,8 +1195,8 @@ bcgs_status bcgs_set_option(bcgs_ctx c, int32_t option, int64_t value)
     case BCGS_OPT_PROFILE: c->profile = (int)value; break;
     case BCGS_OPT_POLL: c->poll = std::max<int>(1, (int)value); break;
     case BCGS_OPT_TB_VARIANT:
-        if (value != 2 && value != 7)
-            return fail(c, BCGS_E_INVALID, "temporally blocked layout %lld: 2 or 7",
+        if (value != 2 && value != 7 && value != 8 && value != 10)
+            return fail(c, BCGS_E_INVALID, "temporally blocked layout %lld: 2, 7, 8 or 10",
                         (long long)value);
         c->tb_variant = (int)value;
         break;
@@ -1204,7 +1204,10 @@ bcgs_status bcgs_set_option(bcgs_ctx c, int32_t option, int64_t value)
     case BCGS_OPT_ABLATE: c->ablate = (int)(value & 3); break;
     case BCGS_OPT_SYNC2: c->sync2_opt = (int)value; drop_graph(c); break;
     case BCGS_OPT_EXACT_DOT: c->exact_opt = value ? 1 : 0; break;
-    case BCGS_OPT_STENCIL: c->stencil_tma = value ? 1 : 0; break;
+    case BCGS_OPT_STENCIL:
+        if (value < 0 || value > 4096) return fail(c, BCGS_E_INVALID, "stencil option %lld", (long long)value);
+        c->stencil_tma = (int)value;
+        break;
     case BCGS_OPT_PIPELINED:   // allocate now (an allocation synchronises the device)
         c->pipelined_opt = value ? 1 : 0;
         if (c->pipelined_opt) TRY(pipe_alloc(c));

@@ -23,7 +23,8 @@ constexpr int VSZ = (BXV * BYV * 8 + 127) / 128 * 128;        // bytes, 128-B al
 constexpr int ASZ = TXO * TYO * 8;
 constexpr int SLOT = VSZ + ASZ;
 constexpr int SMEM = NS * SLOT + 128;
-constexpr int ZC = 32;                                        // planes per CTA (chunk)
+constexpr int ZC = 32;                      // planes per CTA (chunk) on deep slabs
+constexpr int ZC_MIN = 4;                   // partial-slot capacity (ctx.cuh max_blocks)
 }  // namespace st
 
 struct StMaps {
@@ -34,7 +35,7 @@ struct StMaps {
 template <int ND>
 __global__ void __launch_bounds__(st::NW * 32, 3) k_stencil_tma(
     const __grid_constant__ StMaps maps, double* __restrict__ out, int nx, int ny, int kb, int ke,
-    double h2inv, dd* __restrict__ part, const DevState* __restrict__ st)
+    int zc, double h2inv, dd* __restrict__ part, const DevState* __restrict__ st)
 {
     using namespace st;
     if (st && st->done) return;
@@ -43,7 +44,7 @@ __global__ void __launch_bounds__(st::NW * 32, 3) k_stencil_tma(
     uint64_t* bar = reinterpret_cast<uint64_t*>(smb + NS * SLOT);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int x0 = blockIdx.x * TXO, y0 = blockIdx.y * TYO;
-    const int k0 = kb + blockIdx.z * ZC, k1 = min(ke, k0 + ZC);
+    const int k0 = kb + blockIdx.z * zc, k1 = min(ke, k0 + zc);
     // step s (0-based) consumes v planes k0-1+s .. k0+1+s and a plane k0+s; slot s % NS
     // receives v plane k0+1+s and a plane k0+s (plane k0-1 and k0 arrive in the prologue)
     const int nsteps = k1 - k0;
@@ -145,6 +146,30 @@ bool stencil_tma_ok(bcgs_ctx c)
            c->mbc.zhi < 0;
 }
 
+// Planes per CTA.  Each CTA pays 2 extra v planes (the z-neighbours of its first and last
+// plane) and one pipeline fill; deep slabs use ZC (many waves of 3 CTAs per SM: the tail is
+// a small fraction).  On thin slabs (the per-rank shape of a multi-GPU run, 512^2 x 64 at
+// P = 8) ZC leaves a fractional last wave of 3 x 148 slots, so the chunk length minimises
+// waves x (planes + 2) there.  BCGS_OPT_STENCIL >= 2 fixes the length (measurement).
+static int stencil_zc(bcgs_ctx c, int tiles, int planes)
+{
+    using namespace st;
+    if (c->stencil_tma >= 2) return std::max(ZC_MIN, c->stencil_tma);
+    const int64_t slots = (int64_t)kNumSMs * 3;
+    const int64_t deep = (int64_t)tiles * ((planes + ZC - 1) / ZC);
+    if (deep >= 4 * slots) return ZC;
+    int best = ZC;
+    double best_cost = 1e300;
+    for (int nch = 1; nch <= (planes + ZC_MIN - 1) / ZC_MIN; ++nch) {
+        const int zc = (planes + nch - 1) / nch;
+        if (zc < ZC_MIN) break;
+        const int64_t waves = ((int64_t)tiles * nch + slots - 1) / slots;
+        const double cost = (double)waves * (zc + 2);
+        if (cost < best_cost * 0.999) { best_cost = cost; best = zc; }
+    }
+    return best;
+}
+
 template <int ND>
 bcgs_status launch_stencil_tma(bcgs_ctx c, const double* v, const double* a, double* out,
                                int kb, int ke, dd* part, int* nparts)
@@ -170,9 +195,10 @@ bcgs_status launch_stencil_tma(bcgs_ctx c, const double* v, const double* a, dou
     if (!mk(&maps.v, v, BXV, BYV) || (ND >= 1 && !mk(&maps.a, a, TXO, TYO)))
         return fail(c, BCGS_E_CUDA, "cuTensorMapEncodeTiled failed (stencil)");
     if (ND == 0) maps.a = maps.v;
+    const int zc = stencil_zc(c, (int)((nx + TXO - 1) / TXO) * (int)((ny + TYO - 1) / TYO), ke - kb);
     const dim3 grid((unsigned)((nx + TXO - 1) / TXO), (unsigned)((ny + TYO - 1) / TYO),
-                    (unsigned)((ke - kb + ZC - 1) / ZC));
-    kern<<<grid, NW * 32, SMEM, c->s>>>(maps, out, (int)nx, (int)ny, kb, ke, c->h2inv, part,
+                    (unsigned)((ke - kb + zc - 1) / zc));
+    kern<<<grid, NW * 32, SMEM, c->s>>>(maps, out, (int)nx, (int)ny, kb, ke, zc, c->h2inv, part,
                                         c->st);
     CUDA_OK(c, cudaGetLastError());
     *nparts = (int)(grid.x * grid.y * grid.z);

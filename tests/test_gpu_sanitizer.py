@@ -22,4 +22,6 @@ def test_compute_sanitizer_clean(tool):
     r = subprocess.run([cs, "--tool", tool, "--error-exitcode", "3", sys.executable,
                         os.path.join(ROOT, "tools", "sanitize_run.py")],
                        capture_output=True, text=True, timeout=900)
+    if "closed on this pool" in r.stdout + r.stderr:   # the GPU pool's wrapper refuses to run
+        pytest.skip("compute-sanitizer is disabled on this GPU pool")
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
