@@ -184,7 +184,7 @@ struct bcgs_ctx_s {
     std::chrono::steady_clock::time_point t0;
     // graph
     cudaGraphExec_t gexec = nullptr;
-    int graph_key = -1;
+    int graph_key = -1;              // (sync2, pipelined) of the captured iteration
     // profiling
     std::vector<EvRec> pending;
     std::vector<cudaEvent_t> free_ev;

@@ -87,17 +87,29 @@ __device__ __forceinline__ void block_reduce_dd(double (&p)[ND], double (&m)[ND]
     const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
     const int nthr = blockDim.x * blockDim.y * blockDim.z;
     const int lane = tid & 31, warp = tid >> 5, nwarp = (nthr + 31) >> 5;
-#pragma unroll
-    for (int d = 0; d < ND; ++d) {
+    // the ND trees are independent: level-outer / dot-inner loops let their dependency
+    // chains interleave (same operands per dd_add as dot-outer: bitwise the same tree)
+    auto warp_tree = [&]() {
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
-            double op = __shfl_down_sync(0xffffffffu, p[d], off);
-            double om = __shfl_down_sync(0xffffffffu, m[d], off);
-            double os = __shfl_down_sync(0xffffffffu, s[d], off);
-            double oa = __shfl_down_sync(0xffffffffu, ab[d], off);
-            if (lane + off < 32) dd_add(p[d], m[d], s[d], ab[d], op, om, os, oa);
+            double op[ND], om[ND], os[ND], oa[ND];
+#pragma unroll
+            for (int d = 0; d < ND; ++d) {
+                op[d] = __shfl_down_sync(0xffffffffu, p[d], off);
+                om[d] = __shfl_down_sync(0xffffffffu, m[d], off);
+                os[d] = __shfl_down_sync(0xffffffffu, s[d], off);
+                oa[d] = __shfl_down_sync(0xffffffffu, ab[d], off);
+            }
+            if (lane + off < 32) {
+#pragma unroll
+                for (int d = 0; d < ND; ++d) dd_add(p[d], m[d], s[d], ab[d], op[d], om[d], os[d], oa[d]);
+            }
         }
-        if (lane == 0) sh[warp][d] = dd{p[d], m[d], s[d], ab[d]};
+    };
+    warp_tree();
+    if (lane == 0) {
+#pragma unroll
+        for (int d = 0; d < ND; ++d) sh[warp][d] = dd{p[d], m[d], s[d], ab[d]};
     }
     __syncthreads();
     if (warp == 0) {
@@ -108,15 +120,11 @@ __device__ __forceinline__ void block_reduce_dd(double (&p)[ND], double (&m)[ND]
             m[d] = v.mid;
             s[d] = v.lo;
             ab[d] = v.ab;
+        }
+        warp_tree();
+        if (lane == 0) {
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                double op = __shfl_down_sync(0xffffffffu, p[d], off);
-                double om = __shfl_down_sync(0xffffffffu, m[d], off);
-                double os = __shfl_down_sync(0xffffffffu, s[d], off);
-                double oa = __shfl_down_sync(0xffffffffu, ab[d], off);
-                if (lane + off < 32) dd_add(p[d], m[d], s[d], ab[d], op, om, os, oa);
-            }
-            if (lane == 0) out[d] = dd{p[d], m[d], s[d], ab[d]};
+            for (int d = 0; d < ND; ++d) out[d] = dd{p[d], m[d], s[d], ab[d]};
         }
     }
 }

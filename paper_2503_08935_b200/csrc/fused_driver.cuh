@@ -45,9 +45,7 @@ void variant_tile(bcgs_ctx c, bool neu, int k, int* tx, int* ty)
 {
     const int hx = (k + 1) / 2 * 2;                        // TMA: even x-halo
     const bool tma = c->tb_variant != 2 && c->lay.nx % 2 == 0;
-    if (tma && !neu && k == 4 && (c->tb_variant == 8 || c->tb_variant == 10)) {
-        *tx = 64 - 2 * hx; *ty = 24 - 2 * k;               // x-pair layouts (k_xp.cuh)
-    } else if (tma && neu && k <= 5) {
+    if (tma && neu && k <= 5) {
         *tx = 32 - 2 * hx; *ty = 32 - 2 * k;               // 16 warps x RY = 2
     } else if (tma && !neu && k <= 4) {
         *tx = 32 - 2 * hx; *ty = 48 - 2 * k;               // 24 warps x RY = 2

@@ -35,7 +35,7 @@ struct StMaps {
 template <int ND>
 __global__ void __launch_bounds__(st::NW * 32, 3) k_stencil_tma(
     const __grid_constant__ StMaps maps, double* __restrict__ out, int nx, int ny, int kb, int ke,
-    int zc, double h2inv, dd* __restrict__ part, const DevState* __restrict__ st)
+    int zch, double h2inv, dd* __restrict__ part, const DevState* __restrict__ st)
 {
     using namespace st;
     if (st && st->done) return;
@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(st::NW * 32, 3) k_stencil_tma(
     uint64_t* bar = reinterpret_cast<uint64_t*>(smb + NS * SLOT);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int x0 = blockIdx.x * TXO, y0 = blockIdx.y * TYO;
-    const int k0 = kb + blockIdx.z * zc, k1 = min(ke, k0 + zc);
+    const int k0 = kb + blockIdx.z * zch, k1 = min(ke, k0 + zch);
     // step s (0-based) consumes v planes k0-1+s .. k0+1+s and a plane k0+s; slot s % NS
     // receives v plane k0+1+s and a plane k0+s (plane k0-1 and k0 arrive in the prologue)
     const int nsteps = k1 - k0;

@@ -5,7 +5,6 @@
 #include <atomic>
 
 #include "ctx.cuh"
-#include "k_xp.cuh"
 
 namespace fused {
 
@@ -131,24 +130,6 @@ bcgs_status launch_tb4_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
     return BCGS_OK;
 }
 
-template <int K, int RY, int NW, int NS, int MODE>
-bcgs_status launch_xp_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
-{
-    using S = XpShape<K, RY, NW, NS>;
-    static_assert(S::smem <= 227 * 1024, "xp shared memory budget");
-    auto kern = k_cheb_xp<K, RY, NW, NS, MODE>;
-    static std::atomic<uint64_t> attr_dev{0};
-    TRY(ensure_smem_attr(c, kern, S::smem, attr_dev));
-    TbMaps maps;
-    if (!make_maps(c, &maps, a, MODE, S::EY, S::EX))
-        return fail(c, BCGS_E_CUDA, "cuTensorMapEncodeTiled failed");
-    dim3 grid((unsigned)((a.nx + S::TX - 1) / S::TX), (unsigned)((a.ny + S::TY - 1) / S::TY),
-              (unsigned)nchunk_total);
-    kern<<<grid, NW * 32, S::smem, c->s>>>(a, maps);
-    CUDA_OK(c, cudaGetLastError());
-    return BCGS_OK;
-}
-
 // Kernel layout per degree: k <= 4 the TMA warp-row kernel with 24 warps
 // (BCGS_OPT_TB_VARIANT 7, default); Neumann faces the 16-warp TMA kernel with mirror ghosts
 // (k <= 5); otherwise (odd nx: no TMA, variant 2, one-pass k = 5..8) the square tile.
@@ -161,10 +142,6 @@ bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz)
                 return launch_tb4_k<K, 2, 16, 4, MODE, true>(c, a, nz);
         }
         return launch_tb_k<K, MODE, true>(c, a, nz);
-    }
-    if constexpr (K == 4) {   // x-pair layouts (k_xp.cuh): 8 = 12 warps x RY 2, 10 = 24 x 1
-        if (c->tb_variant == 8 && tma_ok(c)) return launch_xp_k<K, 2, 12, 3, MODE>(c, a, nz);
-        if (c->tb_variant == 10 && tma_ok(c)) return launch_xp_k<K, 1, 24, 3, MODE>(c, a, nz);
     }
     if constexpr (K <= 4) {   // register budget of the 24-warp layout
         if (c->tb_variant != 2 && tma_ok(c)) return launch_tb4_k<K, 2, 24, 3, MODE>(c, a, nz);
