@@ -127,6 +127,11 @@ typedef enum {
                                /* stencil that follows it; linear preconditioners only;   */
                                /* six more fields (library-owned).  Same iterates as Alg. 3 */
                                /* in exact arithmetic; the oracle implements the same flag */
+    BCGS_OPT_TB_SCHEDULE = 15, /* work split of the temporally blocked kernel (24-warp TMA */
+                               /* layout): 0 = auto (default: segments where a wave cost  */
+                               /* model gains >= 10 %), 1 = tile x z-chunk grid, 2 = one  */
+                               /* CTA per SM, each an equal share of the tile-major work  */
+                               /* (DESIGN.md §4).  Bitwise the same results               */
     BCGS_OPT_STENCIL = 14      /* stencil+dot kernels of a4 / a9: 1 = TMA-staged z-march  */
                                /* (default; Dirichlet faces, even nx; planes per CTA from */
                                /* a wave cost model), v >= 2 = TMA with v planes per CTA  */

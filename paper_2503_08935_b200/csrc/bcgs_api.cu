@@ -1207,6 +1207,10 @@ bcgs_status bcgs_set_option(bcgs_ctx c, int32_t option, int64_t value)
     case BCGS_OPT_ABLATE: c->ablate = (int)(value & 3); break;
     case BCGS_OPT_SYNC2: c->sync2_opt = (int)value; drop_graph(c); break;
     case BCGS_OPT_EXACT_DOT: c->exact_opt = value ? 1 : 0; break;
+    case BCGS_OPT_TB_SCHEDULE:
+        if (value < 0 || value > 2) return fail(c, BCGS_E_INVALID, "tb schedule %lld: 0..2", (long long)value);
+        c->tb_schedule = (int)value;
+        break;
     case BCGS_OPT_STENCIL:
         if (value < 0 || value > 4096) return fail(c, BCGS_E_INVALID, "stencil option %lld", (long long)value);
         c->stencil_tma = (int)value;

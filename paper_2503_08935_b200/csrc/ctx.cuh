@@ -152,6 +152,7 @@ struct bcgs_ctx_s {
     long long *limbs = nullptr, *glimbs = nullptr;   // R19 exact path (xdot.cuh)
     const double* src[9][10] = {};   // operand pairs of each reduction stage (exact path)
     int exact_opt = 0;               // BCGS_OPT_EXACT_DOT
+    int tb_schedule = 0;             // BCGS_OPT_TB_SCHEDULE: 0 auto, 1 chunk grid, 2 segments
     int stencil_tma = 1;             // BCGS_OPT_STENCIL: TMA-staged stencil+dot (st_tma.cu);
                                      // >= 2: fixed planes per CTA
     int pipelined_opt = 0, pipelined = 0;   // BCGS_OPT_PIPELINED (option / active solve)

@@ -140,25 +140,25 @@ __device__ __forceinline__ void combine_partials(const dd* __restrict__ part, in
 #pragma unroll
     for (int d = 0; d < ND; ++d) { p[d] = 0.0; m[d] = 0.0; s[d] = 0.0; ab[d] = 0.0; }
     const int T = blockDim.x;
-    int b = threadIdx.x;
-    for (; b + 7 * T < nparts; b += 8 * T) {
+    // up to 8 partials per thread in flight (a ragged last group is predicated, not a
+    // serial tail of dependent loads); the adds keep the order b, b + T, b + 2T, ...
+    for (int b = threadIdx.x; b < nparts; b += 8 * T) {
         dd v[8][ND];
 #pragma unroll
         for (int u = 0; u < 8; ++u)
 #pragma unroll
-            for (int d = 0; d < ND; ++d) v[u][d] = part[(int64_t)(b + u * T) * ND + d];
+            for (int d = 0; d < ND; ++d)
+                v[u][d] = b + u * T < nparts ? part[(int64_t)(b + u * T) * ND + d]
+                                             : dd{0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int u = 0; u < 8; ++u)
+            if (b + u * T < nparts) {
 #pragma unroll
-            for (int d = 0; d < ND; ++d)
-                dd_add(p[d], m[d], s[d], ab[d], v[u][d].hi, v[u][d].mid, v[u][d].lo, v[u][d].ab);
+                for (int d = 0; d < ND; ++d)
+                    dd_add(p[d], m[d], s[d], ab[d], v[u][d].hi, v[u][d].mid, v[u][d].lo,
+                           v[u][d].ab);
+            }
     }
-    for (; b < nparts; b += T)
-#pragma unroll
-        for (int d = 0; d < ND; ++d) {
-            const dd v = part[(int64_t)b * ND + d];
-            dd_add(p[d], m[d], s[d], ab[d], v.hi, v.mid, v.lo, v.ab);
-        }
     block_reduce_dd<ND>(p, m, s, ab, res);
     __syncthreads();
 }

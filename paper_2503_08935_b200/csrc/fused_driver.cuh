@@ -97,6 +97,21 @@ bcgs_status launch_tb(bcgs_ctx c, TbArgs& a)
     a.zch = (int)((a.Lb + best_n - 1) / best_n);
     a.nchunk = (a.Lb + a.zch - 1) / a.zch;
     const int nz = a.nchunk * nblk;
+    // segment mode: one CTA per SM, each an equal share of the tile-major (tile, plane)
+    // work (parts pay 2k warm-up / drain planes each).  Used only where it beats the chunk
+    // grid by >= 10 %: tile counts that do not fill the SMs (256^3: 77 tiles -> ~150 vs
+    // 180 plane-steps per SM).  On deep grids the chunk grid keeps neighbouring tiles at
+    // the same plane, so their recomputed halo boxes are still in L2 (measured).
+    a.nseg = 0;
+    const bool tb4 = c->tb_variant != 2 && tb_tma_ok(c) && !neu && k <= 4 && !a.ext;
+    if (tb4) {
+        const int64_t per = (tiles * a.Lb + kNumSMs - 1) / kNumSMs;
+        const double seg = (double)per + 2.0 * k * (double)((per + a.Lb - 1) / a.Lb + 1);
+        if (c->tb_schedule == 2 || (c->tb_schedule == 0 && seg < 0.9 * best)) {
+            a.nseg = kNumSMs;
+            a.nblk = nblk;
+        }
+    }
     switch (k) {
     case 1: return launch_variant<1, MODE>(c, a, nz);
     case 2: return launch_variant<2, MODE>(c, a, nz);

@@ -3,6 +3,7 @@
 #pragma once
 namespace fused {
 bool stencil_tma_ok(bcgs_ctx c);   // st_tma.cu
+bool tb_tma_ok(bcgs_ctx c);        // st_tma.cu: k_cheb_tb4 usable (segment mode)
 template <int ND>
 bcgs_status launch_stencil_tma(bcgs_ctx c, const double* v, const double* a, double* out,
                                int kb, int ke, dd* part, int* nparts);

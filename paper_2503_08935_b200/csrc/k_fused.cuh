@@ -42,6 +42,10 @@ struct TbArgs {
     // wrote (qsel = 1: selected by the iteration parity like side_a/side_b)
     int qsel;
     int nx, ny, Lb, zch, nchunk;
+    // segment mode (nseg > 0, k_cheb_tb4 only): a 1-D grid of nseg CTAs, each owning an
+    // equal share of the tile-major (tile x, tile y, block, plane) work -- balances tile
+    // counts that do not fill the SMs (256^3: 77 tiles on 148 SMs); 0 = the 3-D grid
+    int nseg, ntx, nty, nblk;
     // extended-slab mode (G(CI), ext = 1): zero ghosts outside planes [zv0, zv1), outputs
     // for planes [zo0, zo1) only, one block; plane indices are extended-slab indices.
     int ext, zv0, zv1, zo0, zo1;

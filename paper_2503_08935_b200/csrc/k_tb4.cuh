@@ -306,13 +306,110 @@ struct Tb4Thread {
     }
 };
 
-template <int K, int RY, int NW, int NS, int MODE, bool NEU = false, bool O2 = false>
+// One (tile, slab block, output planes [c0, c1)) part of the launch: tile geometry and
+// masks, the TMA prologue and the z-march.  `again`: a later part of the same CTA (segment
+// mode) -- the stage barriers are re-armed at phase 0 (every plane issued by the previous
+// part was consumed, and all threads passed its last step's barrier); the register rings
+// and level planes keep the previous part's finite values, which only reach the warm-up
+// cone of planes below c0, never an output (same as a chunk start inside a block) -- except
+// the level-0 ring at a block start, whose planes below b0 are the zero ghosts (reset).
+template <int K, int RY, int NW, int NS, int MODE, bool NEU, bool O2>
+__device__ __forceinline__ void tb4_part(Tb4Thread<K, RY, NW, NS, MODE, NEU, O2>& th,
+                                         const TbArgs& a, int bx, int by, int blk, int c0,
+                                         int c1, bool again)
+{
+    using S = Tb4Shape<K, RY, NW, NS>;
+    constexpr int TX = S::TX, TY = S::TY, U = S::QW, HX = S::HX;
+    const int lane = th.lane;
+    th.tx0 = bx * TX - HX;
+    th.ty0 = by * TY - K;
+    const int gx = th.tx0 + lane;
+    const int dx = max(HX - lane, lane - (HX + TX - 1));
+    int wdy = 1 << 20;
+    th.mir = ((gx == 0 && (a.bc.m & 1)) ? 1 : 0) | ((gx == a.nx - 1 && (a.bc.m & 2)) ? 2 : 0);
+#pragma unroll
+    for (int r = 0; r < RY; ++r) {
+        const int ey = th.ey0 + r;
+        const int gy = th.ty0 + ey;
+        const int dy = max(K - ey, ey - (K + TY - 1));
+        wdy = min(wdy, dy);
+        const int dist = max(dx, dy);
+        th.in_dom[r] = gx >= 0 && gx < a.nx && gy >= 0 && gy < a.ny;
+        th.in_tile[r] = th.in_dom[r] && dist <= 0;
+        if (gy == 0 && (a.bc.m & 4)) th.mir |= 4 << (2 * r);
+        if (gy == a.ny - 1 && (a.bc.m & 8)) th.mir |= 8 << (2 * r);
+        th.col[r] = th.in_dom[r] ? (uint32_t)(gx + a.nx * gy) : 0u;
+        unsigned msk = 0;
+#pragma unroll
+        for (int j = 1; j <= K; ++j)
+            if (th.in_dom[r] && dist <= K - j) msk |= 1u << j;
+        th.actmask[r] = msk;
+    }
+    th.wdy = wdy;
+    th.b0 = a.ext ? a.zv0 : blk * a.Lb;
+    th.b1 = a.ext ? a.zv1 : th.b0 + a.Lb;
+    th.c0 = c0;
+    th.c1 = c1;
+    th.t0 = max(th.b0, th.c0 - K);
+    th.t1 = th.c1 - 1 + K;
+    if (again && th.t0 == th.b0) {
+        // a part starting at its block's first plane: the level-0 ring stands for the zero
+        // ghost planes below the block (R8 block cut) -- reset it as at kernel start (the
+        // previous part's values would enter level 1 at plane b0 as its z- neighbour)
+#pragma unroll
+        for (int d = 0; d < S::QW; ++d)
+#pragma unroll
+            for (int r = 0; r < RY; ++r) {
+                th.qw[d][r] = 0.0;
+                if (MODE == MODE_C) th.qr[d][r] = 0.0;
+            }
+#pragma unroll
+        for (int r = 0; r < RY; ++r) th.y2c[r] = 0.0;
+    }
+    if (again) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int s = 0; s < NS; ++s) mbar_init(&th.bar[s], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int tt = th.t0; tt < th.t0 + NS && tt < th.b1 && tt <= th.t1; ++tt) th.issue(tt);
+
+    // interior tile: the extended tile lies inside the grid -> masks only near block ends
+    const bool interior = th.tx0 >= 0 && th.tx0 + 32 <= a.nx && th.ty0 >= 0 &&
+                          th.ty0 + S::EY <= a.ny;
+    const int nsteps = th.t1 - th.t0 + 1;
+    const int NB = nsteps / U, tail = nsteps - NB * U;
+    int t = th.t0;
+    if (interior) {
+        // masked prologue while a level's plane is below the block (t - K < b0), masked
+        // epilogue once planes beyond the block appear (t >= b1); unmasked in between.
+        const int pro_end = max(th.t0, th.b0 + K + (NEU ? 1 : 0));   // first unmasked step
+        const int epi_beg = min(th.t1 + 1, th.b1);          // first step that must be masked
+        const int npro = min(NB, (pro_end - th.t0 + U - 1) / U);
+        th.template run_blocks<true>(t, npro);
+        t += npro * U;
+        const int nmid = max(0, min(NB - npro, (epi_beg - t) / U));
+        th.template run_blocks<false>(t, nmid);
+        t += nmid * U;
+        th.template run_blocks<true>(t, NB - npro - nmid);
+        t += (NB - npro - nmid) * U;
+    } else {
+        th.template run_blocks<true>(t, NB);
+        t += NB * U;
+    }
+    th.run_tail(t, tail);
+}
+
+template <int K, int RY, int NW, int NS, int MODE, bool NEU = false, bool O2 = false,
+          bool SEG = false>
 __global__ void __launch_bounds__(NW * 32, 1) k_cheb_tb4(const __grid_constant__ TbArgs a,
                                                     const __grid_constant__ TbMaps maps)
 {
     using T = Tb4Thread<K, RY, NW, NS, MODE, NEU, O2>;
     using S = Tb4Shape<K, RY, NW, NS>;
-    constexpr int TX = S::TX, TY = S::TY, U = S::QW;
     extern __shared__ __align__(128) double smraw[];
 
     const DevState* st = a.st;
@@ -341,44 +438,27 @@ __global__ void __launch_bounds__(NW * 32, 1) k_cheb_tb4(const __grid_constant__
         const bool odd = st && (st->iter & 1);
         th.pmap = !a.qsel ? &maps.r : odd ? &maps.pa : &maps.pb;
     }
-    const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
-    th.lane = lane;
-    th.ey0 = wy * RY;
-    constexpr int HX = S::HX;
-    th.tx0 = (int)blockIdx.x * TX - HX;
-    th.ty0 = blockIdx.y * TY - K;
-    const int gx = th.tx0 + lane;
-    const int dx = max(HX - lane, lane - (HX + TX - 1));
-    int wdy = 1 << 20;
-    th.mir = ((gx == 0 && (a.bc.m & 1)) ? 1 : 0) | ((gx == a.nx - 1 && (a.bc.m & 2)) ? 2 : 0);
-#pragma unroll
-    for (int r = 0; r < RY; ++r) {
-        const int ey = th.ey0 + r;
-        const int gy = th.ty0 + ey;
-        const int dy = max(K - ey, ey - (K + TY - 1));
-        wdy = min(wdy, dy);
-        const int dist = max(dx, dy);
-        th.in_dom[r] = gx >= 0 && gx < a.nx && gy >= 0 && gy < a.ny;
-        th.in_tile[r] = th.in_dom[r] && dist <= 0;
-        if (gy == 0 && (a.bc.m & 4)) th.mir |= 4 << (2 * r);
-        if (gy == a.ny - 1 && (a.bc.m & 8)) th.mir |= 8 << (2 * r);
-        th.col[r] = th.in_dom[r] ? (uint32_t)(gx + a.nx * gy) : 0u;
-        unsigned msk = 0;
-#pragma unroll
-        for (int j = 1; j <= K; ++j)
-            if (th.in_dom[r] && dist <= K - j) msk |= 1u << j;
-        th.actmask[r] = msk;
-    }
-    th.wdy = wdy;
-    const int blk = blockIdx.z / a.nchunk, ch = blockIdx.z % a.nchunk;
-    th.b0 = a.ext ? a.zv0 : blk * a.Lb;
-    th.b1 = a.ext ? a.zv1 : th.b0 + a.Lb;
-    th.c0 = (a.ext ? a.zo0 : th.b0) + ch * a.zch;
-    th.c1 = min(a.ext ? a.zo1 : th.b1, th.c0 + a.zch);
-    if (th.c0 >= (a.ext ? a.zo1 : th.b1)) return;
-    th.t0 = max(th.b0, th.c0 - K);
-    th.t1 = th.c1 - 1 + K;
+    th.lane = threadIdx.x & 31;
+    th.ey0 = (threadIdx.x >> 5) * RY;
     th.plane = (uint32_t)(a.nx * a.ny);
+    // output planes of a tile-block: the block, or the extended slab's output window
+    const int zlo = a.ext ? a.zo0 : 0, Lo = a.ext ? a.zo1 - a.zo0 : a.Lb;
+    int bx = blockIdx.x, by = blockIdx.y, blk = 0, c0 = 0, c1 = 0;
+    int64_t u = 0, u1 = 0;
+    if (!SEG) {          // grid mode: blockIdx = (tile x, tile y, block * nchunk + chunk)
+        blk = blockIdx.z / a.nchunk;
+        const int ch = blockIdx.z % a.nchunk;
+        const int lo = a.ext ? zlo : blk * a.Lb;
+        c0 = lo + ch * a.zch;
+        c1 = min(lo + Lo, c0 + a.zch);
+        if (c0 >= lo + Lo) return;
+    } else {             // segment mode: CTA i owns [i T / nseg, (i+1) T / nseg) of the
+                         // tile-major (tile x, tile y, block, plane) order, T = tiles x Lo
+        const int64_t T = (int64_t)a.ntx * a.nty * (a.ext ? 1 : a.nblk) * Lo;
+        u = T * blockIdx.x / a.nseg;
+        u1 = T * (blockIdx.x + 1) / a.nseg;
+        if (u >= u1) return;
+    }
 #pragma unroll
     for (int d = 0; d < S::QW; ++d)
 #pragma unroll
@@ -398,33 +478,21 @@ __global__ void __launch_bounds__(NW * 32, 1) k_cheb_tb4(const __grid_constant__
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (threadIdx.x == 0)
-        for (int tt = th.t0; tt < th.t0 + NS && tt < th.b1 && tt <= th.t1; ++tt) th.issue(tt);
-
-    // interior tile: the extended tile lies inside the grid -> masks only near block ends
-    const bool interior = th.tx0 >= 0 && th.tx0 + 32 <= a.nx && th.ty0 >= 0 &&
-                          th.ty0 + S::EY <= a.ny;
-    const int nsteps = th.t1 - th.t0 + 1;
-    const int NB = nsteps / U, tail = nsteps - NB * U;
-    int t = th.t0;
-    if (interior) {
-        // masked prologue while a level's plane is below the block (t - K < b0), masked
-        // epilogue once planes beyond the block appear (t >= b1); unmasked in between.
-        const int pro_end = max(th.t0, th.b0 + K + (NEU ? 1 : 0));   // first unmasked step
-        const int epi_beg = min(th.t1 + 1, th.b1);          // first step that must be masked
-        const int npro = min(NB, (pro_end - th.t0 + U - 1) / U);
-        th.template run_blocks<true>(t, npro);
-        t += npro * U;
-        const int nmid = max(0, min(NB - npro, (epi_beg - t) / U));
-        th.template run_blocks<false>(t, nmid);
-        t += nmid * U;
-        th.template run_blocks<true>(t, NB - npro - nmid);
-        t += (NB - npro - nmid) * U;
-    } else {
-        th.template run_blocks<true>(t, NB);
-        t += NB * U;
+    if (!SEG) {
+        tb4_part(th, a, bx, by, blk, c0, c1, false);
+        return;
     }
-    th.run_tail(t, tail);
+    for (bool again = false; u < u1; again = true) {
+        const int64_t w = u / Lo;
+        const int z0 = (int)(u - w * Lo);
+        const int z1 = (u1 - u) < (int64_t)(Lo - z0) ? z0 + (int)(u1 - u) : Lo;
+        bx = (int)(w % a.ntx);
+        by = (int)((w / a.ntx) % a.nty);
+        blk = (int)(w / ((int64_t)a.ntx * a.nty));
+        const int lo = a.ext ? zlo : blk * a.Lb;
+        tb4_part(th, a, bx, by, blk, lo + z0, lo + z1, again);
+        u += z1 - z0;
+    }
 }
 
 }  // namespace fused

@@ -139,6 +139,9 @@ __global__ void __launch_bounds__(st::NW * 32, 3) k_stencil_tma(
     }
 }
 
+// the TMA-fed Chebyshev kernel (k_tb4.cuh) can run this context's slab (segment mode)
+bool tb_tma_ok(bcgs_ctx c) { return tma_ok(c); }
+
 // capability: Dirichlet faces, nx even (16-byte rows), 32-bit-safe maps
 bool stencil_tma_ok(bcgs_ctx c)
 {

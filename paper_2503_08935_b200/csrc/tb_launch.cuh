@@ -34,6 +34,7 @@ template <> struct Tile<8> { static constexpr int X = 16, Y = 8; };
 template <int K, int MODE, bool NEU = false>
 bcgs_status launch_tb_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
 {
+    if (a.nseg) return fail(c, BCGS_E_STATE, "segment mode needs the TMA kernel");
     constexpr int TX = Tile<K>::X, TY = Tile<K>::Y;
     using S = TbShape<K, TX, TY>;
     auto kern = k_cheb_tb<K, TX, TY, MODE, NEU>;
@@ -112,12 +113,14 @@ inline bool make_maps(bcgs_ctx c, TbMaps* maps, const TbArgs& a, int mode, int b
     return ok;
 }
 
-template <int K, int RY, int NW, int NS, int MODE, bool NEU = false, bool O2 = false>
+template <int K, int RY, int NW, int NS, int MODE, bool NEU = false, bool O2 = false,
+          bool SEG = false>
 bcgs_status launch_tb4_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
 {
     using S = Tb4Shape<K, RY, NW, NS>;
     static_assert(S::smem <= 227 * 1024, "tb4 shared memory budget");
-    auto kern = k_cheb_tb4<K, RY, NW, NS, MODE, NEU, O2>;
+    if (a.nseg > 0 && !SEG) return fail(c, BCGS_E_STATE, "segment mode: wrong kernel instance");
+    auto kern = k_cheb_tb4<K, RY, NW, NS, MODE, NEU, O2, SEG>;
     static std::atomic<uint64_t> attr_dev{0};
     TRY(ensure_smem_attr(c, kern, S::smem, attr_dev));
     TbMaps maps;
@@ -125,6 +128,11 @@ bcgs_status launch_tb4_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
         return fail(c, BCGS_E_CUDA, "cuTensorMapEncodeTiled failed");
     dim3 grid((unsigned)((a.nx + S::TX - 1) / S::TX), (unsigned)((a.ny + S::TY - 1) / S::TY),
               (unsigned)nchunk_total);
+    if (a.nseg > 0) {   // segment mode (launch_tb): a 1-D grid over the tile-major work
+        a.ntx = (int)grid.x;
+        a.nty = (int)grid.y;
+        grid = dim3((unsigned)a.nseg, 1, 1);
+    }
     kern<<<grid, NW * 32, S::smem, c->s>>>(a, maps);
     CUDA_OK(c, cudaGetLastError());
     return BCGS_OK;
@@ -144,7 +152,10 @@ bcgs_status launch_variant(bcgs_ctx c, TbArgs& a, int nz)
         return launch_tb_k<K, MODE, true>(c, a, nz);
     }
     if constexpr (K <= 4) {   // register budget of the 24-warp layout
-        if (c->tb_variant != 2 && tma_ok(c)) return launch_tb4_k<K, 2, 24, 3, MODE>(c, a, nz);
+        if (c->tb_variant != 2 && tma_ok(c)) {
+            if (a.nseg > 0) return launch_tb4_k<K, 2, 24, 3, MODE, false, false, true>(c, a, nz);
+            return launch_tb4_k<K, 2, 24, 3, MODE>(c, a, nz);
+        }
     }
     return launch_tb_k<K, MODE>(c, a, nz);
 }

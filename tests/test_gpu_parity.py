@@ -328,6 +328,45 @@ def test_tb_variants_bitwise(bc, orc, variant, k):
     assert np.array_equal(out, orc.apply_cheb(q, h, 2, k, ivl[0], ivl[1]))
 
 
+@pytest.mark.parametrize("n3,bpr,k", [((70, 52, 40), 2, 4), ((132, 90, 33), 1, 3),
+                                      ((64, 200, 48), 3, 2)])
+def test_tb_segment_schedule_bitwise(bc, orc, n3, bpr, k):
+    """Segment scheduling of the temporally blocked kernel (BCGS_OPT_TB_SCHEDULE = 2: one CTA
+    per SM, parts spanning tile and block boundaries) gives the oracle's Chebyshev
+    application and iterates bitwise (p-update + M^-1 p, s-update + M^-1 s)."""
+    h = si.unit_cube_h(n3[0])
+    s = bc.Solver(n3, h)
+    s.set_option(bc.OPT_TB_SCHEDULE, 2)
+    s.set_preconditioner("gnocomm", k, blocks_per_rank=bpr)
+    q = np.random.default_rng(11).standard_normal(n3[::-1])
+    ivl = orc.pc_interval(n3[::-1], h, bpr, "gnocomm")
+    assert np.array_equal(host(s.apply_preconditioner(dev(q))),
+                          orc.apply_cheb(q, h, bpr, k, ivl[0], ivl[1]))
+    s.set_rhs_random(si.SEED)
+    rep = s.solve(fixed_iters=12)
+    o = orc.bicgstab(orc.rhs_random(n3[::-1], si.SEED), h, pc="gnocomm", k=k, nslab=bpr,
+                     fixed_it=12)
+    assert rep["iterations"] == o.iterations == 12
+    assert np.array_equal(s.residual_history(), o.history)
+    assert np.array_equal(host(s.solution()), o.x)
+    s.close()
+
+
+def test_c2_256_segment_schedule_bitwise(bc, orc):
+    """Config C2 (256³, k = 4, one GPU) runs the segment schedule by default (77 tiles on 148
+    SMs); first 5 iterations bitwise equal to the oracle's."""
+    n = 256
+    h = si.unit_cube_h(n)
+    s = bc.Solver(n, h)
+    s.set_preconditioner("gnocomm", 4)
+    s.set_rhs_random(si.SEED)
+    rep = s.solve(fixed_iters=5)
+    o = orc.bicgstab(orc.rhs_random((n, n, n), si.SEED), h, pc="gnocomm", k=4, fixed_it=5)
+    assert np.array_equal(s.residual_history(), o.history)
+    assert np.array_equal(host(s.solution()), o.x)
+    s.close()
+
+
 def test_unpreconditioned_streaming_path(bc, orc):
     """M = I on the fused path: no p̂ / r̂ copies (no precond_sweep launches), bitwise oracle."""
     n = 48
