@@ -127,6 +127,13 @@ typedef enum {
                                /* stencil that follows it; linear preconditioners only;   */
                                /* six more fields (library-owned).  Same iterates as Alg. 3 */
                                /* in exact arithmetic; the oracle implements the same flag */
+    BCGS_OPT_PDL = 16,         /* 1 = consecutive kernels of an iteration use programmatic */
+                               /* dependent launch (one rank, NCCL / p2p off, not while    */
+                               /* profiling): the next kernel is launched as soon as every */
+                               /* CTA of its predecessor has exited and waits for the      */
+                               /* predecessor's completion; 0 = ordinary launches (default: */
+                               /* graph replay already hides the launch gaps)*/
+                               /* Bitwise the same results                                 */
     BCGS_OPT_TB_SCHEDULE = 15, /* work split of the temporally blocked kernel (24-warp TMA */
                                /* layout): 0 = auto (default: segments where a wave cost  */
                                /* model gains >= 10 %), 1 = tile x z-chunk grid, 2 = one  */

@@ -24,7 +24,7 @@ PC = {"none": 0, "gnocomm": 1, "bj": 2, "g": 3, "bj_bicgs": 4, "g_bicgs": 5}
 MEM_DEVICE, MEM_HOST = 0, 1
 OPT_KERNELS, OPT_GRAPH, OPT_PROFILE, OPT_POLL, OPT_TB_VARIANT = 0, 1, 2, 3, 4
 OPT_MULTIPASS, OPT_ABLATE, OPT_SYNC2, OPT_EXACT_DOT, OPT_COMM_TIMEOUT = 8, 9, 10, 11, 12
-OPT_PIPELINED, OPT_STENCIL, OPT_TB_SCHEDULE = 13, 14, 15
+OPT_PIPELINED, OPT_STENCIL, OPT_TB_SCHEDULE, OPT_PDL = 13, 14, 15, 16
 HIST_CAP = 16384
 MAX_DEGREE = 64
 

@@ -419,9 +419,9 @@ bcgs_status reduce(bcgs_ctx c, int nparts, int stage, int depth, int k3_mask,
     const bool gather = c->nranks > 1 || c->comm;
     {
         Prof pf(c, KC_FINALIZE, 0.0);
-        k_finalize<ND><<<1, 1024, 0, c->s>>>(c->part, nparts, stage, c->st, c->hist, c->scal,
-                                              c->rank_out, gather ? 2 : 1, depth, nprod,
-                                              self_mask, k3_mask);
+        CUDA_OK(c, launch_k(c, k_finalize<ND>, dim3(1), dim3(1024), 0, (const dd*)c->part,
+                            nparts, stage, c->st, c->hist, c->scal, c->rank_out,
+                            gather ? 2 : 1, depth, nprod, self_mask, k3_mask));
     }
     if (gather) {
         TRY(allgather_pairs(c, ND));
@@ -1207,6 +1207,7 @@ bcgs_status bcgs_set_option(bcgs_ctx c, int32_t option, int64_t value)
     case BCGS_OPT_ABLATE: c->ablate = (int)(value & 3); break;
     case BCGS_OPT_SYNC2: c->sync2_opt = (int)value; drop_graph(c); break;
     case BCGS_OPT_EXACT_DOT: c->exact_opt = value ? 1 : 0; break;
+    case BCGS_OPT_PDL: c->pdl = value ? 1 : 0; break;
     case BCGS_OPT_TB_SCHEDULE:
         if (value < 0 || value > 2) return fail(c, BCGS_E_INVALID, "tb schedule %lld: 0..2", (long long)value);
         c->tb_schedule = (int)value;

@@ -152,6 +152,8 @@ struct bcgs_ctx_s {
     long long *limbs = nullptr, *glimbs = nullptr;   // R19 exact path (xdot.cuh)
     const double* src[9][10] = {};   // operand pairs of each reduction stage (exact path)
     int exact_opt = 0;               // BCGS_OPT_EXACT_DOT
+    int pdl = 0;                     // BCGS_OPT_PDL: programmatic dependent launches (off:
+                                     // measured no gain over graph replay)
     int tb_schedule = 0;             // BCGS_OPT_TB_SCHEDULE: 0 auto, 1 chunk grid, 2 segments
     int stencil_tma = 1;             // BCGS_OPT_STENCIL: TMA-staged stencil+dot (st_tma.cu);
                                      // >= 2: fixed planes per CTA
@@ -235,6 +237,36 @@ inline bcgs_status fail(bcgs_ctx c, bcgs_status s, const char* fmt, ...)
         if (r_ != ncclSuccess)                                                              \
             return fail((c), BCGS_E_NCCL, "%s failed: %s", #call, ncclGetErrorString(r_)); \
     } while (0)
+
+// PDL chain (BCGS_OPT_PDL): one rank, no transport kernels or host waits in between, no
+// profiling events
+inline bool pdl_active(bcgs_ctx c)
+{
+    return c->pdl && c->nranks == 1 && !c->p2p && !c->comm && !c->profile;
+}
+
+// Launch a kernel that begins with pdl_enter(): with programmatic stream serialization
+// when the PDL chain is active, as an ordinary launch otherwise.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(bcgs_ctx c, void (*kern)(KArgs...), dim3 grid, dim3 block,
+                            size_t smem, Args&&... args)
+{
+    if (!pdl_active(c)) {
+        kern<<<grid, block, smem, c->s>>>(std::forward<Args>(args)...);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 inline double* F(bcgs_ctx c, int v) { return c->vec[v]; }
 inline bool inner_pc(bcgs_ctx c) { return c->pc == BCGS_PC_BJ_BICGS || c->pc == BCGS_PC_G_BICGS; }

@@ -140,18 +140,20 @@ __device__ __forceinline__ void combine_partials(const dd* __restrict__ part, in
 #pragma unroll
     for (int d = 0; d < ND; ++d) { p[d] = 0.0; m[d] = 0.0; s[d] = 0.0; ab[d] = 0.0; }
     const int T = blockDim.x;
-    // up to 8 partials per thread in flight (a ragged last group is predicated, not a
-    // serial tail of dependent loads); the adds keep the order b, b + T, b + 2T, ...
-    for (int b = threadIdx.x; b < nparts; b += 8 * T) {
-        dd v[8][ND];
+    // U partials per thread in flight (a ragged last group is predicated, not a serial tail
+    // of dependent loads; U x ND quadruples stay within the 64-register budget of a
+    // 1024-thread CTA); the adds keep the order b, b + T, b + 2T, ...
+    constexpr int U = ND >= 4 ? 1 : 4 / ND;
+    for (int b = threadIdx.x; b < nparts; b += U * T) {
+        dd v[U][ND];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < U; ++u)
 #pragma unroll
             for (int d = 0; d < ND; ++d)
                 v[u][d] = b + u * T < nparts ? part[(int64_t)(b + u * T) * ND + d]
                                              : dd{0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < U; ++u)
             if (b + u * T < nparts) {
 #pragma unroll
                 for (int d = 0; d < ND; ++d)

@@ -333,10 +333,12 @@ a11:
     {
         Prof pf(c, KC_FUSED_XR, 64.0 * n);
         if (vec)
-            stream::k_update_xr2<2><<<kEwBlocks, 256, 0, c->s>>>(
-                (double2*)F(c, V_X), (const double2*)F(c, V_PH), (const double2*)F(c, V_RH),
-                (const double2*)F(c, V_S), (double2*)F(c, V_R), (const double2*)F(c, V_T),
-                (const double2*)F(c, V_RT), n / 2, c->part, st);
+            CUDA_OK(c, launch_k(c, stream::k_update_xr2<2>, dim3(kEwBlocks), dim3(256), 0,
+                                (double2*)F(c, V_X), (const double2*)F(c, V_PH),
+                                (const double2*)F(c, V_RH), (const double2*)F(c, V_S),
+                                (double2*)F(c, V_R), (const double2*)F(c, V_T),
+                                (const double2*)F(c, V_RT), (int64_t)(n / 2), c->part,
+                                (const DevState*)st));
         else
             k_update_xr_s<<<kEwBlocks, ref::EW_THREADS, 0, c->s>>>(
                 F(c, V_X), F(c, V_PH), F(c, V_RH), F(c, V_S), F(c, V_R), F(c, V_T), F(c, V_RT),

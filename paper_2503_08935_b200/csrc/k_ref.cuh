@@ -286,6 +286,7 @@ __global__ void __launch_bounds__(1024) k_finalize(const dd* __restrict__ part, 
                                                    int depth, double nprod, int self_mask,
                                                    int k3_mask)
 {
+    pdl_enter();
     if (stage != STAGE_SETUP && stage != STAGE_DOT && st->done) return;
     __shared__ dd res[ND];
     combine_partials<ND>(part, nparts, res);

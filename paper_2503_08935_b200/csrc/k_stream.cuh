@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(256) k_update_xr2(double2* __restrict__ x,
                                                     dd* __restrict__ part,
                                                     const DevState* __restrict__ st)
 {
+    pdl_enter();
     if (st->done) return;
     const double alpha = st->alpha, omega = st->omega;
     double p[2] = {0.0, 0.0}, m[2] = {0.0, 0.0}, q[2] = {0.0, 0.0}, ab[2] = {0.0, 0.0};

@@ -412,6 +412,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_cheb_tb4(const __grid_constant__
     using S = Tb4Shape<K, RY, NW, NS>;
     extern __shared__ __align__(128) double smraw[];
 
+    pdl_enter();
     const DevState* st = a.st;
     if (st && st->done) return;
     T th;

@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(st::NW * 32, 3) k_stencil_tma(
     int zch, double h2inv, dd* __restrict__ part, const DevState* __restrict__ st)
 {
     using namespace st;
+    pdl_enter();
     if (st && st->done) return;
     extern __shared__ __align__(128) double smraw[];   // (same declaration as k_tb4.cuh)
     unsigned char* smb = reinterpret_cast<unsigned char*>(smraw);
@@ -201,9 +202,8 @@ bcgs_status launch_stencil_tma(bcgs_ctx c, const double* v, const double* a, dou
     const int zc = stencil_zc(c, (int)((nx + TXO - 1) / TXO) * (int)((ny + TYO - 1) / TYO), ke - kb);
     const dim3 grid((unsigned)((nx + TXO - 1) / TXO), (unsigned)((ny + TYO - 1) / TYO),
                     (unsigned)((ke - kb + zc - 1) / zc));
-    kern<<<grid, NW * 32, SMEM, c->s>>>(maps, out, (int)nx, (int)ny, kb, ke, zc, c->h2inv, part,
-                                        c->st);
-    CUDA_OK(c, cudaGetLastError());
+    CUDA_OK(c, launch_k(c, kern, grid, dim3(NW * 32), SMEM, maps, out, (int)nx, (int)ny, kb, ke,
+                        zc, c->h2inv, part, (const DevState*)c->st));
     *nparts = (int)(grid.x * grid.y * grid.z);
     return BCGS_OK;
 }

@@ -14,6 +14,19 @@
 enum : int32_t { DONE_RUNNING = 0, DONE_OK = 1, DONE_BREAKDOWN = 2, DONE_MAXIT = 3,
                  DONE_PENDING = 4, DONE_COMM_ERROR = 5 };
 
+// Programmatic dependent launch (PDL, DESIGN.md §4 "Launch chain"): a kernel launched with
+// programmatic stream serialization is launched once every CTA of its predecessor has
+// exited (no explicit trigger: dependents that became resident earlier would hold SM
+// resources the predecessor's later CTAs need -- measured slower), before the predecessor's
+// grid completion is processed; it waits here -- before touching any data -- until the
+// predecessor has completed and its memory is visible.  Every kernel the library launches
+// that way calls this first (completion stays transitive along the chain); a no-op for
+// ordinary launches.
+__device__ __forceinline__ void pdl_enter()
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 struct DevState {
     double rho, alpha, omega, beta, nb;
     double den;           // pipelined: the α denominator r~ᵀw + β (r~ᵀS - ω r~ᵀz)

@@ -133,8 +133,7 @@ bcgs_status launch_tb4_k(bcgs_ctx c, TbArgs& a, int nchunk_total)
         a.nty = (int)grid.y;
         grid = dim3((unsigned)a.nseg, 1, 1);
     }
-    kern<<<grid, NW * 32, S::smem, c->s>>>(a, maps);
-    CUDA_OK(c, cudaGetLastError());
+    CUDA_OK(c, launch_k(c, kern, grid, dim3(NW * 32), S::smem, a, maps));
     return BCGS_OK;
 }
 

@@ -352,6 +352,24 @@ def test_tb_segment_schedule_bitwise(bc, orc, n3, bpr, k):
     s.close()
 
 
+@pytest.mark.parametrize("n3,bpr", [((70, 52, 40), 2), ((64, 64, 64), 1)])
+def test_pdl_launch_chain_bitwise(bc, orc, n3, bpr):
+    """BCGS_OPT_PDL = 1 (programmatic dependent launches inside the captured iteration):
+    iterates bitwise equal to the oracle's."""
+    h = si.unit_cube_h(n3[0])
+    s = bc.Solver(n3, h)
+    s.set_option(bc.OPT_PDL, 1)
+    s.set_preconditioner("gnocomm", 4, blocks_per_rank=bpr)
+    s.set_rhs_random(si.SEED)
+    rep = s.solve(tol=1e-8)
+    o = orc.bicgstab(orc.rhs_random(n3[::-1], si.SEED), h, pc="gnocomm", k=4, nslab=bpr,
+                     tol=1e-8)
+    assert rep["converged"] and rep["iterations"] == o.iterations
+    assert np.array_equal(s.residual_history(), o.history)
+    assert np.array_equal(host(s.solution()), o.x)
+    s.close()
+
+
 def test_c2_256_segment_schedule_bitwise(bc, orc):
     """Config C2 (256³, k = 4, one GPU) runs the segment schedule by default (77 tiles on 148
     SMs); first 5 iterations bitwise equal to the oracle's."""
@@ -382,6 +400,18 @@ def test_unpreconditioned_streaming_path(bc, orc):
     assert rep["iterations"] == o.iterations
     assert np.array_equal(s.residual_history(), o.history)
     assert np.array_equal(host(s.solution()), o.x)
+    s.close()
+
+
+def test_schedule_and_stencil_options_validated(bc):
+    """BCGS_OPT_TB_SCHEDULE takes 0..2, BCGS_OPT_STENCIL 0..4096 (>= 2: planes per CTA)."""
+    s, n3, h = make(bc, 16, pc="gnocomm", degree=2)
+    for opt, bad in ((bc.OPT_TB_SCHEDULE, 3), (bc.OPT_TB_SCHEDULE, -1), (bc.OPT_STENCIL, -1),
+                     (bc.OPT_STENCIL, 5000)):
+        with pytest.raises(bc.BcgsError):
+            s.set_option(opt, bad)
+    for opt, good in ((bc.OPT_TB_SCHEDULE, 1), (bc.OPT_STENCIL, 2), (bc.OPT_STENCIL, 0)):
+        s.set_option(opt, good)
     s.close()
 
 

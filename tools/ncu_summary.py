@@ -33,6 +33,8 @@ for row in rows:
             "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
             "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
             "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
+            "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum",
+            "smsp__inst_executed.sum", "smsp__inst_executed_pipe_fp64.sum",
             "l1tex__throughput.avg.pct_of_peak_sustained_active",
             "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
             "lts__throughput.avg.pct_of_peak_sustained_elapsed",

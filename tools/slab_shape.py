@@ -51,6 +51,7 @@ def main():
                     help="BCGS_OPT_STENCIL values to compare (1 = auto chunk, >= 2 planes per CTA)")
     ap.add_argument("--schedule", default="0",
                     help="BCGS_OPT_TB_SCHEDULE values (0 auto, 1 chunk grid, 2 segments)")
+    ap.add_argument("--pdl", default="1", help="BCGS_OPT_PDL values")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -59,13 +60,15 @@ def main():
     h = si.unit_cube_h(n)
     rows = []
     t1 = None
-    combos = [(int(x), int(v), int(g)) for x in a.L.split(",") for v in a.stencil.split(",")
-              for g in a.schedule.split(",")]
-    for L, sv, sched in combos:
+    combos = [(int(x), int(v), int(g), int(q)) for x in a.L.split(",")
+              for v in a.stencil.split(",") for g in a.schedule.split(",")
+              for q in a.pdl.split(",")]
+    for L, sv, sched, pdl in combos:
         P = n // L
         s = bcgs.Solver((n, n, L), h)
         s.set_option(bcgs.OPT_STENCIL, sv)
         s.set_option(bcgs.OPT_TB_SCHEDULE, sched)
+        s.set_option(bcgs.OPT_PDL, pdl)
         s.set_preconditioner("gnocomm", a.degree)
         s.set_rhs_random(si.SEED)
         s.begin(fixed_iters=a.warmup + 2 * a.steps)
@@ -75,11 +78,11 @@ def main():
         kt = s.kernel_times()
         rep = s.finish()
         assert rep["iterations"] == a.warmup + 2 * a.steps, rep
-        if t1 is None and P == 1 and sv == 1 and sched == 0:
+        if t1 is None and P == 1 and sv == 1 and sched == 0 and pdl == 1:
             t1 = ms
         pts = n * n * L
         gbs = 200.0 * pts / (ms * 1e-3) / 1e9
-        row = {"L": L, "P": P, "stencil_opt": sv, "schedule": sched, "ms_per_iter": ms, "alg_gbs": gbs, "frac": gbs / peak,
+        row = {"L": L, "P": P, "stencil_opt": sv, "schedule": sched, "pdl": pdl, "ms_per_iter": ms, "alg_gbs": gbs, "frac": gbs / peak,
                "E_P_compute_bound": (t1 / (P * ms)) if t1 else None,
                "kernel_ms": {k: v["ms"] / a.steps for k, v in kt.items()}}
         rows.append(row)
