@@ -289,7 +289,16 @@ __global__ void __launch_bounds__(1024) k_finalize(const dd* __restrict__ part, 
     pdl_enter();
     if (stage != STAGE_SETUP && stage != STAGE_DOT && st->done) return;
     __shared__ dd res[ND];
-    combine_partials<ND>(part, nparts, res);
+    // the stage's scalar step reads and writes a dozen DevState fields one after another
+    // (one thread): stage a copy in shared memory now -- its loads overlap the partials'
+    // -- and write it back once, instead of a chain of dependent global loads at the end
+    __shared__ DevState sst;
+    constexpr int NW8 = (int)(sizeof(DevState) / 8);
+    static_assert(sizeof(DevState) % 8 == 0, "DevState copied as 8-byte words");
+    if (threadIdx.x < 32)
+        for (int i = threadIdx.x; i < NW8; i += 32)
+            reinterpret_cast<uint64_t*>(&sst)[i] = reinterpret_cast<const uint64_t*>(st)[i];
+    combine_partials<ND>(part, nparts, res);   // ends with __syncthreads
     if (threadIdx.x == 0) {
         if (nranks > 1) {
 #pragma unroll
@@ -302,9 +311,15 @@ __global__ void __launch_bounds__(1024) k_finalize(const dd* __restrict__ part, 
                 dd_add(comb[d].hi, comb[d].mid, comb[d].lo, comb[d].ab, res[d].hi, res[d].mid,
                        res[d].lo, res[d].ab);
             }
-            finish_stage(st, stage, ND, comb, reduce_depth(depth, nparts, 1), nprod, self_mask,
-                         k3_mask, hist, scal);
+            finish_stage(&sst, stage, ND, comb, reduce_depth(depth, nparts, 1), nprod,
+                         self_mask, k3_mask, hist, scal);
         }
+    }
+    if (nranks <= 1) {   // write the updated state back (the only writer while it runs)
+        __syncthreads();
+        if (threadIdx.x < 32)
+            for (int i = threadIdx.x; i < NW8; i += 32)
+                reinterpret_cast<uint64_t*>(st)[i] = reinterpret_cast<const uint64_t*>(&sst)[i];
     }
 }
 
