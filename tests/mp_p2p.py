@@ -1,4 +1,5 @@
-"""Multi-process runner for the p2p transport tests: P OS processes on ONE GPU, each a rank
+"""Multi-process runner for the transport tests (p2p: P OS processes on ONE GPU; NCCL: one
+GPU per rank, tests/test_gpu_nccl_multi.py).  p2p: P OS processes on ONE GPU, each a rank
 with its own CUDA context (one process per rank -- the deployment shape), mailboxes mapped
 through CUDA IPC (bcgs_p2p_handle / bcgs_p2p_connect), records exchanged over gloo.  The
 contexts time-slice on the shared GPU, so the device-side waits are slow but the protocol
@@ -12,14 +13,22 @@ def _worker(rank, world, port, job, q):
     import torch
     import torch.distributed as dist
     from paper_2503_08935_b200 import bcgs
-    torch.cuda.set_device(0)
+    # job["transport"] == "nccl": one GPU per rank (NCCL refuses two ranks on one device)
+    nccl = job.get("transport", "p2p") == "nccl"
+    dev = rank if nccl else 0
+    torch.cuda.set_device(dev)
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     try:
         n3 = job["n3"]
         h = si.unit_cube_h(n3[0])
-        s = bcgs.Solver(n3, h, rank=rank, nranks=world, transport="p2p", device=0)
-        bcgs.connect_p2p(s)
+        if nccl:
+            uid = [bcgs.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            s = bcgs.Solver(n3, h, rank=rank, nranks=world, nccl_id=uid[0], device=dev)
+        else:
+            s = bcgs.Solver(n3, h, rank=rank, nranks=world, transport="p2p", device=0)
+            bcgs.connect_p2p(s)
         s.set_option(bcgs.OPT_COMM_TIMEOUT, 120)
         for opt, val in job.get("options", {}).items():
             s.set_option(getattr(bcgs, opt), val)
