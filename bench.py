@@ -361,11 +361,13 @@ def main():
                 "timing": "average launch duration from CUDA events on the launching stream over "
                           "a second timed pass of K iterations (pass B)"}
         if dom_name in ("fused_p_cheb", "fused_s_cheb"):
-            roof["limiter"] = ("L1/shared-memory throughput (ncu l1tex 79.5 % / 75.2 % of peak "
-                               "for the p / s kernels, FP64 pipe 41 %, 24 warps per SM at the "
-                               "80-register cap: profiles/round2_ncu_full_r2a.txt, DESIGN.md "
-                               "§4); the HBM fraction is reported against the kernel's "
-                               "compulsory bytes")
+            roof["limiter"] = ("L1/shared-memory throughput and FP64 dependency latency per "
+                               "z-step (ncu l1tex 80 % / 75 % of peak for the p / s kernels, "
+                               "issue slots 54 %, FP64 pipe 42 %, 24 warps per SM at the "
+                               "80-register cap: profiles/round2b_ncu_full.txt; a layout with "
+                               "26 % fewer shared wavefronts but 12 warps was slower: "
+                               "profiles/round2b_ncu_xpair_512.txt, DESIGN.md §4, §8); the HBM "
+                               "fraction is reported against the kernel's compulsory bytes")
         if dom_name in FLOPS_PER_PT:
             # the temporally blocked Chebyshev kernels are FP64-ALU heavy: report that roof too
             fl = FLOPS_PER_PT[dom_name](k) * pts_local
