@@ -51,7 +51,7 @@ def main():
                     help="BCGS_OPT_STENCIL values to compare (1 = auto chunk, >= 2 planes per CTA)")
     ap.add_argument("--schedule", default="0",
                     help="BCGS_OPT_TB_SCHEDULE values (0 auto, 1 chunk grid, 2 segments)")
-    ap.add_argument("--pdl", default="1", help="BCGS_OPT_PDL values")
+    ap.add_argument("--pdl", default="0", help="BCGS_OPT_PDL values (library default 0)")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -78,7 +78,7 @@ def main():
         kt = s.kernel_times()
         rep = s.finish()
         assert rep["iterations"] == a.warmup + 2 * a.steps, rep
-        if t1 is None and P == 1 and sv == 1 and sched == 0 and pdl == 1:
+        if t1 is None and P == 1 and sv == 1 and sched == 0 and pdl == 0:
             t1 = ms
         pts = n * n * L
         gbs = 200.0 * pts / (ms * 1e-3) / 1e9
