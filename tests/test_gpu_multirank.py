@@ -23,7 +23,7 @@ def bc():
     return bcgs
 
 
-def run_group(bc, n3, h, P, pc, k, kernels, tol=1e-8, fixed=0, rhs=None):
+def run_group(bc, n3, h, P, pc, k, kernels, tol=1e-8, fixed=0, rhs=None, options=None):
     grp = bc.local_group(n3, h, P)
     L = n3[2] // P
     reps = [None] * P
@@ -33,6 +33,8 @@ def run_group(bc, n3, h, P, pc, k, kernels, tol=1e-8, fixed=0, rhs=None):
         try:
             s = grp[r]
             s.set_option(bc.OPT_KERNELS, kernels)
+            for opt, val in (options or {}).items():
+                s.set_option(getattr(bc, opt), val)
             s.set_preconditioner(pc, k)
             if rhs is None:
                 s.set_rhs_random(si.SEED)
@@ -68,6 +70,22 @@ def test_local_group_matches_oracle(bc, orc, P, n3, pc, k, kernels):
     for rep, hist in zip(reps, hists):
         assert rep["iterations"] == o.iterations
         assert np.array_equal(hist, o.history)        # identical scalars on every rank
+    assert np.array_equal(x, o.x)
+
+
+@pytest.mark.parametrize("options", [{"OPT_TB_SCHEDULE": 2}, {"OPT_STENCIL": 5},
+                                     {"OPT_STENCIL": 4, "OPT_TB_SCHEDULE": 2}])
+def test_local_group_schedules_match_oracle(bc, orc, options):
+    """Ranks running the segment schedule of the Chebyshev kernel and short stencil chunks
+    (the interior launch of the halo-overlapped stencil, planes 1..L-2, in 4- / 5-plane
+    chunks) -- bitwise the oracle's P-slab iterates."""
+    n3, P = (70, 52, 48), 2
+    h = si.unit_cube_h(n3[0])
+    reps, x, hists = run_group(bc, n3, h, P, "gnocomm", 4, 1, options=options)
+    o = orc.bicgstab(orc.rhs_random(n3[::-1], si.SEED), h, pc="gnocomm", k=4, nslab=P, tol=1e-8)
+    for rep, hist in zip(reps, hists):
+        assert rep["iterations"] == o.iterations
+        assert np.array_equal(hist, o.history)
     assert np.array_equal(x, o.x)
 
 

@@ -370,6 +370,25 @@ def test_pdl_launch_chain_bitwise(bc, orc, n3, bpr):
     s.close()
 
 
+@pytest.mark.parametrize("zc", [4, 5, 13, 64])
+def test_stencil_chunk_lengths_bitwise(bc, orc, zc):
+    """The TMA stencil+dot with forced chunk lengths (BCGS_OPT_STENCIL = planes per CTA;
+    ragged last chunks, chunks longer than the block) -- iterates bitwise the oracle's."""
+    n3 = (96, 80, 70)
+    h = si.unit_cube_h(n3[0])
+    s = bc.Solver(n3, h)
+    s.set_option(bc.OPT_STENCIL, zc)
+    s.set_preconditioner("gnocomm", 4, blocks_per_rank=2)
+    s.set_rhs_random(si.SEED)
+    rep = s.solve(fixed_iters=10)
+    o = orc.bicgstab(orc.rhs_random(n3[::-1], si.SEED), h, pc="gnocomm", k=4, nslab=2,
+                     fixed_it=10)
+    assert rep["iterations"] == o.iterations == 10
+    assert np.array_equal(s.residual_history(), o.history)
+    assert np.array_equal(host(s.solution()), o.x)
+    s.close()
+
+
 def test_c2_256_segment_schedule_bitwise(bc, orc):
     """Config C2 (256³, k = 4, one GPU) runs the segment schedule by default (77 tiles on 148
     SMs); first 5 iterations bitwise equal to the oracle's."""
