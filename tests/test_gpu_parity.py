@@ -90,9 +90,9 @@ def test_dot_equals_oracle(bc, orc, n):
 # --------------------------------------------------------------------------- whole solves
 
 def compare_solve(bc, orc, n, pc="gnocomm", k=4, bpr=1, kernels=1, tol=1e-8, fixed=0,
-                  rhs=None, max_it=5000):
+                  rhs=None, max_it=5000, c_min=10.0):
     s, n3, h = make(bc, n, kernels=kernels)
-    s.set_preconditioner(pc, k, blocks_per_rank=bpr)
+    s.set_preconditioner(pc, k, c_min=c_min, blocks_per_rank=bpr)
     if rhs is None:
         s.set_rhs_random(si.SEED)
         b = orc.rhs_random(n3[::-1], si.SEED)
@@ -103,7 +103,8 @@ def compare_solve(bc, orc, n, pc="gnocomm", k=4, bpr=1, kernels=1, tol=1e-8, fix
     g_hist = s.residual_history()
     g_scal = s.scalar_history()
     g_x = host(s.solution())
-    o = orc.bicgstab(b, h, pc=pc, k=k, nslab=bpr, tol=tol, max_it=max_it, fixed_it=fixed)
+    o = orc.bicgstab(b, h, pc=pc, k=k, nslab=bpr, tol=tol, max_it=max_it, fixed_it=fixed,
+                     c_min=c_min)
     return rep, g_hist, g_scal, g_x, o
 
 
@@ -140,6 +141,31 @@ def test_c1_mms_polyexp_unpreconditioned(bc, orc):
                                         (64, "gnocomm", 8, 1)])
 def test_solve_parity(bc, orc, n, pc, k, bpr, kernels):
     assert_parity(*compare_solve(bc, orc, n, pc, k, bpr, kernels))
+
+
+@pytest.mark.parametrize("n,pc,k,bpr", [((1, 1, 1), "none", 0, 1), ((2, 1, 3), "gnocomm", 2, 1),
+                                        ((3, 5, 1), "none", 0, 1), ((1, 7, 2), "bj", 3, 2),
+                                        ((5, 4, 3), "gnocomm", 4, 3), ((2, 2, 9), "gnocomm", 4, 3),
+                                        ((66, 1, 1), "gnocomm", 4, 1), ((2, 130, 2), "gnocomm", 3, 1)])
+def test_solve_parity_degenerate_grids(bc, orc, n, pc, k, bpr):
+    """Degenerate extents: a single unknown, one-plane slabs and blocks, 1-point lines along
+    each axis, slab blocks thinner than the degree (R24 warning case), odd / even nx --
+    every kernel family's edge handling (TMA boxes larger than the grid, one-tile grids,
+    the stencil chunk model at 1-3 planes), bitwise vs the oracle.  GNoComm with c_min = 1:
+    these spectra are narrower than R9's default rescaling c_min / c_max ~ 10 (next test)."""
+    assert_parity(*compare_solve(bc, orc, n, pc, k, bpr, 1, c_min=1.0))
+
+
+@pytest.mark.parametrize("n", [(1, 1, 1), (66, 1, 1)])
+def test_narrow_spectrum_rejects_default_rescaling(bc, orc, n):
+    """R9: a' = c_min λmin, b' = c_max λmax is empty when λmax / λmin < c_min / c_max -- the
+    library refuses with BCGS_E_SPECTRUM, as the oracle's interval is empty too."""
+    s, n3, h = make(bc, n)
+    a, b = orc.pc_interval(n3[::-1], h, 1, "gnocomm")
+    assert not a < b
+    with pytest.raises(bc.BcgsError, match="spectrum"):
+        s.set_preconditioner("gnocomm", 4)
+    s.close()
 
 
 @pytest.mark.parametrize("kernels", KERNELS)
