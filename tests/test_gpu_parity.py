@@ -156,6 +156,43 @@ def test_solve_parity_degenerate_grids(bc, orc, n, pc, k, bpr):
     assert_parity(*compare_solve(bc, orc, n, pc, k, bpr, 1, c_min=1.0))
 
 
+def _random_configs(count, seed=20251018):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        n3 = tuple(int(rng.integers(1, 5)) if rng.random() < 0.25 else int(rng.integers(5, 72))
+                   for _ in range(3))
+        pc = ["gnocomm", "bj", "g", "none"][int(rng.integers(0, 4))]
+        k = 0 if pc == "none" else int(rng.integers(1, 9))
+        bpr = int(rng.choice([d for d in range(1, 5) if n3[2] % d == 0]))
+        if pc == "g":
+            bpr = 1
+        out.append((n3, pc, k, bpr))
+    return out
+
+
+@pytest.mark.parametrize("n3,pc,k,bpr", _random_configs(24))
+def test_random_configs_fixed_iterations_bitwise(bc, orc, n3, pc, k, bpr):
+    """Seeded random extents (1..71 per axis, a quarter of them 1..4; odd and even nx),
+    preconditioners, degrees 1-8 and block counts: 6 fixed iterations bitwise vs the oracle
+    (c_min = 1 keeps every rescaled interval non-empty)."""
+    s, _, h = make(bc, n3)
+    try:
+        s.set_preconditioner(pc, k, c_min=1.0, blocks_per_rank=bpr)
+    except bc.BcgsError as ex:   # a spectrum with a single eigenvalue (all axes of length 1)
+        a, b = orc.pc_interval(n3[::-1], h, bpr, pc, c_min=1.0)
+        assert "spectrum" in str(ex) and not a < b
+        return
+    s.set_rhs_random(si.SEED)
+    rep = s.solve(fixed_iters=6)
+    o = orc.bicgstab(orc.rhs_random(n3[::-1], si.SEED), h, pc=pc, k=k, nslab=bpr, fixed_it=6,
+                     c_min=1.0)
+    assert rep["iterations"] == o.iterations
+    assert np.array_equal(s.residual_history(), o.history)
+    assert np.array_equal(host(s.solution()), o.x)
+    s.close()
+
+
 @pytest.mark.parametrize("n", [(1, 1, 1), (66, 1, 1)])
 def test_narrow_spectrum_rejects_default_rescaling(bc, orc, n):
     """R9: a' = c_min λmin, b' = c_max λmax is empty when λmax / λmin < c_min / c_max -- the
