@@ -293,6 +293,7 @@ def main():
     ms_iter_prof = timed(args.steps, 1)
     clk = clocks.stop()
     ktimes = s.kernel_times()
+    phases = s.phase_times()     # SPEC S:382 phase keys, pass B
     s.set_option(bcgs.OPT_PROFILE, 0)
     rep = s.finish()
     # every enqueued iteration must have run: after a breakdown the remaining iterations are
@@ -420,6 +421,7 @@ def main():
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "comm": comm,
             "kernel_ms_per_step": {kk: v["ms"] / args.steps for kk, v in ktimes.items()},
+            "phase_ms_per_step": {kk: v / args.steps for kk, v in phases.items()},
             "ms_per_step_profiled_pass": ms_iter_prof,
             "clocks": clk, "report": {kk: rep[kk] for kk in ("iterations", "rel_residual",
                                                              "true_rel_residual")},

@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define BCGS_ABI_VERSION 5
+#define BCGS_ABI_VERSION 6
 #define BCGS_MAX_DEGREE 64       /* Chebyshev degree k (sweeps per application) cap      */
 #define BCGS_HIST_CAP 16384      /* max outer iterations recorded per solve              */
 
@@ -317,6 +317,20 @@ bcgs_status bcgs_dot(bcgs_ctx ctx, const double* d_a, const double* d_b, double*
 int32_t bcgs_kernel_times(bcgs_ctx ctx, char* names_out, int32_t names_cap, double* ms_out,
                           int64_t* calls_out, double* bytes_out, int32_t cap);
 void bcgs_kernel_times_reset(bcgs_ctx ctx);
+
+/* The same timings grouped into the SPEC's six phase keys (in this order):
+ * [0] "preconditioner"  (a2 / a7: the Chebyshev kernels -- the fused ones also carry the
+ *                        p / s vector updates a14 / a6 -- and reference sweeps)
+ * [1] "halo_exchange"   (a3 / a8 on the comm stream; overlaps the interior stencil)
+ * [2] "allreduce"       (a5 / a10 / a13: finalize, all-gather, scalar step)
+ * [3] "stencil_kernels" (a4 / a9: stencil + dot)
+ * [4] "vector_kernels"  (a6, a11, a12, a14 when not fused into the preconditioner)
+ * [5] "total"           (sum of [0..4]; [1] overlaps [3], so this exceeds wall time)
+ * host_out6[i] = milliseconds accumulated while BCGS_OPT_PROFILE = 1 (zeros otherwise).
+ * With BCGS_OPT_PROFILE = 1 every timed launch is also wrapped in an NVTX range
+ * "<phase key>/<kernel class>" (visible to nsys / ncu --nvtx; no-ops without a tool).
+ * BCGS_E_INVALID for a null context or output. */
+bcgs_status bcgs_get_phase_times(bcgs_ctx ctx, double* host_out6);
 
 #ifdef __cplusplus
 }

@@ -41,8 +41,13 @@ EXPORTS = [
     "bcgs_apply_operator", "bcgs_apply_preconditioner", "bcgs_dot", "bcgs_kernel_times",
     "bcgs_kernel_times_reset", "bcgs_set_inner_solver", "bcgs_inner_iterations",
     "bcgs_exact_dots", "bcgs_certification_info", "bcgs_create_p2p", "bcgs_p2p_handle", "bcgs_p2p_connect",
-    "bcgs_create_local_p2p",
+    "bcgs_create_local_p2p", "bcgs_get_phase_times",
 ]
+
+
+# SPEC S:382 phase keys, in bcgs_get_phase_times order
+PHASE_KEYS = ("preconditioner", "halo_exchange", "allreduce", "stencil_kernels",
+              "vector_kernels", "total")
 
 
 class BcgsError(RuntimeError):
@@ -115,6 +120,7 @@ def load() -> ctypes.CDLL:
         "bcgs_dot": (i32, [P, P, P, P]),
         "bcgs_kernel_times": (i32, [P, ctypes.c_char_p, i32, P, P, P, i32]),
         "bcgs_kernel_times_reset": (None, [P]),
+        "bcgs_get_phase_times": (i32, [P, P]),
         "bcgs_set_inner_solver": (i32, [P, f64, i32]),
         "bcgs_inner_iterations": (i64, [P]),
         "bcgs_exact_dots": (ctypes.c_int32, [P]),
@@ -379,6 +385,13 @@ class Solver:
 
     def kernel_times_reset(self):
         self.lib.bcgs_kernel_times_reset(self.ctx)
+
+    def phase_times(self) -> dict:
+        """Milliseconds per SPEC phase key accumulated while OPT_PROFILE = 1."""
+        out = np.zeros(6)
+        self._check(self.lib.bcgs_get_phase_times(self.ctx, out.ctypes.data),
+                    "bcgs_get_phase_times")
+        return dict(zip(PHASE_KEYS, (float(v) for v in out)))
 
 
 def connect_p2p(solver: "Solver", group=None):

@@ -6,6 +6,7 @@
 // Built with --fmad=false (R17): no FMA contraction in any kernel; fma() appears only in
 // Dot2's TwoProd (dd.cuh).
 #include "ctx.cuh"
+#include <nvtx3/nvToolsExt.h>
 #include "k_ref.cuh"
 #include "k_stream.cuh"
 #include "pipe.cuh"
@@ -67,11 +68,16 @@ struct Prof {
         if (c->profile) {
             a = get_ev(c);
             cudaEventRecord(a, s);
+            // "<S:382 phase key>/<kernel class>" (host range around the launch)
+            char name[64];
+            snprintf(name, sizeof name, "%s/%s", kPhaseName[kc_phase(cls)], kClassName[cls]);
+            nvtxRangePushA(name);
         }
     }
     ~Prof()
     {
         if (c->profile) {
+            nvtxRangePop();
             cudaEvent_t b = get_ev(c);
             cudaEventRecord(b, s);
             c->pending.push_back({cls, a, b, bytes});
@@ -1657,6 +1663,18 @@ int32_t bcgs_kernel_times(bcgs_ctx c, char* names_out, int32_t names_cap, double
         names_out[names_cap - 1] = 0;
     }
     return m;
+}
+
+bcgs_status bcgs_get_phase_times(bcgs_ctx c, double* host_out6)
+{
+    if (!c || !host_out6) return BCGS_E_INVALID;
+    harvest(c);
+    for (int p = 0; p <= PH_COUNT; ++p) host_out6[p] = 0.0;
+    for (int i = 0; i < KC_COUNT; ++i) {
+        host_out6[kc_phase(i)] += c->ktime[i];
+        host_out6[PH_COUNT] += c->ktime[i];
+    }
+    return BCGS_OK;
 }
 
 void bcgs_kernel_times_reset(bcgs_ctx c)

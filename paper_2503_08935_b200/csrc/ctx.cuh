@@ -38,6 +38,22 @@ enum KClass {
 inline const char* kClassName[KC_COUNT] = {
     "precond_sweep", "stencil_dot1", "axpy_s", "stencil_dot2", "update_xr", "update_p",
     "finalize", "halo", "allgather", "scalars", "fused_p_cheb", "fused_s_cheb", "fused_xr"};
+// SPEC S:382 phase keys and the phase of each kernel class (bcgs_get_phase_times, NVTX)
+constexpr int PH_PRECOND = 0, PH_HALO = 1, PH_ALLREDUCE = 2, PH_STENCIL = 3, PH_VECTOR = 4,
+              PH_COUNT = 5;
+inline const char* kPhaseName[PH_COUNT + 1] = {"preconditioner", "halo_exchange", "allreduce",
+                                                "stencil_kernels", "vector_kernels", "total"};
+inline int kc_phase(int kc)
+{
+    switch (kc) {
+    case KC_PRECOND: case KC_FUSED_P1: case KC_FUSED_P2: return PH_PRECOND;
+    case KC_HALO: return PH_HALO;
+    case KC_FINALIZE: case KC_ALLGATHER: case KC_SCALARS: return PH_ALLREDUCE;
+    case KC_STENCIL1: case KC_STENCIL2: return PH_STENCIL;
+    default: return PH_VECTOR;   // KC_AXPY, KC_UPDATE_XR, KC_UPDATE_P, KC_FUSED_XR
+    }
+}
+
 
 inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 

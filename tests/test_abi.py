@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_status_strings():
     lib = bcgs.load()
-    assert lib.bcgs_abi_version() == 5
+    assert lib.bcgs_abi_version() == 6
     assert lib.bcgs_status_string(7) == b"breakdown"
 
 

@@ -485,6 +485,27 @@ def test_unpreconditioned_streaming_path(bc, orc):
     s.close()
 
 
+def test_phase_times_spec_keys(bc):
+    """bcgs_get_phase_times: the SPEC's six phase keys from the profiled kernels --
+    every phase of a one-rank fused iteration but the halo is timed, total = their sum."""
+    s, n3, h = make(bc, 64, pc="gnocomm", degree=4)
+    s.set_rhs_random(si.SEED)
+    s.set_option(bc.OPT_PROFILE, 1)
+    s.kernel_times_reset()
+    s.solve(fixed_iters=5)
+    ph = s.phase_times()
+    assert tuple(ph) == bc.PHASE_KEYS
+    for key in ("preconditioner", "allreduce", "stencil_kernels", "vector_kernels"):
+        assert ph[key] > 0, (key, ph)
+    assert ph["halo_exchange"] == 0.0
+    parts = sum(v for k, v in ph.items() if k != "total")
+    assert ph["total"] == pytest.approx(parts, rel=1e-12)
+    kt = s.kernel_times()
+    assert ph["preconditioner"] == pytest.approx(kt["fused_p_cheb"]["ms"] + kt["fused_s_cheb"]["ms"],
+                                                 rel=1e-12)
+    s.close()
+
+
 def test_schedule_and_stencil_options_validated(bc):
     """BCGS_OPT_TB_SCHEDULE takes 0..2, BCGS_OPT_STENCIL 0..4096 (>= 2: planes per CTA)."""
     s, n3, h = make(bc, 16, pc="gnocomm", degree=2)
