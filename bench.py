@@ -126,6 +126,22 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def ncu_bytes_per_pt(n, world, k, args):
+    """Measured DRAM bytes per grid point per iteration: the committed ncu
+    capture's dram read + write of the iteration's five kernels at 512^3 (one rank, the
+    default fused GNoComm k = 4 path), divided by the points; None for other workloads."""
+    if (n, world, k, args.pc, args.kernels) != (512, 1, 4, "gnocomm", 1) or args.sync2 or \
+            args.pipelined:
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        keys = ["fused_p_cheb", "stencil_dot1", "fused_s_cheb", "stencil_dot2", "fused_xr"]
+        return sum(tr[f"{kk}@512"] for kk in keys) / float(512 ** 3)
+    except Exception:
+        return None
+
+
 def max_over_ranks(value: float, dist=None, device=None) -> float:
     """Max of a per-rank float over all ranks (timings are reported as the slowest rank)."""
     if dist is None or not dist.is_available() or not dist.is_initialized() \
@@ -417,7 +433,8 @@ def main():
             "gdof_s": gdof,
             "iteration_roofline": {"alg_bytes_per_pt": alg_bpp,
                                    "achieved_gbs": iter_gbs, "peak_gbs": peak,
-                                   "frac": iter_gbs / peak},
+                                   "frac": iter_gbs / peak,
+                                   "ncu_bytes_per_pt": ncu_bytes_per_pt(n, world, k, args)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "comm": comm,
             "kernel_ms_per_step": {kk: v["ms"] / args.steps for kk, v in ktimes.items()},
