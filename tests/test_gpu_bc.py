@@ -188,3 +188,39 @@ def test_bc_config_errors(bc):
     s = bc.Solver((8, 8, 8), 0.1, bc=(0, 0, 0, 0, 1, 0))
     with pytest.raises(bc.BcgsError):
         s.set_preconditioner("gnocomm", 2, blocks_per_rank=8)   # 1-plane block at a z face
+
+
+def _random_bc_configs(count, seed=20251019):
+    """Seeded mixed-face configurations: each face Dirichlet or Neumann (never all six
+    Neumann: singular), extents >= 2 along a Neumann axis and >= 2 planes per block with a
+    Neumann z face (R27), odd and even nx, every preconditioner kind."""
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        faces = tuple(int(v) for v in rng.integers(0, 2, size=6))
+        if sum(faces) == 6:
+            continue
+        n3 = [int(rng.integers(2, 48)) for _ in range(3)]
+        pc = ["gnocomm", "bj", "g", "none"][int(rng.integers(0, 4))]
+        k = 0 if pc == "none" else int(rng.integers(1, 9))
+        divs = [d for d in range(1, 5) if n3[2] % d == 0 and n3[2] // d >= 2]
+        bpr = 1 if pc == "g" else int(rng.choice(divs))
+        out.append((tuple(n3), faces, pc, k, bpr))
+    return out
+
+
+@pytest.mark.parametrize("n3,faces,pc,k,bpr", _random_bc_configs(16))
+def test_random_bc_configs_bitwise(bc, orc, n3, faces, pc, k, bpr):
+    """Seeded random mixed Dirichlet / Neumann problems: 6 fixed iterations bitwise vs the
+    oracle (mirror ghosts in every kernel family, mixed Chebyshev intervals, c_min = 1)."""
+    h = 0.09
+    s = bc.Solver(n3, h, bc=faces)
+    s.set_preconditioner(pc, k, c_min=1.0, blocks_per_rank=bpr)
+    b = orc.rhs_random(n3[::-1], si.SEED)
+    s.set_rhs(dev(b))
+    rep = s.solve(fixed_iters=6)
+    o = orc.bicgstab(b, h, pc=pc, k=k, nslab=bpr, fixed_it=6, bc=faces, c_min=1.0)
+    assert rep["iterations"] == o.iterations
+    assert np.array_equal(s.residual_history(), o.history)
+    assert np.array_equal(host(s.solution()), o.x)
+    s.close()
