@@ -142,8 +142,9 @@ typedef enum {
     BCGS_OPT_STENCIL = 14      /* stencil+dot kernels of a4 / a9: 1 = TMA-staged z-march  */
                                /* (default; Dirichlet faces, even nx; planes per CTA from */
                                /* a wave cost model), v >= 2 = TMA with v planes per CTA  */
-                               /* (>= 4; measurement), 0 = L1-cached z-march.  Bitwise the */
-                               /* same results; values outside 0..4096: BCGS_E_INVALID    */
+                               /* (clamped to 4..64; measurement), 0 = L1-cached z-march. */
+                               /* Bitwise the same results; values outside 0..64:         */
+                               /* BCGS_E_INVALID (64 bounds the certified dot chains)     */
 } bcgs_option;
 
 /* Boundary condition kind of a physical face (Eq. 4 / Eq. 5). */

@@ -396,7 +396,10 @@ inline int ew_depth(int64_t n)
     const int64_t T = (int64_t)kEwBlocks * 256;
     return (int)(2 * ((n + T - 1) / T + 2));
 }
-constexpr int kStencilDepth = 2 * 2 * stream::SZC;   // 2 points per plane and chain
+// per-thread dot chains of the stencil kernels: 2 products per plane and chain over <= 64
+// planes (TMA stencil: 2 rows x st::ZC_MAX; L1 stencil: 2 x 2 x SZC), + 1 for the chain merge
+constexpr int kStencilDepth = 2 * 2 * stream::SZC + 2;
+static_assert(2 * 64 + 1 <= kStencilDepth, "TMA stencil chunk cap (st_tma.cu ZC_MAX)");
 
 // Reduce `nparts` partial triples of ND dots, then complete the stage (certified) or park it
 // for the exact path.  src = the ND operand pairs (a_d, b_d), recorded for that path.
@@ -1219,7 +1222,9 @@ bcgs_status bcgs_set_option(bcgs_ctx c, int32_t option, int64_t value)
         c->tb_schedule = (int)value;
         break;
     case BCGS_OPT_STENCIL:
-        if (value < 0 || value > 4096) return fail(c, BCGS_E_INVALID, "stencil option %lld", (long long)value);
+        // planes per CTA <= 64: the certification bound of the stencil dots (kStencilDepth,
+        // R19) covers per-thread chains of 2 products per plane over at most 64 planes
+        if (value < 0 || value > 64) return fail(c, BCGS_E_INVALID, "stencil option %lld: 0..64", (long long)value);
         c->stencil_tma = (int)value;
         break;
     case BCGS_OPT_PIPELINED:   // allocate now (an allocation synchronises the device)

@@ -25,6 +25,8 @@ constexpr int SLOT = VSZ + ASZ;
 constexpr int SMEM = NS * SLOT + 128;
 constexpr int ZC = 32;                      // planes per CTA (chunk) on deep slabs
 constexpr int ZC_MIN = 4;                   // partial-slot capacity (ctx.cuh max_blocks)
+constexpr int ZC_MAX = 64;                  // dot chains of 2 RY-row products per plane must
+                                            // stay within kStencilDepth = 128 (bcgs_api.cu, R19)
 }  // namespace st
 
 struct StMaps {
@@ -158,7 +160,7 @@ bool stencil_tma_ok(bcgs_ctx c)
 static int stencil_zc(bcgs_ctx c, int tiles, int planes)
 {
     using namespace st;
-    if (c->stencil_tma >= 2) return std::max(ZC_MIN, c->stencil_tma);
+    if (c->stencil_tma >= 2) return std::min(ZC_MAX, std::max(ZC_MIN, c->stencil_tma));
     const int64_t slots = (int64_t)kNumSMs * 3;
     const int64_t deep = (int64_t)tiles * ((planes + ZC - 1) / ZC);
     if (deep >= 4 * slots) return ZC;

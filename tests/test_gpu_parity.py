@@ -507,10 +507,11 @@ def test_phase_times_spec_keys(bc):
 
 
 def test_schedule_and_stencil_options_validated(bc):
-    """BCGS_OPT_TB_SCHEDULE takes 0..2, BCGS_OPT_STENCIL 0..4096 (>= 2: planes per CTA)."""
+    """BCGS_OPT_TB_SCHEDULE takes 0..2, BCGS_OPT_STENCIL 0..64 (>= 2: planes per CTA; 64 keeps
+    the stencil dots' per-thread chains inside the certification depth, R19)."""
     s, n3, h = make(bc, 16, pc="gnocomm", degree=2)
     for opt, bad in ((bc.OPT_TB_SCHEDULE, 3), (bc.OPT_TB_SCHEDULE, -1), (bc.OPT_STENCIL, -1),
-                     (bc.OPT_STENCIL, 5000)):
+                     (bc.OPT_STENCIL, 65), (bc.OPT_STENCIL, 5000)):
         with pytest.raises(bc.BcgsError):
             s.set_option(opt, bad)
     for opt, good in ((bc.OPT_TB_SCHEDULE, 1), (bc.OPT_STENCIL, 2), (bc.OPT_STENCIL, 0)):
